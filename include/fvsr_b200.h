@@ -1,0 +1,203 @@
+/*
+ * fvsr_b200.h — C-ABI of the B200-native FlashVSR block-sparse streaming attention.
+ *
+ * This is the drop-in boundary for the reference's hot-path operator API
+ * (P = /root/reference/proj):
+ *
+ *   fvsr_plan_sparse            replaces vsr::plan_sparse            P/include/vsr/sparse.hpp:45-52
+ *                                                                     (P/src/sparse.cpp:72-139)
+ *   fvsr_sparse_attention_exec  replaces vsr::sparse_attention_exec  P/include/vsr/sparse.hpp:59-64
+ *                                                                     (P/src/sparse.cpp:208-254)
+ *   fvsr_sparsity_report        replaces vsr::sparsity_report        P/include/vsr/sparse.hpp:66
+ *   fvsr_ring_*                 replace vsr::KVCache append / sliding evict / frames and the
+ *                               per-step concat_rows context assembly
+ *                               P/include/vsr/kv_cache.hpp:27-73, P/src/kv_cache.cpp:39-106,
+ *                               P/src/stream.cpp:154-164,244-249
+ *   fvsr_ring_attention         replaces head_attention for every head of one layer
+ *                               P/src/stream.cpp:175-194 (called at :251)
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Tensors are bf16 bit patterns (uint16_t) in DEVICE
+ *     memory unless a name ends in _host.  Token order is the reference's TokenGrid order:
+ *     frame-major, then row-major inside a frame (P/include/vsr/grid.hpp:17-20).
+ *   - Multi-head tensors are head-major: q is [heads][Lq][d], k/v are [heads][Lk][d].
+ *   - Every call is stream-ordered on the cudaStream_t passed in (NULL = legacy default
+ *     stream) and never allocates device memory once the context's workspace has grown to
+ *     the largest shape seen.  Different streams are independent, which replaces the
+ *     reference's `threads` argument (P/src/sparse.cpp:229-253).
+ *   - Errors: every entry point returns an fvsr_status.  Host-detectable contract
+ *     violations are returned immediately, mirroring the reference's VSR_REQUIRE checks
+ *     (same exception taxonomy, P/include/vsr/common.hpp:10-48).  Data-dependent errors
+ *     found on the device (non-finite pooled values -> SHAPE, a softmax row with no
+ *     reachable key -> DEGENERATE) are latched in the context's device error word and
+ *     reported by fvsr_check_errors() (which synchronizes the stream), or immediately by
+ *     any call made with FVSR_FLAG_SYNC_CHECK.
+ *   - fvsr_last_error() returns a thread-local message for the last failing call.
+ *   - There is no CPU fallback: without a usable sm_100 device every compute entry point
+ *     returns FVSR_E_CUDA.
+ */
+#ifndef FVSR_B200_H
+#define FVSR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FVSR_API __attribute__((visibility("default")))
+#else
+#define FVSR_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FVSR_ABI_VERSION 1
+
+typedef struct CUstream_st* fvsr_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  FVSR_OK = 0,
+  FVSR_E_SHAPE = 1,       /* vsr::ShapeError */
+  FVSR_E_CONFIG = 2,      /* vsr::ConfigError */
+  FVSR_E_DEGENERATE = 3,  /* vsr::DegenerateRowError */
+  FVSR_E_EMPTY_BLOCK = 4, /* vsr::EmptyBlockError */
+  FVSR_E_INVARIANT = 5,   /* vsr::InvariantError */
+  FVSR_E_CUDA = 6,        /* CUDA runtime / no sm_100 device */
+  FVSR_E_NOMEM = 8        /* device allocation failed */
+} fvsr_status;
+
+/* Token grid: absolute, strictly increasing frame ids (HOST array) over rows x cols.
+ * == vsr::TokenGrid (P/include/vsr/grid.hpp:22-46). */
+typedef struct {
+  const int32_t* frame_ids;
+  int32_t n_frames;
+  int32_t rows;
+  int32_t cols;
+} fvsr_grid;
+
+typedef enum {
+  FVSR_MASK_ALL = 0,      /* MaskMatrix::all_allowed (P/include/vsr/mask.hpp:21-23) */
+  FVSR_MASK_LOCALITY = 1, /* build_locality_mask, analytic on device (P/src/mask.cpp:109-147) */
+  FVSR_MASK_BITMASK = 2   /* explicit MaskMatrix words, DEVICE pointer [Lq][words_per_row] */
+} fvsr_mask_kind;
+
+typedef enum {
+  FVSR_LOCALITY_PRESERVED = 0, /* LocalityWindow::Mode::boundary_preserved */
+  FVSR_LOCALITY_TRUNCATED = 1  /* LocalityWindow::Mode::boundary_truncated */
+} fvsr_locality_mode;
+
+/* Token mask descriptor == vsr::MaskMatrix / vsr::LocalityWindow (P/include/vsr/mask.hpp:16-97).
+ * Locality frame extents are the grid's rows/cols (make_stream_locality, P/src/stream.cpp). */
+typedef struct {
+  int32_t kind;
+  int32_t mode;
+  int32_t extent_h;
+  int32_t extent_w;
+  const uint64_t* bits;  /* FVSR_MASK_BITMASK only */
+  int64_t words_per_row; /* FVSR_MASK_BITMASK only: (Lk + 63) / 64 */
+} fvsr_mask;
+
+enum { FVSR_FLAG_SYNC_CHECK = 1 };
+
+typedef struct fvsr_ctx fvsr_ctx;
+typedef struct fvsr_ring fvsr_ring;
+
+/* ---- library / context ------------------------------------------------------------- */
+FVSR_API int32_t fvsr_abi_version(void);
+FVSR_API const char* fvsr_last_error(void);
+/* Binds to the current CUDA device; fails with FVSR_E_CUDA unless it is sm_100. */
+FVSR_API int32_t fvsr_ctx_create(fvsr_ctx** out);
+FVSR_API void fvsr_ctx_destroy(fvsr_ctx* ctx);
+/* Call flags (FVSR_FLAG_SYNC_CHECK) applied to every later call on this context. */
+FVSR_API int32_t fvsr_ctx_set_flags(fvsr_ctx* ctx, int32_t flags);
+/* Synchronizes `stream`, reads and clears the device error word. */
+FVSR_API int32_t fvsr_check_errors(fvsr_ctx* ctx, fvsr_stream_t stream);
+/* Number of kernel launches this context has issued (instrumentation for benches). */
+FVSR_API int64_t fvsr_ctx_launch_count(const fvsr_ctx* ctx);
+
+/* ---- geometry (host only) ----------------------------------------------------------- */
+/* Block counts of partition_blocks(grid_q) / partition_blocks(grid_k) (P/src/partition.cpp:38-62). */
+FVSR_API int32_t fvsr_block_counts(const fvsr_grid* grid_q, const fvsr_grid* grid_k, int32_t* bnq,
+                          int32_t* bnk);
+
+/* ---- drop-in operator API (flat device tensors) ------------------------------------- */
+/* plan_sparse: per head, pool q/k per (2,8,8) block in exact sequential fp32, score block
+ * pairs (sequential dot, no FMA, x 1/sqrt(d)), restrict to coarse-allowed pairs, keep the
+ * top-k with the forced diagonal (ties toward the lower id).  Outputs (DEVICE):
+ *   sel       [heads][bnq][cap]  ascending key-block ids, -1 padded; cap >= min(topk, bnk)
+ *   sel_count [heads][bnq]
+ *   diag      [heads][bnq]       diagonal block or -1 (SparsePlan::diagonal_block)
+ *   coarse    [heads][bnq][bnk]  fp32 coarse scores (SparsePlan::coarse_scores) or NULL
+ *   allowed   [heads][bnq][bnk]  uint8 coarse-allowed (SparsePlan::coarse_allowed) or NULL
+ * Indices are bit-exact with the reference for identical (bf16-representable) inputs. */
+FVSR_API int32_t fvsr_plan_sparse(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k, int32_t heads,
+                         int32_t d, const fvsr_grid* grid_q, const fvsr_grid* grid_k,
+                         const fvsr_mask* mask, int64_t topk, int32_t cap, int32_t* sel,
+                         int32_t* sel_count, int32_t* diag, float* coarse, uint8_t* allowed,
+                         fvsr_stream_t stream);
+
+/* sparse_attention_exec: exact softmax attention restricted to each query block's
+ * selected key blocks and the token mask, tcgen05 tensor cores, fp32 online softmax,
+ * bf16 out [heads][Lq][d].  Rows outside [row_begin, row_end) are written as zeros
+ * (row_end < 0 means "to the end").  d must be 64 or 128. */
+FVSR_API int32_t fvsr_sparse_attention_exec(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k,
+                                   const uint16_t* v, int32_t heads, int32_t d,
+                                   const fvsr_grid* grid_q, const fvsr_grid* grid_k,
+                                   const fvsr_mask* mask, int32_t cap, const int32_t* sel,
+                                   const int32_t* sel_count, float scale, int64_t row_begin,
+                                   int64_t row_end, uint16_t* out, fvsr_stream_t stream);
+
+/* sparsity_report: per head (DEVICE outputs, uint64 [heads]) executed token pairs, dense
+ * (mask-allowed) token pairs, selected and coarse-allowed block pairs.  executed_flops of
+ * the reference == executed_pairs * (2d+2) (P/src/sparse.cpp:268-281). */
+FVSR_API int32_t fvsr_sparsity_report(fvsr_ctx* ctx, int32_t heads, const fvsr_grid* grid_q,
+                             const fvsr_grid* grid_k, const fvsr_mask* mask, int32_t cap,
+                             const int32_t* sel, const int32_t* sel_count,
+                             uint64_t* executed_pairs, uint64_t* dense_pairs,
+                             uint64_t* selected_blocks, uint64_t* allowed_blocks,
+                             fvsr_stream_t stream);
+
+/* ---- device ring-buffer KV cache (streaming) ---------------------------------------- */
+/* window_frames + 1 slots per (layer, head): the current frame is appended before
+ * attention, exactly as step() does (P/src/stream.cpp:228-229; KVCache::validate allows
+ * window + 1, P/src/kv_cache.cpp:144).  K/V live tile-major and pre-swizzled for the
+ * tensor-core kernel; per-frame-tile pooled partial sums are kept so the mask builder never
+ * re-reads cached keys. */
+FVSR_API int32_t fvsr_ring_create(fvsr_ctx* ctx, int32_t layers, int32_t heads, int32_t d, int32_t rows,
+                         int32_t cols, int32_t window_frames, fvsr_ring** out);
+FVSR_API void fvsr_ring_destroy(fvsr_ring* ring);
+/* KVCache::append for every head of `layer`: k, v are [heads][rows*cols][d] (DEVICE). */
+FVSR_API int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer, int32_t frame_id,
+                         const uint16_t* k, const uint16_t* v, fvsr_stream_t stream);
+/* KVCache::evict with the sliding_window strategy (P/src/kv_cache.cpp:100-106). */
+FVSR_API int32_t fvsr_ring_evict_sliding(fvsr_ring* ring, int32_t layer);
+/* KVCache::frame_ids (identical for every head under sliding eviction). */
+FVSR_API int32_t fvsr_ring_frame_ids(const fvsr_ring* ring, int32_t layer, int32_t* ids, int32_t cap,
+                            int32_t* n);
+
+/* head_attention for heads [0, heads) of `layer`: queries of frames q_frame_ids (usually
+ * the current frame) against the ring's context.  q is [heads][nq*rows*cols][d] (DEVICE),
+ * out likewise.  sel/sel_count (DEVICE, optional) receive the plan as fvsr_plan_sparse would.
+ * unit_begin/unit_end restrict the work to a range of (head, q-tile) units, unit =
+ * head * (nq * tiles) + frame * tiles + tile (head-parallel sharding; pass 0, -1 for all);
+ * rows of units outside the range are left untouched. */
+FVSR_API int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer, const uint16_t* q,
+                            const int32_t* q_frame_ids, int32_t nq, const fvsr_mask* mask,
+                            int64_t topk, float scale, int64_t unit_begin, int64_t unit_end,
+                            uint16_t* out, int32_t sel_cap, int32_t* sel, int32_t* sel_count,
+                            fvsr_stream_t stream);
+
+/* One streaming layer-step from HOST buffers (the end-to-end path): H2D copy of the new
+ * frame's q/k/v ([heads][rows*cols][d] bf16; pinned memory recommended), ring append,
+ * sliding evict, attention, D2H copy of out.  Returns after enqueueing; the host output is
+ * valid once `stream` is synchronized. */
+FVSR_API int32_t fvsr_ring_step_host(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer, int32_t frame_id,
+                            const uint16_t* q_host, const uint16_t* k_host,
+                            const uint16_t* v_host, const fvsr_mask* mask, int64_t topk,
+                            float scale, uint16_t* out_host, fvsr_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FVSR_B200_H */

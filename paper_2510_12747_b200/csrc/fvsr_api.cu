@@ -1,0 +1,730 @@
+// fvsr_api.cu — host implementation of the C-ABI declared in include/fvsr_b200.h.
+//
+// One translation unit: the kernels are included below so the library builds with a
+// single nvcc invocation and no relocatable device code.  Host checks mirror the
+// reference's VSR_REQUIRE contracts (P = /root/reference/proj) and return the same
+// exception taxonomy as status codes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/fvsr_b200.h"
+#include "fvsr_common.cuh"
+#include "kernel_attn.cu"
+#include "kernels_plan.cu"
+
+using namespace fvsr;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define FVSR_CUDA(call)                                                                     \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) return fail(FVSR_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define FVSR_TRY(expr)          \
+  do {                          \
+    int st_ = (expr);           \
+    if (st_ != FVSR_OK) return st_; \
+  } while (0)
+
+int status_from_bits(unsigned bits) {
+  for (int code = 1; code < 8; ++code)
+    if (bits & (1u << code)) return code;
+  return FVSR_OK;
+}
+
+const char* device_error_message(int code) {
+  switch (code) {
+    case FVSR_E_SHAPE: return "non-finite pooled value in plan_sparse (matmul finite check, P/src/tensor.cpp:126-127)";
+    case FVSR_E_DEGENERATE: return "sparse_attention_exec: a query row has no allowed keys in its selected blocks";
+    case FVSR_E_INVARIANT: return "selection list out of range or longer than cap";
+    default: return "device error";
+  }
+}
+
+}  // namespace
+
+struct fvsr_ctx {
+  int device = 0;
+  int flags = 0;
+  unsigned* d_err = nullptr;
+  long long launches = 0;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // staging for fvsr_ring_step_host
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+struct fvsr_ring {
+  int layers, heads, d, rows, cols, window, slots, tiles_w, tiles_h, n_tiles;
+  size_t tile_bytes;
+  uint8_t* k = nullptr;
+  uint8_t* v = nullptr;
+  float* s0 = nullptr;
+  float* s1 = nullptr;
+  std::vector<std::vector<std::pair<int, int>>> ctx;  // per layer: (frame_id, slot), ascending
+  std::vector<std::vector<char>> used;                // per layer: slot occupancy
+  long long kv_head_stride() const { return (long long)slots * n_tiles * (long long)tile_bytes; }
+  long long part_head_stride() const { return (long long)slots * n_tiles * d; }
+  uint8_t* k_layer(int l) const { return k + (long long)l * heads * kv_head_stride(); }
+  uint8_t* v_layer(int l) const { return v + (long long)l * heads * kv_head_stride(); }
+  float* s0_layer(int l) const { return s0 + (long long)l * heads * part_head_stride(); }
+  float* s1_layer(int l) const { return s1 + (long long)l * heads * part_head_stride(); }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------------------
+// validation and geometry
+// ---------------------------------------------------------------------------------------
+int check_grid(const fvsr_grid* g, const char* what) {
+  if (!g) return fail(FVSR_E_CONFIG, "%s: null grid", what);
+  // TokenGrid constructor, P/include/vsr/grid.hpp:48-57
+  if (g->n_frames < 1 || g->rows < 1 || g->cols < 1 || !g->frame_ids)
+    return fail(FVSR_E_CONFIG, "TokenGrid: empty extents (%s)", what);
+  if (g->n_frames > kMaxFrames)
+    return fail(FVSR_E_CONFIG, "%s: %d frames exceeds the kernel limit of %d", what, g->n_frames, kMaxFrames);
+  for (int i = 0; i < g->n_frames; ++i) {
+    if (g->frame_ids[i] < 0) return fail(FVSR_E_CONFIG, "TokenGrid: negative frame id");
+    if (i > 0 && g->frame_ids[i] <= g->frame_ids[i - 1])
+      return fail(FVSR_E_CONFIG, "TokenGrid: frame ids must be strictly increasing");
+  }
+  return FVSR_OK;
+}
+
+long long grid_tokens(const fvsr_grid* g) { return (long long)g->n_frames * g->rows * g->cols; }
+
+int build_geom(const fvsr_grid* gq, const fvsr_grid* gk, int d, const int* k_slots, DevGeom& g) {
+  FVSR_TRY(check_grid(gq, "grid_q"));
+  FVSR_TRY(check_grid(gk, "grid_k"));
+  if (gq->rows != gk->rows || gq->cols != gk->cols)
+    return fail(FVSR_E_CONFIG, "query and key grids must share rows/cols (%dx%d vs %dx%d)", gq->rows, gq->cols,
+                gk->rows, gk->cols);
+  std::memset(&g, 0, sizeof(g));
+  g.rows = gq->rows;
+  g.cols = gq->cols;
+  g.tiles_w = (g.cols + 7) / 8;
+  g.tiles_h = (g.rows + 7) / 8;
+  g.n_tiles = g.tiles_w * g.tiles_h;
+  g.d = d;
+  const long long N = (long long)g.rows * g.cols;
+  // temporal rows: consecutive frames sharing frame/2 (kBlockT = 2, P/include/vsr/partition.hpp:11)
+  auto trows = [&](const fvsr_grid* gr, int* first, int* count, int* ftr, int& ntr) {
+    ntr = 0;
+    for (int i = 0; i < gr->n_frames; ++i) {
+      if (i > 0 && gr->frame_ids[i] / 2 == gr->frame_ids[i - 1] / 2) {
+        count[ntr - 1] = 2;
+      } else {
+        first[ntr] = i;
+        count[ntr] = 1;
+        ++ntr;
+      }
+      if (ftr) ftr[i] = ntr - 1;
+    }
+  };
+  trows(gq, g.q_tr_first, g.q_tr_count, g.q_frame_tr, g.nq_trows);
+  trows(gk, g.k_tr_first, g.k_tr_count, nullptr, g.nk_trows);
+  g.nqf = gq->n_frames;
+  g.nkf = gk->n_frames;
+  g.bnq = g.nq_trows * g.n_tiles;
+  g.bnk = g.nk_trows * g.n_tiles;
+  for (int i = 0; i < g.nqf; ++i) g.q_frame_tok0[i] = (int)(i * N);
+  for (int i = 0; i < g.nkf; ++i) {
+    g.k_frame_tok0[i] = (int)(i * N);
+    g.k_slot[i] = k_slots ? k_slots[i] : i;
+  }
+  for (int a = 0; a < g.nq_trows; ++a) {
+    const int key = gq->frame_ids[g.q_tr_first[a]] / 2;
+    g.q_tr_diag[a] = -1;
+    for (int b = 0; b < g.nk_trows; ++b)
+      if (gk->frame_ids[g.k_tr_first[b]] / 2 == key) g.q_tr_diag[a] = b;
+  }
+  if (N * std::max(g.nqf, g.nkf) > (long long)INT32_MAX)
+    return fail(FVSR_E_CONFIG, "grid too large for 32-bit token indices");
+  return FVSR_OK;
+}
+
+int build_mask(const fvsr_mask* m, const DevGeom& g, long long lk, DevMask& dm) {
+  std::memset(&dm, 0, sizeof(dm));
+  dm.frame_h = g.rows;
+  dm.frame_w = g.cols;
+  if (!m || m->kind == FVSR_MASK_ALL) {
+    dm.kind = 0;
+    dm.extent_h = dm.extent_w = 1;
+    return FVSR_OK;
+  }
+  dm.kind = m->kind;
+  dm.mode = m->mode;
+  dm.extent_h = m->extent_h;
+  dm.extent_w = m->extent_w;
+  if (m->kind == FVSR_MASK_LOCALITY) {
+    // build_locality_mask, P/src/mask.cpp:113-116
+    if (m->extent_h < 1 || m->extent_w < 1) return fail(FVSR_E_CONFIG, "build_locality_mask: extents must be >= 1");
+    if (m->extent_h > g.rows || m->extent_w > g.cols)
+      return fail(FVSR_E_CONFIG, "build_locality_mask: extent larger than frame");
+    if (m->mode != FVSR_LOCALITY_PRESERVED && m->mode != FVSR_LOCALITY_TRUNCATED)
+      return fail(FVSR_E_CONFIG, "locality mode must be preserved (0) or truncated (1)");
+    return FVSR_OK;
+  }
+  if (m->kind == FVSR_MASK_BITMASK) {
+    if (!m->bits) return fail(FVSR_E_SHAPE, "bitmask mask without bits");
+    if (m->words_per_row != (lk + 63) / 64) return fail(FVSR_E_SHAPE, "mask shape mismatch (words_per_row)");
+    dm.bits = m->bits;
+    dm.words_per_row = m->words_per_row;
+    return FVSR_OK;
+  }
+  return fail(FVSR_E_CONFIG, "unknown mask kind %d", m->kind);
+}
+
+void* ws_get(fvsr_ctx* ctx, size_t bytes, int* st) {
+  if (bytes > ctx->ws_bytes) {
+    if (ctx->ws) cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_bytes = 0;
+    if (cudaMalloc(&ctx->ws, bytes) != cudaSuccess) {
+      *st = fail(FVSR_E_NOMEM, "workspace allocation of %zu bytes failed", bytes);
+      return nullptr;
+    }
+    ctx->ws_bytes = bytes;
+  }
+  *st = FVSR_OK;
+  return ctx->ws;
+}
+
+struct Carve {
+  uint8_t* base;
+  size_t off = 0;
+  explicit Carve(void* b) : base(static_cast<uint8_t*>(b)) {}
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 1023) & ~size_t(1023);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    return p;
+  }
+  static size_t need(std::initializer_list<size_t> sizes) {
+    size_t o = 0;
+    for (size_t s : sizes) o = ((o + 1023) & ~size_t(1023)) + s;
+    return o + 1024;
+  }
+};
+
+int after_launch(fvsr_ctx* ctx, cudaStream_t s, int nlaunch) {
+  ctx->launches += nlaunch;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FVSR_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  if (ctx->flags & FVSR_FLAG_SYNC_CHECK) return fvsr_check_errors(ctx, reinterpret_cast<fvsr_stream_t>(s));
+  return FVSR_OK;
+}
+
+int npow2(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// ---- launch helpers ---------------------------------------------------------------------
+void launch_pack(const uint16_t* src, long long src_head_stride, int heads, int nframes, const DevGeom& g,
+                 uint8_t* dst, long long dst_head_stride, const int* slots, cudaStream_t s) {
+  SlotList sl{};
+  for (int i = 0; i < nframes; ++i) sl.s[i] = slots ? slots[i] : i;
+  dim3 grid(g.n_tiles, nframes, heads);
+  pack_frames_kernel<<<grid, 256, 0, s>>>(src, src_head_stride, g.rows, g.cols, g.tiles_w, g.n_tiles, g.d, dst,
+                                          dst_head_stride, sl);
+}
+
+// Pooled partials for the t_rows of a frame list.
+void launch_pool_trows(const uint16_t* src, long long src_head_stride, int heads, const int* tr_first,
+                       const int* tr_count, int ntr, const DevGeom& g, const int* slots, float* s0, float* s1,
+                       long long part_head_stride, cudaStream_t s) {
+  PoolGroups pg{};
+  SlotList sl{};
+  int nf = 0;
+  for (int a = 0; a < ntr; ++a) {
+    pg.first[a] = tr_first[a];
+    pg.count[a] = tr_count[a];
+    pg.ext_slot[a] = -1;
+    nf = std::max(nf, tr_first[a] + tr_count[a]);
+  }
+  for (int i = 0; i < nf; ++i) sl.s[i] = slots ? slots[i] : i;
+  dim3 grid(g.n_tiles, ntr, heads);
+  const int threads = std::min(256, ((g.d + 31) / 32) * 32);
+  pool_partials_kernel<<<grid, threads, 0, s>>>(src, src_head_stride, g.rows, g.cols, g.tiles_w, g.n_tiles, g.d, pg,
+                                                sl, s0, s1, part_head_stride, nullptr);
+}
+
+int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads, const float* q_s0,
+                  const float* q_s1, long long q_head_stride, const float* k_s0, const float* k_s1,
+                  long long k_head_stride, float scale, long long topk, int cap, int* sel, int* sel_count,
+                  int* diag, float* coarse, uint8_t* allowed, cudaStream_t s) {
+  SelectParams p{};
+  p.q_s0 = q_s0;
+  p.q_s1 = q_s1;
+  p.q_head_stride = q_head_stride;
+  p.k_s0 = k_s0;
+  p.k_s1 = k_s1;
+  p.k_head_stride = k_head_stride;
+  p.scale = scale;
+  p.topk = topk;
+  p.cap = cap;
+  p.npow2 = npow2(g.bnk);
+  p.sel = sel;
+  p.sel_count = sel_count;
+  p.diag = diag;
+  p.coarse = coarse;
+  p.allowed = allowed;
+  p.err = ctx->d_err;
+  const size_t smem = (size_t)p.npow2 * 8 + (size_t)g.d * 4 + 2 * (size_t)g.bnk + 16;
+  if (smem > 48 * 1024) {
+    if (smem > 200 * 1024) return fail(FVSR_E_CONFIG, "too many key blocks (%d) for the selector", g.bnk);
+    FVSR_CUDA(cudaFuncSetAttribute(score_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  dim3 grid(g.bnq, heads);
+  score_select_kernel<<<grid, 256, smem, s>>>(g, dm, p);
+  return FVSR_OK;
+}
+
+template <int D>
+int launch_attn_d(const DevGeom& g, const DevMask& dm, const AttnParams& p, long long units, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)AttnCfg<D>::kBytes));
+    configured = true;
+  }
+  if (units <= 0) return FVSR_OK;
+  sparse_attn_kernel<D><<<(unsigned)units, 192, AttnCfg<D>::kBytes, s>>>(g, dm, p);
+  return FVSR_OK;
+}
+
+int launch_attn(const DevGeom& g, const DevMask& dm, const AttnParams& p, long long units, cudaStream_t s) {
+  if (g.d == 128) return launch_attn_d<128>(g, dm, p, units, s);
+  if (g.d == 64) return launch_attn_d<64>(g, dm, p, units, s);
+  return fail(FVSR_E_CONFIG, "sparse_attention_exec: head_dim %d unsupported (64 or 128)", g.d);
+}
+
+int check_ctx(fvsr_ctx* ctx) {
+  if (!ctx) return fail(FVSR_E_CONFIG, "null context");
+  int dev = -1;
+  FVSR_CUDA(cudaGetDevice(&dev));
+  if (dev != ctx->device) FVSR_CUDA(cudaSetDevice(ctx->device));
+  return FVSR_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+// C-ABI
+// =========================================================================================
+extern "C" {
+
+int32_t fvsr_abi_version(void) { return FVSR_ABI_VERSION; }
+
+const char* fvsr_last_error(void) { return g_last_error.c_str(); }
+
+int32_t fvsr_ctx_create(fvsr_ctx** out) {
+  if (!out) return fail(FVSR_E_CONFIG, "null output pointer");
+  *out = nullptr;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(FVSR_E_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  cudaDeviceProp prop{};
+  FVSR_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(FVSR_E_CUDA, "fvsr_b200 requires an sm_100 (B200) device; found sm_%d%d (%s)", prop.major, prop.minor,
+                prop.name);
+  auto* c = new fvsr_ctx();
+  c->device = dev;
+  if (cudaMalloc(&c->d_err, sizeof(unsigned)) != cudaSuccess) {
+    delete c;
+    return fail(FVSR_E_NOMEM, "error word allocation failed");
+  }
+  cudaMemset(c->d_err, 0, sizeof(unsigned));
+  *out = c;
+  return FVSR_OK;
+}
+
+void fvsr_ctx_destroy(fvsr_ctx* ctx) {
+  if (!ctx) return;
+  cudaFree(ctx->d_err);
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->stage) cudaFree(ctx->stage);
+  delete ctx;
+}
+
+int32_t fvsr_ctx_set_flags(fvsr_ctx* ctx, int32_t flags) {
+  if (!ctx) return fail(FVSR_E_CONFIG, "null context");
+  ctx->flags = flags;
+  return FVSR_OK;
+}
+
+int64_t fvsr_ctx_launch_count(const fvsr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int32_t fvsr_check_errors(fvsr_ctx* ctx, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  FVSR_CUDA(cudaStreamSynchronize(s));
+  unsigned bits = 0;
+  FVSR_CUDA(cudaMemcpy(&bits, ctx->d_err, sizeof(bits), cudaMemcpyDeviceToHost));
+  if (bits) FVSR_CUDA(cudaMemset(ctx->d_err, 0, sizeof(unsigned)));
+  const int code = status_from_bits(bits);
+  if (code) return fail(code, "%s", device_error_message(code));
+  return FVSR_OK;
+}
+
+int32_t fvsr_block_counts(const fvsr_grid* grid_q, const fvsr_grid* grid_k, int32_t* bnq, int32_t* bnk) {
+  DevGeom g;
+  FVSR_TRY(build_geom(grid_q, grid_k, 1, nullptr, g));
+  if (bnq) *bnq = g.bnq;
+  if (bnk) *bnk = g.bnk;
+  return FVSR_OK;
+}
+
+int32_t fvsr_plan_sparse(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k, int32_t heads, int32_t d,
+                         const fvsr_grid* grid_q, const fvsr_grid* grid_k, const fvsr_mask* mask, int64_t topk,
+                         int32_t cap, int32_t* sel, int32_t* sel_count, int32_t* diag, float* coarse,
+                         uint8_t* allowed, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!q || !k || !sel || !sel_count) return fail(FVSR_E_SHAPE, "plan_sparse: null tensor");
+  if (heads < 1 || d < 1) return fail(FVSR_E_SHAPE, "plan_sparse: heads and head_dim must be >= 1");
+  DevGeom g;
+  FVSR_TRY(build_geom(grid_q, grid_k, d, nullptr, g));
+  DevMask dm;
+  FVSR_TRY(build_mask(mask, g, grid_tokens(grid_k), dm));
+  if (topk < 1) return fail(FVSR_E_CONFIG, "plan_sparse: topk must be >= 1");  // sparse.cpp:83
+  if (cap < std::min<long long>(topk, g.bnk))
+    return fail(FVSR_E_SHAPE, "plan_sparse: cap %d < min(topk, bnk) = %lld", cap, std::min<long long>(topk, g.bnk));
+  const long long Lq = grid_tokens(grid_q), Lk = grid_tokens(grid_k);
+  const size_t qpart = (size_t)heads * g.nqf * g.n_tiles * d, kpart = (size_t)heads * g.nkf * g.n_tiles * d;
+  int st;
+  void* ws = ws_get(ctx, Carve::need({qpart * 4, qpart * 4, kpart * 4, kpart * 4}), &st);
+  if (!ws) return st;
+  Carve cv(ws);
+  float* qs0 = cv.take<float>(qpart);
+  float* qs1 = cv.take<float>(qpart);
+  float* ks0 = cv.take<float>(kpart);
+  float* ks1 = cv.take<float>(kpart);
+  launch_pool_trows(q, Lq * d, heads, g.q_tr_first, g.q_tr_count, g.nq_trows, g, nullptr, qs0, qs1,
+                    (long long)g.nqf * g.n_tiles * d, s);
+  launch_pool_trows(k, Lk * d, heads, g.k_tr_first, g.k_tr_count, g.nk_trows, g, nullptr, ks0, ks1,
+                    (long long)g.nkf * g.n_tiles * d, s);
+  const float scale = 1.0f / std::sqrt(static_cast<float>(d));  // sparse.cpp:97
+  FVSR_TRY(launch_select(ctx, g, dm, heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, ks0, ks1,
+                         (long long)g.nkf * g.n_tiles * d, scale, topk, cap, sel, sel_count, diag, coarse, allowed, s));
+  return after_launch(ctx, s, 3);
+}
+
+int32_t fvsr_sparse_attention_exec(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                                   int32_t heads, int32_t d, const fvsr_grid* grid_q, const fvsr_grid* grid_k,
+                                   const fvsr_mask* mask, int32_t cap, const int32_t* sel,
+                                   const int32_t* sel_count, float scale, int64_t row_begin, int64_t row_end,
+                                   uint16_t* out, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!q || !k || !v || !sel || !sel_count || !out) return fail(FVSR_E_SHAPE, "sparse_attention_exec: null tensor");
+  if (heads < 1) return fail(FVSR_E_SHAPE, "sparse_attention_exec: heads must be >= 1");
+  if (d != 64 && d != 128)
+    return fail(FVSR_E_CONFIG, "sparse_attention_exec: head_dim %d unsupported by the tensor-core kernel (64, 128)", d);
+  if (cap < 1) return fail(FVSR_E_SHAPE, "sparse_attention_exec: cap must be >= 1");
+  DevGeom g;
+  FVSR_TRY(build_geom(grid_q, grid_k, d, nullptr, g));
+  DevMask dm;
+  FVSR_TRY(build_mask(mask, g, grid_tokens(grid_k), dm));
+  const long long Lq = grid_tokens(grid_q), Lk = grid_tokens(grid_k);
+  if (row_end < 0 || row_end > Lq) row_end = Lq;  // sparse.cpp:224
+  if (row_begin < 0 || row_begin > row_end)
+    return fail(FVSR_E_CONFIG, "sparse_attention_exec: empty or inverted row range");  // :225
+  const size_t tb = (size_t)d * 128;
+  const size_t qbytes = (size_t)heads * g.nqf * g.n_tiles * tb, kbytes = (size_t)heads * g.nkf * g.n_tiles * tb;
+  int st;
+  void* ws = ws_get(ctx, Carve::need({qbytes, kbytes, kbytes}), &st);
+  if (!ws) return st;
+  Carve cv(ws);
+  uint8_t* qp = cv.take<uint8_t>(qbytes);
+  uint8_t* kp = cv.take<uint8_t>(kbytes);
+  uint8_t* vp = cv.take<uint8_t>(kbytes);
+  launch_pack(q, Lq * d, heads, g.nqf, g, qp, (long long)g.nqf * g.n_tiles * tb, nullptr, s);
+  launch_pack(k, Lk * d, heads, g.nkf, g, kp, (long long)g.nkf * g.n_tiles * tb, nullptr, s);
+  launch_pack(v, Lk * d, heads, g.nkf, g, vp, (long long)g.nkf * g.n_tiles * tb, nullptr, s);
+  AttnParams p{};
+  p.q = qp;
+  p.q_head_stride = (long long)g.nqf * g.n_tiles * tb;
+  p.k = kp;
+  p.v = vp;
+  p.kv_head_stride = (long long)g.nkf * g.n_tiles * tb;
+  p.sel = sel;
+  p.sel_count = sel_count;
+  p.cap = cap;
+  p.out = out;
+  p.out_head_stride = Lq * d;
+  p.row_begin = row_begin;
+  p.row_end = row_end;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.unit_begin = 0;
+  p.err = ctx->d_err;
+  FVSR_TRY(launch_attn(g, dm, p, (long long)heads * g.nqf * g.n_tiles, s));
+  return after_launch(ctx, s, 4);
+}
+
+int32_t fvsr_sparsity_report(fvsr_ctx* ctx, int32_t heads, const fvsr_grid* grid_q, const fvsr_grid* grid_k,
+                             const fvsr_mask* mask, int32_t cap, const int32_t* sel, const int32_t* sel_count,
+                             uint64_t* executed_pairs, uint64_t* dense_pairs, uint64_t* selected_blocks,
+                             uint64_t* allowed_blocks, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!sel || !sel_count || !executed_pairs || !dense_pairs || !selected_blocks || !allowed_blocks)
+    return fail(FVSR_E_SHAPE, "sparsity_report: null tensor");
+  DevGeom g;
+  FVSR_TRY(build_geom(grid_q, grid_k, 1, nullptr, g));
+  DevMask dm;
+  FVSR_TRY(build_mask(mask, g, grid_tokens(grid_k), dm));
+  for (uint64_t* o : {executed_pairs, dense_pairs, selected_blocks, allowed_blocks})
+    FVSR_CUDA(cudaMemsetAsync(o, 0, sizeof(uint64_t) * heads, s));
+  dim3 grid(g.bnq, heads);
+  sparsity_count_kernel<<<grid, 128, 0, s>>>(g, dm, sel, sel_count, cap,
+                                             reinterpret_cast<unsigned long long*>(executed_pairs),
+                                             reinterpret_cast<unsigned long long*>(dense_pairs),
+                                             reinterpret_cast<unsigned long long*>(selected_blocks),
+                                             reinterpret_cast<unsigned long long*>(allowed_blocks));
+  return after_launch(ctx, s, 1);
+}
+
+// ---- ring ---------------------------------------------------------------------------------
+int32_t fvsr_ring_create(fvsr_ctx* ctx, int32_t layers, int32_t heads, int32_t d, int32_t rows, int32_t cols,
+                         int32_t window_frames, fvsr_ring** out) {
+  FVSR_TRY(check_ctx(ctx));
+  if (!out) return fail(FVSR_E_CONFIG, "null output pointer");
+  *out = nullptr;
+  if (layers < 1 || heads < 1 || window_frames < 1)
+    return fail(FVSR_E_CONFIG, "KVCache: empty extents");  // kv_cache.cpp:31
+  if (rows < 1 || cols < 1) return fail(FVSR_E_CONFIG, "TokenGrid: empty extents");
+  if (d != 64 && d != 128) return fail(FVSR_E_CONFIG, "ring: head_dim %d unsupported (64 or 128)", d);
+  if (window_frames + 1 > kMaxFrames)
+    return fail(FVSR_E_CONFIG, "ring: window %d exceeds the kernel limit of %d frames", window_frames, kMaxFrames - 1);
+  auto* r = new fvsr_ring();
+  r->layers = layers;
+  r->heads = heads;
+  r->d = d;
+  r->rows = rows;
+  r->cols = cols;
+  r->window = window_frames;
+  r->slots = window_frames + 1;
+  r->tiles_w = (cols + 7) / 8;
+  r->tiles_h = (rows + 7) / 8;
+  r->n_tiles = r->tiles_w * r->tiles_h;
+  r->tile_bytes = (size_t)d * 128;
+  const size_t kvb = (size_t)layers * heads * r->kv_head_stride();
+  const size_t pb = (size_t)layers * heads * r->part_head_stride() * sizeof(float);
+  if (cudaMalloc(&r->k, kvb) != cudaSuccess || cudaMalloc(&r->v, kvb) != cudaSuccess ||
+      cudaMalloc(&r->s0, pb) != cudaSuccess || cudaMalloc(&r->s1, pb) != cudaSuccess) {
+    fvsr_ring_destroy(r);
+    return fail(FVSR_E_NOMEM, "ring allocation of %zu bytes failed", 2 * kvb + 2 * pb);
+  }
+  r->ctx.assign(layers, {});
+  r->used.assign(layers, std::vector<char>(r->slots, 0));
+  *out = r;
+  return FVSR_OK;
+}
+
+void fvsr_ring_destroy(fvsr_ring* ring) {
+  if (!ring) return;
+  cudaFree(ring->k);
+  cudaFree(ring->v);
+  cudaFree(ring->s0);
+  cudaFree(ring->s1);
+  delete ring;
+}
+
+int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* k,
+                         const uint16_t* v, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!r || !k || !v) return fail(FVSR_E_SHAPE, "ring_append: null argument");
+  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer/head out of range");
+  if (frame_id < 0) return fail(FVSR_E_CONFIG, "TokenGrid: negative frame id");
+  auto& c = r->ctx[layer];
+  if (!c.empty() && frame_id <= c.back().first)
+    return fail(FVSR_E_INVARIANT, "KVCache: frame ids must increase");  // kv_cache.cpp:42
+  int slot = -1;
+  for (int i = 0; i < r->slots; ++i)
+    if (!r->used[layer][i]) { slot = i; break; }
+  if (slot < 0)
+    return fail(FVSR_E_INVARIANT, "KVCache: head retains more than window + current (evict before append)");
+  int partner = -1;
+  if ((frame_id & 1) && !c.empty() && c.back().first == frame_id - 1) partner = c.back().second;
+
+  DevGeom g{};
+  g.rows = r->rows;
+  g.cols = r->cols;
+  g.tiles_w = r->tiles_w;
+  g.tiles_h = r->tiles_h;
+  g.n_tiles = r->n_tiles;
+  g.d = r->d;
+  const long long N = (long long)r->rows * r->cols;
+  const int slots1[1] = {slot};
+  launch_pack(k, N * r->d, r->heads, 1, g, r->k_layer(layer), r->kv_head_stride(), slots1, s);
+  launch_pack(v, N * r->d, r->heads, 1, g, r->v_layer(layer), r->kv_head_stride(), slots1, s);
+  PoolGroups pg{};
+  pg.first[0] = 0;
+  pg.count[0] = 1;
+  pg.ext_slot[0] = partner;
+  SlotList sl{};
+  sl.s[0] = slot;
+  dim3 grid(r->n_tiles, 1, r->heads);
+  pool_partials_kernel<<<grid, std::min(256, r->d), 0, s>>>(k, N * r->d, r->rows, r->cols, r->tiles_w, r->n_tiles,
+                                                            r->d, pg, sl, r->s0_layer(layer), r->s1_layer(layer),
+                                                            r->part_head_stride(), r->s0_layer(layer));
+  r->used[layer][slot] = 1;
+  c.emplace_back(frame_id, slot);
+  return after_launch(ctx, s, 3);
+}
+
+int32_t fvsr_ring_evict_sliding(fvsr_ring* r, int32_t layer) {
+  if (!r) return fail(FVSR_E_CONFIG, "null ring");
+  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
+  auto& c = r->ctx[layer];
+  while ((int)c.size() > r->window) {  // kv_cache.cpp:100-106
+    r->used[layer][c.front().second] = 0;
+    c.erase(c.begin());
+  }
+  return FVSR_OK;
+}
+
+int32_t fvsr_ring_frame_ids(const fvsr_ring* r, int32_t layer, int32_t* ids, int32_t cap, int32_t* n) {
+  if (!r) return fail(FVSR_E_CONFIG, "null ring");
+  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
+  const auto& c = r->ctx[layer];
+  if (n) *n = (int32_t)c.size();
+  if ((int)c.size() > cap) return fail(FVSR_E_SHAPE, "frame id buffer too small");
+  for (size_t i = 0; i < c.size(); ++i) ids[i] = c[i].first;
+  return FVSR_OK;
+}
+
+int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const uint16_t* q,
+                            const int32_t* q_frame_ids, int32_t nq, const fvsr_mask* mask, int64_t topk, float scale,
+                            int64_t unit_begin, int64_t unit_end, uint16_t* out, int32_t sel_cap, int32_t* sel,
+                            int32_t* sel_count, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!r || !q || !out || !q_frame_ids) return fail(FVSR_E_SHAPE, "ring_attention: null argument");
+  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
+  const auto& c = r->ctx[layer];
+  if (c.empty()) return fail(FVSR_E_CONFIG, "ring_attention: empty context");
+  std::vector<int> kids, kslots;
+  for (auto& fs : c) {
+    kids.push_back(fs.first);
+    kslots.push_back(fs.second);
+  }
+  fvsr_grid gq{q_frame_ids, nq, r->rows, r->cols};
+  fvsr_grid gk{kids.data(), (int)kids.size(), r->rows, r->cols};
+  DevGeom g;
+  FVSR_TRY(build_geom(&gq, &gk, r->d, kslots.data(), g));
+  DevMask dm;
+  FVSR_TRY(build_mask(mask, g, grid_tokens(&gk), dm));
+  if (topk < 1) return fail(FVSR_E_CONFIG, "plan_sparse: topk must be >= 1");
+  const int cap_need = (int)std::min<long long>(topk, g.bnk);
+  if (sel && sel_cap < cap_need) return fail(FVSR_E_SHAPE, "ring_attention: sel_cap < min(topk, bnk)");
+  const int cap = sel ? sel_cap : cap_need;
+  const int d = r->d;
+  const long long Lq = grid_tokens(&gq);
+  const size_t tb = r->tile_bytes;
+  const size_t qbytes = (size_t)r->heads * g.nqf * g.n_tiles * tb;
+  const size_t qpart = (size_t)r->heads * g.nqf * g.n_tiles * d;
+  const size_t nsel = (size_t)r->heads * g.bnq;
+  int st;
+  void* ws = ws_get(ctx, Carve::need({qbytes, qpart * 4, qpart * 4, nsel * cap * 4, nsel * 4}), &st);
+  if (!ws) return st;
+  Carve cv(ws);
+  uint8_t* qp = cv.take<uint8_t>(qbytes);
+  float* qs0 = cv.take<float>(qpart);
+  float* qs1 = cv.take<float>(qpart);
+  int* wsel = cv.take<int>(nsel * cap);
+  int* wcnt = cv.take<int>(nsel);
+  int* use_sel = sel ? sel : wsel;
+  int* use_cnt = sel_count ? sel_count : wcnt;
+
+  launch_pack(q, Lq * d, r->heads, g.nqf, g, qp, (long long)g.nqf * g.n_tiles * tb, nullptr, s);
+  launch_pool_trows(q, Lq * d, r->heads, g.q_tr_first, g.q_tr_count, g.nq_trows, g, nullptr, qs0, qs1,
+                    (long long)g.nqf * g.n_tiles * d, s);
+  const float cscale = 1.0f / std::sqrt(static_cast<float>(d));
+  FVSR_TRY(launch_select(ctx, g, dm, r->heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, r->s0_layer(layer),
+                         r->s1_layer(layer), r->part_head_stride(), cscale, topk, cap, use_sel, use_cnt, nullptr,
+                         nullptr, nullptr, s));
+  const long long units_total = (long long)r->heads * g.nqf * g.n_tiles;
+  if (unit_end < 0 || unit_end > units_total) unit_end = units_total;
+  if (unit_begin < 0 || unit_begin > unit_end) return fail(FVSR_E_CONFIG, "ring_attention: bad unit range");
+  AttnParams p{};
+  p.q = qp;
+  p.q_head_stride = (long long)g.nqf * g.n_tiles * tb;
+  p.k = r->k_layer(layer);
+  p.v = r->v_layer(layer);
+  p.kv_head_stride = r->kv_head_stride();
+  p.sel = use_sel;
+  p.sel_count = use_cnt;
+  p.cap = cap;
+  p.out = out;
+  p.out_head_stride = Lq * d;
+  p.row_begin = 0;
+  p.row_end = Lq;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.unit_begin = unit_begin;
+  p.err = ctx->d_err;
+  FVSR_TRY(launch_attn(g, dm, p, unit_end - unit_begin, s));
+  return after_launch(ctx, s, 4);
+}
+
+int32_t fvsr_ring_step_host(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* q_host,
+                            const uint16_t* k_host, const uint16_t* v_host, const fvsr_mask* mask, int64_t topk,
+                            float scale, uint16_t* out_host, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!r || !q_host || !k_host || !v_host || !out_host) return fail(FVSR_E_SHAPE, "ring_step_host: null argument");
+  const size_t n = (size_t)r->heads * r->rows * r->cols * r->d;  // elements per tensor
+  const size_t bytes = n * sizeof(uint16_t);
+  if (ctx->stage_bytes < 4 * bytes) {
+    if (ctx->stage) cudaFree(ctx->stage);
+    ctx->stage = nullptr;
+    ctx->stage_bytes = 0;
+    if (cudaMalloc(&ctx->stage, 4 * bytes) != cudaSuccess) return fail(FVSR_E_NOMEM, "staging allocation failed");
+    ctx->stage_bytes = 4 * bytes;
+  }
+  uint16_t* dq = static_cast<uint16_t*>(ctx->stage);
+  uint16_t* dk = dq + n;
+  uint16_t* dv = dk + n;
+  uint16_t* dout = dv + n;
+  FVSR_CUDA(cudaMemcpyAsync(dq, q_host, bytes, cudaMemcpyHostToDevice, s));
+  FVSR_CUDA(cudaMemcpyAsync(dk, k_host, bytes, cudaMemcpyHostToDevice, s));
+  FVSR_CUDA(cudaMemcpyAsync(dv, v_host, bytes, cudaMemcpyHostToDevice, s));
+  FVSR_TRY(fvsr_ring_append(ctx, r, layer, frame_id, dk, dv, stream));
+  const int32_t qids[1] = {frame_id};
+  FVSR_TRY(fvsr_ring_attention(ctx, r, layer, dq, qids, 1, mask, topk, scale, 0, -1, dout, 0, nullptr, nullptr,
+                               stream));
+  FVSR_TRY(fvsr_ring_evict_sliding(r, layer));
+  FVSR_CUDA(cudaMemcpyAsync(out_host, dout, bytes, cudaMemcpyDeviceToHost, s));
+  return FVSR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+"""Device-resident ring-buffer KV cache for chunk-by-chunk streaming.
+
+Replaces vsr::KVCache (P/include/vsr/kv_cache.hpp:27-73; P = /root/reference/proj) with
+the sliding-window strategy, plus the per-step ``concat_rows`` context assembly of
+step() (P/src/stream.cpp:244-249): a layer keeps window+1 frame slots per head in HBM,
+tile-major and pre-swizzled for the tensor-core kernel, and attention addresses the
+slots directly, so no context is ever copied.
+
+    ring = KVRing(layers, heads, d, rows, cols, window_frames)
+    ring.append(layer, t, k, v)             # KVCache::append for every head
+    out  = ring.attention(layer, q, [t], mask, topk)   # head_attention, all heads
+    ring.evict(layer)                       # KVCache::evict (sliding window)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import Optional, Sequence
+
+import torch
+
+from . import _abi
+from ._abi import ShapeError, check
+from .sparse import Context, Mask, _heads3, _stream
+
+
+class KVRing:
+    def __init__(self, layers: int, heads: int, d: int, rows: int, cols: int, window_frames: int,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or Context.default()
+        self.layers, self.heads, self.d, self.rows, self.cols = layers, heads, d, rows, cols
+        self.window = window_frames
+        h = C.c_void_p()
+        check(self.ctx.lib.fvsr_ring_create(self.ctx.h, layers, heads, d, rows, cols, window_frames, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.fvsr_ring_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def tokens_per_frame(self) -> int:
+        return self.rows * self.cols
+
+    def _frame(self, x: torch.Tensor, name: str) -> torch.Tensor:
+        x3 = _heads3(x, name)
+        if x3.shape != (self.heads, self.tokens_per_frame, self.d):
+            raise ShapeError(f"{name}: expected [{self.heads}, {self.tokens_per_frame}, {self.d}], got {tuple(x3.shape)}")
+        return x3
+
+    def append(self, layer: int, frame_id: int, k: torch.Tensor, v: torch.Tensor) -> None:
+        k3, v3 = self._frame(k, "append k"), self._frame(v, "append v")
+        check(self.ctx.lib.fvsr_ring_append(self.ctx.h, self.h, layer, int(frame_id), k3.data_ptr(), v3.data_ptr(),
+                                            _stream()))
+
+    def evict(self, layer: int) -> None:
+        check(self.ctx.lib.fvsr_ring_evict_sliding(self.h, layer))
+
+    def frame_ids(self, layer: int):
+        buf = (C.c_int32 * 64)()
+        n = C.c_int32()
+        check(self.ctx.lib.fvsr_ring_frame_ids(self.h, layer, buf, 64, C.byref(n)))
+        return [buf[i] for i in range(n.value)]
+
+    def retained(self, layer: int) -> int:
+        return len(self.frame_ids(layer))
+
+    def attention(self, layer: int, q: torch.Tensor, q_frame_ids: Sequence[int], mask: Optional[Mask] = None,
+                  topk: int = 1, scale: Optional[float] = None, *, unit_begin: int = 0, unit_end: int = -1,
+                  out: Optional[torch.Tensor] = None, sel: Optional[torch.Tensor] = None,
+                  sel_count: Optional[torch.Tensor] = None, check_errors: bool = True) -> torch.Tensor:
+        mask = mask or Mask.all_allowed()
+        q3 = _heads3(q, "ring attention q")
+        nq = len(q_frame_ids)
+        if q3.shape != (self.heads, nq * self.tokens_per_frame, self.d):
+            raise ShapeError("ring attention: q must be [heads, nq*rows*cols, d]")
+        if scale is None:
+            scale = 1.0 / math.sqrt(self.d)
+        if out is None:
+            out = torch.empty_like(q3)
+        ids = (C.c_int32 * nq)(*[int(f) for f in q_frame_ids])
+        md = mask.c()
+        cap = sel.shape[-1] if sel is not None else 0
+        check(self.ctx.lib.fvsr_ring_attention(self.ctx.h, self.h, layer, q3.data_ptr(), ids, nq, C.byref(md),
+                                               int(topk), float(scale), int(unit_begin), int(unit_end),
+                                               out.data_ptr(), cap, sel.data_ptr() if sel is not None else None,
+                                               sel_count.data_ptr() if sel_count is not None else None, _stream()))
+        if check_errors:
+            self.ctx.check_errors()
+        return out
+
+    def step_host(self, layer: int, frame_id: int, q_host: torch.Tensor, k_host: torch.Tensor,
+                  v_host: torch.Tensor, out_host: torch.Tensor, mask: Optional[Mask] = None, topk: int = 1,
+                  scale: Optional[float] = None) -> None:
+        """One streaming layer-step from host (pinned) bf16 buffers: H2D, append, attention,
+        sliding evict, D2H.  Asynchronous on the current stream."""
+        mask = mask or Mask.all_allowed()
+        for t, nm in ((q_host, "q"), (k_host, "k"), (v_host, "v"), (out_host, "out")):
+            if t.is_cuda or t.dtype != torch.bfloat16 or t.numel() != self.heads * self.tokens_per_frame * self.d:
+                raise ShapeError(f"step_host {nm}: host bf16 tensor of heads*rows*cols*d elements required")
+        if scale is None:
+            scale = 1.0 / math.sqrt(self.d)
+        md = mask.c()
+        check(self.ctx.lib.fvsr_ring_step_host(self.ctx.h, self.h, layer, int(frame_id), q_host.data_ptr(),
+                                               k_host.data_ptr(), v_host.data_ptr(), C.byref(md), int(topk),
+                                               float(scale), out_host.data_ptr(), _stream()))

@@ -1,0 +1,101 @@
+"""GPU parity of the device ring-buffer KV cache (KVCache append / sliding evict +
+head_attention, P/src/kv_cache.cpp:39-106, P/src/stream.cpp:175-256) against the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+from tests.helpers import MAX_ABS_TOL, REL_L2_TOL, max_abs, oracle_outs, oracle_plans, rel_l2, to_dev
+
+pytestmark = pytest.mark.gpu
+fv = pytest.importorskip("paper_2510_12747_b200")
+
+
+def frame_data(seed, heads, n, d):
+    port = oracle.Port()
+    out = []
+    for h in range(heads):
+        x = port.gaussian(seed * 1000 + h, 3 * n * d).reshape(3, n, d)
+        out.append(oracle.bf16_round(x))
+    a = np.stack(out)  # [heads, 3, n, d]
+    return a[:, 0], a[:, 1], a[:, 2]
+
+
+@pytest.mark.parametrize("window,start,mask", [(4, 0, None), (3, 5, ("loc", 9, 13, True)), (2, 1, ("loc", 7, 7, False))])
+def test_streaming_ring_matches_oracle(window, start, mask):
+    heads, rows, cols, d, topk, layers = 2, 20, 36, 128, 4, 2
+    n = rows * cols
+    fmask = fv.Mask.all_allowed() if mask is None else fv.Mask.locality(mask[1], mask[2], mask[3])
+    omask = oracle.Mask.all() if mask is None else oracle.Mask.locality(mask[1], mask[2], mask[3])
+    ring = fv.KVRing(layers, heads, d, rows, cols, window)
+    ctx_k, ctx_v, ids = [], [], []
+    for t in range(start, start + 9):
+        q, k, v = frame_data(t + 17, heads, n, d)
+        layer = t % layers  # exercise per-layer bookkeeping
+        ring.append(layer, t, to_dev(k), to_dev(v))
+        if layer == 0:
+            ids.append(t); ctx_k.append(k); ctx_v.append(v)
+            assert ring.frame_ids(0) == ids
+            out = ring.attention(0, to_dev(q), [t], fmask, topk).float().cpu().numpy()
+            K, V = np.concatenate(ctx_k, axis=1), np.concatenate(ctx_v, axis=1)
+            refs = oracle_plans(q, K, [t], ids, rows, cols, omask, topk)
+            ref = oracle_outs(q, K, V, [t], ids, rows, cols, omask, refs, oracle.head_scale(d))
+            assert rel_l2(out, ref) <= REL_L2_TOL, rel_l2(out, ref)
+            assert max_abs(out, ref) <= MAX_ABS_TOL, max_abs(out, ref)
+            ring.evict(0)
+            while len(ids) > window:
+                ids.pop(0); ctx_k.pop(0); ctx_v.pop(0)
+            assert ring.frame_ids(0) == ids
+        else:
+            ring.evict(layer)
+            assert len(ring.frame_ids(layer)) <= window
+
+
+def test_ring_selection_bit_exact_and_invariants():
+    import torch
+    heads, rows, cols, d, topk, window = 3, 16, 40, 64, 5, 4
+    n = rows * cols
+    ring = fv.KVRing(1, heads, d, rows, cols, window)
+    ks, vs, ids = [], [], []
+    for t in range(7, 14):
+        q, k, v = frame_data(t, heads, n, d)
+        ring.append(0, t, to_dev(k), to_dev(v))
+        ids.append(t); ks.append(k); vs.append(v)
+        g = fv.TokenGrid(ids, rows, cols)
+        bnq, bnk = fv.block_counts(fv.TokenGrid([t], rows, cols), g)
+        cap = min(topk, bnk)
+        sel = torch.empty((heads, bnq, cap), dtype=torch.int32, device="cuda")
+        cnt = torch.empty((heads, bnq), dtype=torch.int32, device="cuda")
+        ring.attention(0, to_dev(q), [t], fv.Mask.all_allowed(), topk, sel=sel, sel_count=cnt)
+        refs = oracle_plans(q, np.concatenate(ks, axis=1), [t], ids, rows, cols, oracle.Mask.all(), topk)
+        for h in range(heads):
+            np.testing.assert_array_equal(sel[h].cpu().numpy(), refs[h].sel)
+            np.testing.assert_array_equal(cnt[h].cpu().numpy(), refs[h].count)
+        ring.evict(0)
+        while len(ids) > window:
+            ids.pop(0); ks.pop(0); vs.pop(0)
+    # KVCache contracts: increasing ids, window + current
+    with pytest.raises(fv.InvariantError):
+        ring.append(0, 5, to_dev(k), to_dev(v))
+    ring.append(0, 20, to_dev(k), to_dev(v))
+    with pytest.raises(fv.InvariantError):
+        ring.append(0, 21, to_dev(k), to_dev(v))
+
+
+def test_ring_step_host_end_to_end():
+    import torch
+    heads, rows, cols, d, topk, window = 2, 24, 32, 128, 6, 4
+    n = rows * cols
+    ring = fv.KVRing(1, heads, d, rows, cols, window)
+    ring2 = fv.KVRing(1, heads, d, rows, cols, window)
+    for t in range(6):
+        q, k, v = frame_data(100 + t, heads, n, d)
+        qh = torch.from_numpy(q).to(torch.bfloat16).pin_memory()
+        kh = torch.from_numpy(k).to(torch.bfloat16).pin_memory()
+        vh = torch.from_numpy(v).to(torch.bfloat16).pin_memory()
+        oh = torch.empty_like(qh).pin_memory()
+        ring.step_host(0, t, qh, kh, vh, oh, fv.Mask.all_allowed(), topk)
+        torch.cuda.synchronize()
+        ring2.append(0, t, to_dev(k), to_dev(v))
+        dev = ring2.attention(0, to_dev(q), [t], fv.Mask.all_allowed(), topk)
+        ring2.evict(0)
+        assert torch.equal(oh.cuda(), dev)
