@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""Benchmark: FlashVSR block-sparse streaming attention layer-step on B200.
+
+Metric (BASELINE.json): sparse-attn tokens/s & effective TFLOP/s at the 768x1408 latent
+(48x88 tokens/frame), 12 heads, d=128, sliding window W=4 (context = 5 frames), top-k 27
+(= topk_for_density(0.136, 198), P/src/bench.cpp:62-69), all-allowed token mask.
+
+One step = one streaming layer-step of the hot path for every head: append the new
+frame's K/V to the device ring (KVCache::append), build the plan (pool Q, score against the
+ring's pooled K partials, top-k with forced diagonal), block-sparse attention over the
+ring, sliding evict.  Steps cycle over a 30-layer stack of rings (BASELINE config #3), so
+each step's inputs (127 MB of ring per layer, 3.8 GB total) are larger than L2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N>1 runs under torchrun: (head, q-tile) units are sharded across ranks (head parallel),
+outputs gathered with NCCL all_gather_into_tensor on NCCL's stream, overlapped with the
+next layer-step; time is the max over ranks.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+ROWS, COLS, HEADS, D, WINDOW, TOPK, LAYERS = 48, 88, 12, 128, 4, 27, 30
+T0 = 32  # steady state: query frame t=32 over context {28..32}
+POOL = 4  # distinct synthetic frames cycled through the stream
+METRIC = "sparse-attn tokens/s & effective TFLOP/s at 768×1408 latent, 1/2/4/8 B200 vs CPU"
+WORKLOAD = ("768x1408 streaming layer-step: 48x88 latent tokens/frame, 12 heads, d=128, KV window W=4 "
+            "(context 5 frames, 198 key blocks), top-k 27 (13.6%), all-allowed mask, Tq=1")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"],
+                "bf16_tflops_sustained": p.get("bf16_tflops_sustained"), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.window = (0.0, 0.0)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        t0, t1 = self.window
+        rows = [s for (t, s) in self.samples if t0 - 0.05 <= t <= t1 + 0.05] or [s for (_, s) in self.samples]
+        mhz, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            parts = [x.strip() for x in r.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                mhz.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(mhz)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU baseline: the reference hot path (oracle/_ref, compiled from /root/reference) on host cores
+# ------------------------------------------------------------------------------------------
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def reference_case(seed: int = 1234, head: int = 0):
+    """One head of the step at t=32 over {28..32}, fp32 values that are bf16-representable."""
+    import oracle
+    N = ROWS * COLS
+    q, k, v = oracle.synthetic_qkv(seed + head, N, 5 * N, D)
+    return q, k, v
+
+
+def time_reference_heads(n_heads: int, threads: int, warmup: int = 1):
+    """Median seconds for one head of the reference head_attention (partition, mask,
+    plan_sparse, sparse_attention_exec; P/src/stream.cpp:175-194)."""
+    import numpy as np
+    import oracle
+    kind = "reference"
+    try:
+        ref = oracle.Ref()
+    except Exception:
+        ref = None
+        kind = "port"
+    scale = oracle.head_scale(D)
+    times = []
+    q, k, v = reference_case()
+    if ref is not None:
+        case = ref.case(q, k, v, [T0], list(range(T0 - WINDOW, T0 + 1)), ROWS, COLS, oracle.Mask.all())
+        for i in range(warmup + n_heads):
+            t = time.perf_counter()
+            case.head_attention(TOPK, scale, threads)
+            dt = time.perf_counter() - t
+            if i >= warmup:
+                times.append(dt)
+    else:
+        port = oracle.Port()
+        threads = 1
+        kf = list(range(T0 - WINDOW, T0 + 1))
+        for i in range(warmup + n_heads):
+            t = time.perf_counter()
+            plan = port.plan(q, k, [T0], kf, ROWS, COLS, oracle.Mask.all(), TOPK)
+            port.exec(q, k, v, [T0], kf, ROWS, COLS, oracle.Mask.all(), plan, scale)
+            dt = time.perf_counter() - t
+            if i >= warmup:
+                times.append(dt)
+    return statistics.median(times), kind, threads, times
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = cpu_threads()
+    # each step = one head of the layer-step (a bounded sample); value scales to 12 heads.
+    # At most 20 timed samples (+2 warm-up) so the arm ends within minutes for any --steps.
+    n_timed, n_warm = max(1, min(args.steps, 20)), min(args.warmup, 2)
+    med, kind, threads_used, times = time_reference_heads(n_timed, threads, warmup=n_warm)
+    tokens_per_s = ROWS * COLS / (HEADS * med)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": med * HEADS * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (vsr::Rng N(0,1), bf16-rounded)",
+        "config": {"workload": WORKLOAD, "heads": HEADS, "d": D, "latent": [ROWS, COLS], "window": WINDOW,
+                   "topk": TOPK, "mask": "all"},
+        "cpu_baseline": {"value": tokens_per_s, "unit": "tokens/s", "cores": threads_used, "kind": kind,
+                         "sample": f"{n_timed} single-head head_attention calls (1/12 of a layer-step each), "
+                                   f"median {med*1e3:.1f} ms, threads={threads_used}, {cpu_model()}"},
+        "e2e": {"value": tokens_per_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# B200 arm
+# ------------------------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2510_12747_b200 as fv
+    from paper_2510_12747_b200 import _abi, head_parallel as hp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    N = ROWS * COLS
+    tiles = ((ROWS + 7) // 8) * ((COLS + 7) // 8)
+    units = HEADS * tiles
+    sh = hp.shard(units, tiles, world, rank)
+    nh = sh.heads
+    ctx = fv.Context.default()
+    mask = fv.Mask.all_allowed()
+    scale = 1.0 / math.sqrt(D)
+
+    # synthetic pool: POOL frames of q/k/v, N(0,1) rounded to bf16, generated on device
+    gen = torch.Generator(device=dev).manual_seed(2510)
+    pool = [[torch.randn((HEADS, N, D), generator=gen, device=dev).to(torch.bfloat16) for _ in range(3)]
+            for _ in range(POOL)]
+    pool_local = [[x[sh.h0:sh.h1].contiguous() for x in fr] for fr in pool]
+
+    rings = fv.KVRing(LAYERS, nh, D, ROWS, COLS, WINDOW, ctx=ctx)
+    for l in range(LAYERS):
+        for f in range(T0 - WINDOW, T0):
+            _, k, v = pool_local[(f + l) % POOL]
+            rings.append(l, f, k, v)
+            rings.evict(l)
+    torch.cuda.synchronize()
+
+    gather = hp.Gatherer(sh, D, dev) if world > 1 else None
+    out_tok = torch.empty((HEADS, N, D), dtype=torch.bfloat16, device=dev)
+    lib = ctx.lib
+    md = mask.c()
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    import ctypes as C
+
+    state = {"s": 0}
+
+    def step():
+        s = state["s"]
+        state["s"] += 1
+        l = s % LAYERS
+        t = T0 + s // LAYERS
+        q, k, v = pool_local[(t + l) % POOL]
+        _abi.check(lib.fvsr_ring_append(ctx.h, rings.h, l, t, k.data_ptr(), v.data_ptr(), C.c_void_p(sptr)))
+        ids = (C.c_int32 * 1)(t)
+        if gather is None:
+            _abi.check(lib.fvsr_ring_attention(ctx.h, rings.h, l, q.data_ptr(), ids, 1, C.byref(md), TOPK, scale,
+                                               0, -1, out_tok.data_ptr(), 0, 0, None, None, C.c_void_p(sptr)))
+        else:
+            buf = gather.next_shard()
+            _abi.check(lib.fvsr_ring_attention(ctx.h, rings.h, l, q.data_ptr(), ids, 1, C.byref(md), TOPK, scale,
+                                               sh.local_unit_begin, sh.local_unit_end, buf.data_ptr(), 1, 0, None,
+                                               None, C.c_void_p(sptr)))
+            gather.launch()
+        _abi.check(lib.fvsr_ring_evict_sliding(rings.h, l))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warmup ---------------------------------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    if gather:
+        gather.drain()
+    ctx.check_errors()
+    ctx.read_pairs()  # reset the executed-pair counter
+    ctx.timing_read(_abi.TIME_ATTENTION, clear=True)
+
+    # ---- timed region -----------------------------------------------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ctx.timing(True)
+    launches0 = ctx.launch_count()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    if gather:
+        gather.drain()
+    ev1.record(stream)
+    barrier()
+    w1 = time.time()
+    clocks.window = (w0, w1)
+    time.sleep(0.15)
+    clocks.stop()
+    ctx.timing(False)
+    elapsed_ms = ev0.elapsed_time(ev1)
+    launches = ctx.launch_count() - launches0
+    ctx.check_errors()
+    pairs = ctx.read_pairs()
+    attn_ms, attn_n = ctx.timing_read(_abi.TIME_ATTENTION)
+    mb_ms, mb_n = ctx.timing_read(_abi.TIME_MASK_BUILDER)
+    ap_ms, ap_n = ctx.timing_read(_abi.TIME_APPEND, clear=True)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+        pt = torch.tensor([float(pairs), attn_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(pt, op=dist.ReduceOp.SUM)
+        pairs_total = int(pt[0].item())
+    else:
+        pairs_total = pairs
+
+    ms_per_step = elapsed_ms / args.steps
+    tokens_per_s = N * args.steps / (elapsed_ms / 1e3)
+    eff_tflops = 4.0 * D * pairs_total / (elapsed_ms / 1e3) / 1e12
+    pk = peaks()
+
+    # ---- end-to-end through the C-ABI with host buffers -------------------------------------
+    e2e = None
+    h2d = 3 * nh * N * D * 2
+    d2h = (HEADS if world == 1 else HEADS) * N * D * 2
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    hq = [[x.cpu().pin_memory() for x in fr] for fr in pool_local]
+    ho = torch.empty((HEADS, N, D), dtype=torch.bfloat16).pin_memory()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(e2e_steps):
+        s = state["s"]
+        state["s"] += 1
+        l = s % LAYERS
+        t = T0 + s // LAYERS
+        q, k, v = hq[(t + l) % POOL]
+        if world == 1:
+            _abi.check(lib.fvsr_ring_step_host(ctx.h, rings.h, l, t, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                               C.byref(md), TOPK, scale, ho.data_ptr(), C.c_void_p(sptr)))
+        else:
+            qd, kd, vd = (x.to(dev, non_blocking=True) for x in (q, k, v))
+            rings.append(l, t, kd, vd)
+            buf = gather.next_shard()
+            rings.attention(l, qd, [t], mask, TOPK, unit_begin=sh.local_unit_begin, unit_end=sh.local_unit_end,
+                            out=buf, tile_major=True, check_errors=False)
+            gather.launch()
+            full = gather.result()
+            ho.view(-1)[: full.numel()].copy_(full.reshape(-1)[: ho.numel()], non_blocking=True)
+            rings.evict(l)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    ctx.check_errors()
+    e2e = {"value": N * e2e_steps / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
+           "path": "fvsr_ring_step_host (C-ABI, pinned host buffers)" if world == 1 else
+                   "python composition over the C-ABI + NCCL gather, pinned host buffers"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel ---------------------------------------------------
+    attn_avg_ms = attn_ms / max(1, attn_n)
+    pairs_per_launch = pairs / max(1, attn_n)
+    achieved = 4.0 * D * pairs_per_launch / (attn_avg_ms / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(HERE, "profiles", "ncu_attention_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"kernel": "sparse_attn_kernel<128>", "bound": "tensor", "achieved": achieved,
+                "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"],
+                "frac_sustained": achieved / pk["bf16_tflops_sustained"] if pk["bf16_tflops_sustained"] else None,
+                "peak_source": pk["source"] + " burst bf16 (MEASURED_PEAKS.json)", "traffic": traffic,
+                "flops_per_launch": 4.0 * D * pairs_per_launch,
+                "flop_def": "4*d per executed (mask-allowed, selected-block) token pair, counted by the kernel",
+                "avg_launch_us": attn_avg_ms * 1e3, "launches": attn_n}
+    mb_avg = mb_ms / max(1, mb_n)
+    bnk = 3 * tiles  # context {28..32}: t_rows 14, 15, 16
+    mb_bytes = nh * N * D * 2 + nh * bnk * D * 4 + nh * tiles * TOPK * 4  # Q once, pooled K, indices
+    mask_builder = {"avg_us": mb_avg * 1e3, "algorithmic_bytes": mb_bytes,
+                    "gbs": mb_bytes / (mb_avg / 1e3) / 1e9 if mb_avg > 0 else None, "peak_gbs": pk["hbm_gbs"]}
+    ap_avg = ap_ms / max(1, ap_n)
+    ap_bytes = 2 * 2 * nh * N * D * 2 + nh * tiles * D * 4 * 2
+    append = {"avg_us": ap_avg * 1e3, "algorithmic_bytes": ap_bytes,
+              "gbs": ap_bytes / (ap_avg / 1e3) / 1e9 if ap_avg > 0 else None}
+
+    # ---- CPU baseline (reference on host cores, rank 0, N=1 only) ----------------------------
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        threads = cpu_threads()
+        med, kind, threads_used, times = time_reference_heads(args.cpu_heads, threads)
+        cpu = {"value": N / (HEADS * med), "unit": "tokens/s", "cores": threads_used, "kind": kind,
+               "sample": f"{args.cpu_heads} single-head head_attention calls of the same step (partition, mask, "
+                         f"plan_sparse, sparse_attention_exec), median {med*1e3:.1f} ms/head x 12 heads, "
+                         f"threads={threads_used}, {cpu_model()}"}
+
+    line = {
+        "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1) bf16 (torch.Generator seed 2510, 4-frame pool)",
+        "config": {"workload": WORKLOAD, "heads": HEADS, "d": D, "latent": [ROWS, COLS], "window": WINDOW,
+                   "topk": TOPK, "mask": "all", "layers_cycled": LAYERS,
+                   "l2": "inputs larger than L2: steps cycle 30 layer rings (127 MB each, 3.8 GB)",
+                   "parallelism": f"head-parallel x{world}" if world > 1 else "single GPU"},
+        "eff_tflops": eff_tflops,
+        "roofline": roofline,
+        "mask_builder": mask_builder,
+        "kv_append": append,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clocks.summary(),
+        "gpu_launches": launches,
+        "executed_pairs_per_step": pairs_total / args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=600)
+    ap.add_argument("--warmup", type=int, default=30)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=120)
+    ap.add_argument("--cpu-heads", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

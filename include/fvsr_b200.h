@@ -100,6 +100,16 @@ typedef struct {
 
 enum { FVSR_FLAG_SYNC_CHECK = 1 };
 
+/* Output layouts of fvsr_ring_attention. */
+enum {
+  FVSR_OUT_TOKEN_MAJOR = 0, /* [heads][Lq][d] in TokenGrid order */
+  FVSR_OUT_TILE_MAJOR = 1   /* [unit - unit_begin][64][d], one 8x8 query tile per unit (padding rows
+                               included): each rank's shard is contiguous for the NCCL all-gather */
+};
+
+/* Kernel classes timed by fvsr_ctx_timing_enable. */
+enum { FVSR_TIME_APPEND = 0, FVSR_TIME_MASK_BUILDER = 1, FVSR_TIME_ATTENTION = 2 };
+
 typedef struct fvsr_ctx fvsr_ctx;
 typedef struct fvsr_ring fvsr_ring;
 
@@ -115,6 +125,15 @@ FVSR_API int32_t fvsr_ctx_set_flags(fvsr_ctx* ctx, int32_t flags);
 FVSR_API int32_t fvsr_check_errors(fvsr_ctx* ctx, fvsr_stream_t stream);
 /* Number of kernel launches this context has issued (instrumentation for benches). */
 FVSR_API int64_t fvsr_ctx_launch_count(const fvsr_ctx* ctx);
+/* When enabled, every append / mask-builder / attention call records a CUDA-event span on
+ * its own stream; fvsr_ctx_timing_read synchronizes the device and returns the summed
+ * milliseconds and span count of one class (FVSR_TIME_*), optionally clearing all spans. */
+FVSR_API int32_t fvsr_ctx_timing_enable(fvsr_ctx* ctx, int32_t enable);
+FVSR_API int32_t fvsr_ctx_timing_read(fvsr_ctx* ctx, int32_t kind, double* total_ms, int64_t* count,
+                                      int32_t clear);
+/* Executed (mask-allowed, selected-block) token pairs counted by the attention kernel since
+ * the last read — the reference's sparsity_report definition; synchronizes and resets. */
+FVSR_API int32_t fvsr_ctx_read_pairs(fvsr_ctx* ctx, uint64_t* executed_pairs);
 
 /* ---- geometry (host only) ----------------------------------------------------------- */
 /* Block counts of partition_blocks(grid_q) / partition_blocks(grid_k) (P/src/partition.cpp:38-62). */
@@ -181,12 +200,12 @@ FVSR_API int32_t fvsr_ring_frame_ids(const fvsr_ring* ring, int32_t layer, int32
  * out likewise.  sel/sel_count (DEVICE, optional) receive the plan as fvsr_plan_sparse would.
  * unit_begin/unit_end restrict the work to a range of (head, q-tile) units, unit =
  * head * (nq * tiles) + frame * tiles + tile (head-parallel sharding; pass 0, -1 for all);
- * rows of units outside the range are left untouched. */
+ * rows of units outside the range are left untouched.  out_layout: FVSR_OUT_*. */
 FVSR_API int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer, const uint16_t* q,
                             const int32_t* q_frame_ids, int32_t nq, const fvsr_mask* mask,
                             int64_t topk, float scale, int64_t unit_begin, int64_t unit_end,
-                            uint16_t* out, int32_t sel_cap, int32_t* sel, int32_t* sel_count,
-                            fvsr_stream_t stream);
+                            uint16_t* out, int32_t out_layout, int32_t sel_cap, int32_t* sel,
+                            int32_t* sel_count, fvsr_stream_t stream);
 
 /* One streaming layer-step from HOST buffers (the end-to-end path): H2D copy of the new
  * frame's q/k/v ([heads][rows*cols][d] bf16; pinned memory recommended), ring append,

@@ -26,6 +26,8 @@ FVSR_E_NOMEM = 8
 MASK_ALL, MASK_LOCALITY, MASK_BITMASK = 0, 1, 2
 LOCALITY_PRESERVED, LOCALITY_TRUNCATED = 0, 1
 FLAG_SYNC_CHECK = 1
+OUT_TOKEN_MAJOR, OUT_TILE_MAJOR = 0, 1
+TIME_APPEND, TIME_MASK_BUILDER, TIME_ATTENTION = 0, 1, 2
 
 
 class Error(RuntimeError):
@@ -85,6 +87,9 @@ SIGNATURES = {
     "fvsr_ctx_set_flags": (I32, [P, I32]),
     "fvsr_check_errors": (I32, [P, P]),
     "fvsr_ctx_launch_count": (I64, [P]),
+    "fvsr_ctx_timing_enable": (I32, [P, I32]),
+    "fvsr_ctx_timing_read": (I32, [P, I32, C.POINTER(C.c_double), C.POINTER(I64), I32]),
+    "fvsr_ctx_read_pairs": (I32, [P, C.POINTER(C.c_uint64)]),
     "fvsr_block_counts": (I32, [GP, GP, C.POINTER(I32), C.POINTER(I32)]),
     "fvsr_plan_sparse": (I32, [P, P, P, I32, I32, GP, GP, MP, I64, I32, P, P, P, P, P, P]),
     "fvsr_sparse_attention_exec": (I32, [P, P, P, P, I32, I32, GP, GP, MP, I32, P, P, F32, I64, I64, P, P]),
@@ -94,7 +99,8 @@ SIGNATURES = {
     "fvsr_ring_append": (I32, [P, P, I32, I32, P, P, P]),
     "fvsr_ring_evict_sliding": (I32, [P, I32]),
     "fvsr_ring_frame_ids": (I32, [P, I32, C.POINTER(I32), I32, C.POINTER(I32)]),
-    "fvsr_ring_attention": (I32, [P, P, I32, P, C.POINTER(I32), I32, MP, I64, F32, I64, I64, P, I32, P, P, P]),
+    "fvsr_ring_attention": (I32, [P, P, I32, P, C.POINTER(I32), I32, MP, I64, F32, I64, I64, P, I32, I32, P, P,
+                                  P]),
     "fvsr_ring_step_host": (I32, [P, P, I32, I32, P, P, P, MP, I64, F32, P, P]),
 }
 

@@ -69,6 +69,13 @@ struct fvsr_ctx {
   int device = 0;
   int flags = 0;
   unsigned* d_err = nullptr;
+  unsigned long long* d_pairs = nullptr;  // executed token pairs, accumulated by the attention kernel
+  // optional CUDA-event spans per kernel class (fvsr_ctx_timing_enable)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Span { cudaEvent_t a, b; int kind; };
+  std::vector<Span> spans;
   long long launches = 0;
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -245,6 +252,35 @@ int npow2(int n) {
   return p;
 }
 
+// ---- CUDA-event spans on the launching stream ------------------------------------------
+struct SpanGuard {
+  fvsr_ctx* ctx;
+  cudaStream_t s;
+  int kind;
+  cudaEvent_t a = nullptr;
+  cudaEvent_t take() {
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ctx->ev_pool.push_back(e);
+    }
+    return ctx->ev_pool[ctx->ev_used++];
+  }
+  SpanGuard(fvsr_ctx* c, cudaStream_t st, int k) : ctx(c), s(st), kind(k) {
+    if (ctx->timing) {
+      a = take();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~SpanGuard() {
+    if (ctx->timing && a) {
+      cudaEvent_t b = take();
+      cudaEventRecord(b, s);
+      ctx->spans.push_back({a, b, kind});
+    }
+  }
+};
+
 // ---- launch helpers ---------------------------------------------------------------------
 void launch_pack(const uint16_t* src, long long src_head_stride, int heads, int nframes, const DevGeom& g,
                  uint8_t* dst, long long dst_head_stride, const int* slots, cudaStream_t s) {
@@ -357,11 +393,14 @@ int32_t fvsr_ctx_create(fvsr_ctx** out) {
                 prop.name);
   auto* c = new fvsr_ctx();
   c->device = dev;
-  if (cudaMalloc(&c->d_err, sizeof(unsigned)) != cudaSuccess) {
+  if (cudaMalloc(&c->d_err, sizeof(unsigned)) != cudaSuccess ||
+      cudaMalloc(&c->d_pairs, sizeof(unsigned long long)) != cudaSuccess) {
+    cudaFree(c->d_err);
     delete c;
     return fail(FVSR_E_NOMEM, "error word allocation failed");
   }
   cudaMemset(c->d_err, 0, sizeof(unsigned));
+  cudaMemset(c->d_pairs, 0, sizeof(unsigned long long));
   *out = c;
   return FVSR_OK;
 }
@@ -369,6 +408,8 @@ int32_t fvsr_ctx_create(fvsr_ctx** out) {
 void fvsr_ctx_destroy(fvsr_ctx* ctx) {
   if (!ctx) return;
   cudaFree(ctx->d_err);
+  cudaFree(ctx->d_pairs);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->stage) cudaFree(ctx->stage);
   delete ctx;
@@ -381,6 +422,43 @@ int32_t fvsr_ctx_set_flags(fvsr_ctx* ctx, int32_t flags) {
 }
 
 int64_t fvsr_ctx_launch_count(const fvsr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int32_t fvsr_ctx_timing_enable(fvsr_ctx* ctx, int32_t enable) {
+  if (!ctx) return fail(FVSR_E_CONFIG, "null context");
+  ctx->timing = enable != 0;
+  return FVSR_OK;
+}
+
+int32_t fvsr_ctx_timing_read(fvsr_ctx* ctx, int32_t kind, double* total_ms, int64_t* count, int32_t clear) {
+  FVSR_TRY(check_ctx(ctx));
+  FVSR_CUDA(cudaDeviceSynchronize());
+  double ms = 0.0;
+  int64_t n = 0;
+  for (const auto& sp : ctx->spans) {
+    if (sp.kind != kind) continue;
+    float e = 0.f;
+    FVSR_CUDA(cudaEventElapsedTime(&e, sp.a, sp.b));
+    ms += e;
+    ++n;
+  }
+  if (total_ms) *total_ms = ms;
+  if (count) *count = n;
+  if (clear) {
+    ctx->spans.clear();
+    ctx->ev_used = 0;
+  }
+  return FVSR_OK;
+}
+
+int32_t fvsr_ctx_read_pairs(fvsr_ctx* ctx, uint64_t* executed_pairs) {
+  FVSR_TRY(check_ctx(ctx));
+  FVSR_CUDA(cudaDeviceSynchronize());
+  unsigned long long v = 0;
+  FVSR_CUDA(cudaMemcpy(&v, ctx->d_pairs, sizeof(v), cudaMemcpyDeviceToHost));
+  FVSR_CUDA(cudaMemset(ctx->d_pairs, 0, sizeof(v)));
+  if (executed_pairs) *executed_pairs = v;
+  return FVSR_OK;
+}
 
 int32_t fvsr_check_errors(fvsr_ctx* ctx, fvsr_stream_t stream) {
   FVSR_TRY(check_ctx(ctx));
@@ -484,8 +562,13 @@ int32_t fvsr_sparse_attention_exec(fvsr_ctx* ctx, const uint16_t* q, const uint1
   p.row_end = row_end;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.unit_begin = 0;
+  p.out_tile_major = 0;
   p.err = ctx->d_err;
-  FVSR_TRY(launch_attn(g, dm, p, (long long)heads * g.nqf * g.n_tiles, s));
+  p.pairs = ctx->d_pairs;
+  {
+    SpanGuard sg(ctx, s, FVSR_TIME_ATTENTION);
+    FVSR_TRY(launch_attn(g, dm, p, (long long)heads * g.nqf * g.n_tiles, s));
+  }
   return after_launch(ctx, s, 4);
 }
 
@@ -585,6 +668,7 @@ int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t fra
   g.d = r->d;
   const long long N = (long long)r->rows * r->cols;
   const int slots1[1] = {slot};
+  SpanGuard sg(ctx, s, FVSR_TIME_APPEND);
   launch_pack(k, N * r->d, r->heads, 1, g, r->k_layer(layer), r->kv_head_stride(), slots1, s);
   launch_pack(v, N * r->d, r->heads, 1, g, r->v_layer(layer), r->kv_head_stride(), slots1, s);
   PoolGroups pg{};
@@ -625,8 +709,8 @@ int32_t fvsr_ring_frame_ids(const fvsr_ring* r, int32_t layer, int32_t* ids, int
 
 int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const uint16_t* q,
                             const int32_t* q_frame_ids, int32_t nq, const fvsr_mask* mask, int64_t topk, float scale,
-                            int64_t unit_begin, int64_t unit_end, uint16_t* out, int32_t sel_cap, int32_t* sel,
-                            int32_t* sel_count, fvsr_stream_t stream) {
+                            int64_t unit_begin, int64_t unit_end, uint16_t* out, int32_t out_layout,
+                            int32_t sel_cap, int32_t* sel, int32_t* sel_count, fvsr_stream_t stream) {
   FVSR_TRY(check_ctx(ctx));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (!r || !q || !out || !q_frame_ids) return fail(FVSR_E_SHAPE, "ring_attention: null argument");
@@ -666,13 +750,16 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   int* use_sel = sel ? sel : wsel;
   int* use_cnt = sel_count ? sel_count : wcnt;
 
-  launch_pack(q, Lq * d, r->heads, g.nqf, g, qp, (long long)g.nqf * g.n_tiles * tb, nullptr, s);
-  launch_pool_trows(q, Lq * d, r->heads, g.q_tr_first, g.q_tr_count, g.nq_trows, g, nullptr, qs0, qs1,
-                    (long long)g.nqf * g.n_tiles * d, s);
-  const float cscale = 1.0f / std::sqrt(static_cast<float>(d));
-  FVSR_TRY(launch_select(ctx, g, dm, r->heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, r->s0_layer(layer),
-                         r->s1_layer(layer), r->part_head_stride(), cscale, topk, cap, use_sel, use_cnt, nullptr,
-                         nullptr, nullptr, s));
+  {
+    SpanGuard sg(ctx, s, FVSR_TIME_MASK_BUILDER);
+    launch_pack(q, Lq * d, r->heads, g.nqf, g, qp, (long long)g.nqf * g.n_tiles * tb, nullptr, s);
+    launch_pool_trows(q, Lq * d, r->heads, g.q_tr_first, g.q_tr_count, g.nq_trows, g, nullptr, qs0, qs1,
+                      (long long)g.nqf * g.n_tiles * d, s);
+    const float cscale = 1.0f / std::sqrt(static_cast<float>(d));
+    FVSR_TRY(launch_select(ctx, g, dm, r->heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, r->s0_layer(layer),
+                           r->s1_layer(layer), r->part_head_stride(), cscale, topk, cap, use_sel, use_cnt, nullptr,
+                           nullptr, nullptr, s));
+  }
   const long long units_total = (long long)r->heads * g.nqf * g.n_tiles;
   if (unit_end < 0 || unit_end > units_total) unit_end = units_total;
   if (unit_begin < 0 || unit_begin > unit_end) return fail(FVSR_E_CONFIG, "ring_attention: bad unit range");
@@ -691,8 +778,13 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   p.row_end = Lq;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.unit_begin = unit_begin;
+  p.out_tile_major = out_layout == FVSR_OUT_TILE_MAJOR ? 1 : 0;
   p.err = ctx->d_err;
-  FVSR_TRY(launch_attn(g, dm, p, unit_end - unit_begin, s));
+  p.pairs = ctx->d_pairs;
+  {
+    SpanGuard sg(ctx, s, FVSR_TIME_ATTENTION);
+    FVSR_TRY(launch_attn(g, dm, p, unit_end - unit_begin, s));
+  }
   return after_launch(ctx, s, 4);
 }
 
@@ -720,8 +812,8 @@ int32_t fvsr_ring_step_host(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t 
   FVSR_CUDA(cudaMemcpyAsync(dv, v_host, bytes, cudaMemcpyHostToDevice, s));
   FVSR_TRY(fvsr_ring_append(ctx, r, layer, frame_id, dk, dv, stream));
   const int32_t qids[1] = {frame_id};
-  FVSR_TRY(fvsr_ring_attention(ctx, r, layer, dq, qids, 1, mask, topk, scale, 0, -1, dout, 0, nullptr, nullptr,
-                               stream));
+  FVSR_TRY(fvsr_ring_attention(ctx, r, layer, dq, qids, 1, mask, topk, scale, 0, -1, dout, FVSR_OUT_TOKEN_MAJOR, 0,
+                               nullptr, nullptr, stream));
   FVSR_TRY(fvsr_ring_evict_sliding(r, layer));
   FVSR_CUDA(cudaMemcpyAsync(out_host, dout, bytes, cudaMemcpyDeviceToHost, s));
   return FVSR_OK;

@@ -52,7 +52,9 @@ struct AttnParams {
   long long row_begin, row_end;
   float scale_log2;         // scale * log2(e)
   long long unit_begin;
+  int out_tile_major;       // 1: out is [unit - unit_begin][64][d] (head-parallel gather layout)
   unsigned* err;
+  unsigned long long* pairs;// += executed (mask-allowed) token pairs, reference definition
 };
 
 template <int D>
@@ -253,6 +255,14 @@ __global__ void __launch_bounds__(192, 1) sparse_attn_kernel(DevGeom g, DevMask 
 #pragma unroll
     for (int q = 0; q < 64; ++q) lpart[q] = 0.0f;
     const int r_in_tile = j & 63;
+    // query columns that are real tokens (ragged tiles have padding rows)
+    uint32_t qv_lo = 0, qv_hi = 0;
+#pragma unroll
+    for (int q = 0; q < 64; ++q) {
+      const bool ok = (qh0 + (q >> 3)) < g.rows && (qw0 + (q & 7)) < g.cols;
+      if (ok) { if (q < 32) qv_lo |= 1u << q; else qv_hi |= 1u << (q - 32); }
+    }
+    unsigned long long my_pairs = 0;
 
     for (int t = 0; t < n; ++t) {
       const int sb = t & 1;
@@ -294,6 +304,8 @@ __global__ void __launch_bounds__(192, 1) sparse_attn_kernel(DevGeom g, DevMask 
           }
         }
       }
+
+      my_pairs += __popc(mlo & qv_lo) + __popc(mhi & qv_hi);
 
       // ---- S^T row j -> registers ----------------------------------------------------
       mbar_wait(s_full + sb, (t >> 1) & 1);
@@ -380,6 +392,11 @@ __global__ void __launch_bounds__(192, 1) sparse_attn_kernel(DevGeom g, DevMask 
     }
 
     // ---- epilogue ------------------------------------------------------------------------
+    if (p.pairs) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
+      if (lane == 0 && my_pairs) atomicAdd(p.pairs, my_pairs);
+    }
     warp_colreduce64<false>(lpart, lane);
     red[warp * 64 + colreduce_col(lane, 0)] = lpart[0];
     red[warp * 64 + colreduce_col(lane, 1)] = lpart[1];
@@ -418,8 +435,14 @@ __global__ void __launch_bounds__(192, 1) sparse_attn_kernel(DevGeom g, DevMask 
     }
     named_bar_sync(1, 128);
     constexpr int kChunks = D / 8;
+    if (p.out_tile_major) {
+      // unit-contiguous rows (padding rows included) for the head-parallel all-gather
+      uint16_t* outu = p.out + (long long)blockIdx.x * 64 * D;
+      for (int idx = j; idx < 64 * kChunks; idx += 128)
+        *reinterpret_cast<uint4*>(outu + idx * 8) = *reinterpret_cast<const uint4*>(so + idx * 8);
+    }
     uint16_t* outh = p.out + head * p.out_head_stride;
-    for (int idx = j; idx < 64 * kChunks; idx += 128) {
+    for (int idx = j; idx < 64 * kChunks && !p.out_tile_major; idx += 128) {
       const int q = idx / kChunks, ch = idx % kChunks;
       const int qh = qh0 + (q >> 3), qw = qw0 + (q & 7);
       if (qh < g.rows && qw < g.cols) {

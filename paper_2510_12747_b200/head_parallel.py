@@ -1,0 +1,121 @@
+"""Head-parallel sharding of the streaming attention layer-step over N GPUs of one node.
+
+The reference processes heads serially (P/src/stream.cpp:237-256; P =
+/root/reference/proj); heads and, within a head, query tiles are independent given K/V,
+so the (head, q-tile) work units shard with no exchange except gathering the outputs.
+
+    units  = heads * nq * tiles            (unit = head*(nq*tiles) + frame*tiles + tile)
+    rank r owns units [r*per, min(U, (r+1)*per)), per = ceil(U / N)
+    ring   = KV for heads [h0, h1) that its units touch (a head split across two ranks
+             has its K/V on both; 12 heads over 8 GPUs split 1.5 heads per rank)
+    output = tile-major shard [per, 64, d]  ->  NCCL all_gather_into_tensor (equal chunks)
+             -> untile() back to [heads, Lq, d] token order when a consumer needs it.
+
+The gather of layer l runs on NCCL's stream while layer l+1 computes (async_op, double
+buffered); the step's host code never waits on it until the buffer is reused.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Tuple
+
+import torch
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    total_units: int
+    per: int          # units per rank (padded)
+    u0: int           # first unit owned
+    u1: int           # one past the last unit owned
+    units_per_head: int
+    h0: int           # first head touched
+    h1: int           # one past the last head touched
+
+    @property
+    def local_unit_begin(self) -> int:
+        return self.u0 - self.h0 * self.units_per_head
+
+    @property
+    def local_unit_end(self) -> int:
+        return self.u1 - self.h0 * self.units_per_head
+
+    @property
+    def heads(self) -> int:
+        return self.h1 - self.h0
+
+
+def shard(total_units: int, units_per_head: int, world: int, rank: int) -> Shard:
+    per = -(-total_units // world)
+    u0 = min(total_units, rank * per)
+    u1 = min(total_units, u0 + per)
+    if u1 > u0:
+        h0, h1 = u0 // units_per_head, (u1 - 1) // units_per_head + 1
+    else:
+        h0 = h1 = 0
+    return Shard(rank, world, total_units, per, u0, u1, units_per_head, h0, h1)
+
+
+def untile_index(heads: int, nq: int, rows: int, cols: int, device=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """(src_row, dst_row) index pairs mapping tile-major rows [units*64] to token-major rows
+    [heads*nq*rows*cols]; padding rows of ragged tiles are dropped."""
+    tw, th = (cols + 7) // 8, (rows + 7) // 8
+    tiles = tw * th
+    u = torch.arange(heads * nq * tiles, device=device)
+    r = torch.arange(64, device=device)
+    head = (u // (nq * tiles))[:, None]
+    f = ((u % (nq * tiles)) // tiles)[:, None]
+    tile = (u % tiles)[:, None]
+    h = (tile // tw) * 8 + r[None, :] // 8
+    w = (tile % tw) * 8 + r[None, :] % 8
+    valid = (h < rows) & (w < cols)
+    dst = (head * nq + f) * rows * cols + h * cols + w
+    src = u[:, None] * 64 + r[None, :]
+    return src[valid], dst[valid]
+
+
+def untile(tiles: torch.Tensor, heads: int, nq: int, rows: int, cols: int, index=None) -> torch.Tensor:
+    """Tile-major [>=units, 64, d] -> token-major [heads, nq*rows*cols, d]."""
+    d = tiles.shape[-1]
+    src, dst = index if index is not None else untile_index(heads, nq, rows, cols, tiles.device)
+    out = torch.empty((heads * nq * rows * cols, d), dtype=tiles.dtype, device=tiles.device)
+    out[dst] = tiles.reshape(-1, d)[src]
+    return out.view(heads, nq * rows * cols, d)
+
+
+class Gatherer:
+    """Double-buffered async all-gather of tile-major shards (torch.distributed, NCCL/gloo)."""
+
+    def __init__(self, sh: Shard, d: int, device, dtype=torch.bfloat16, group=None):
+        self.sh, self.group = sh, group
+        self.shards = [torch.zeros((sh.per, 64, d), dtype=dtype, device=device) for _ in range(2)]
+        self.full = [torch.empty((sh.per * sh.world, 64, d), dtype=dtype, device=device) for _ in range(2)]
+        self.work = [None, None]
+        self.i = 0
+
+    def next_shard(self) -> torch.Tensor:
+        """Shard buffer for the next layer-step; waits for the gather that last used it."""
+        self.i ^= 1
+        if self.work[self.i] is not None:
+            self.work[self.i].wait()
+            self.work[self.i] = None
+        return self.shards[self.i]
+
+    def launch(self) -> None:
+        import torch.distributed as dist
+        self.work[self.i] = dist.all_gather_into_tensor(self.full[self.i], self.shards[self.i], group=self.group,
+                                                        async_op=True)
+
+    def result(self) -> torch.Tensor:
+        if self.work[self.i] is not None:
+            self.work[self.i].wait()
+            self.work[self.i] = None
+        return self.full[self.i][: self.sh.total_units]
+
+    def drain(self) -> None:
+        for i in range(2):
+            if self.work[i] is not None:
+                self.work[i].wait()
+                self.work[i] = None

@@ -70,8 +70,9 @@ class KVRing:
 
     def attention(self, layer: int, q: torch.Tensor, q_frame_ids: Sequence[int], mask: Optional[Mask] = None,
                   topk: int = 1, scale: Optional[float] = None, *, unit_begin: int = 0, unit_end: int = -1,
-                  out: Optional[torch.Tensor] = None, sel: Optional[torch.Tensor] = None,
-                  sel_count: Optional[torch.Tensor] = None, check_errors: bool = True) -> torch.Tensor:
+                  out: Optional[torch.Tensor] = None, tile_major: bool = False,
+                  sel: Optional[torch.Tensor] = None, sel_count: Optional[torch.Tensor] = None,
+                  check_errors: bool = True) -> torch.Tensor:
         mask = mask or Mask.all_allowed()
         q3 = _heads3(q, "ring attention q")
         nq = len(q_frame_ids)
@@ -80,13 +81,19 @@ class KVRing:
         if scale is None:
             scale = 1.0 / math.sqrt(self.d)
         if out is None:
-            out = torch.empty_like(q3)
+            if tile_major:
+                tiles = ((self.rows + 7) // 8) * ((self.cols + 7) // 8)
+                total = self.heads * nq * tiles
+                u1 = total if unit_end < 0 else min(unit_end, total)
+                out = torch.empty(((u1 - unit_begin), 64, self.d), dtype=torch.bfloat16, device=q3.device)
+            else:
+                out = torch.empty_like(q3)
         ids = (C.c_int32 * nq)(*[int(f) for f in q_frame_ids])
         md = mask.c()
         cap = sel.shape[-1] if sel is not None else 0
         check(self.ctx.lib.fvsr_ring_attention(self.ctx.h, self.h, layer, q3.data_ptr(), ids, nq, C.byref(md),
                                                int(topk), float(scale), int(unit_begin), int(unit_end),
-                                               out.data_ptr(), cap, sel.data_ptr() if sel is not None else None,
+                                               out.data_ptr(), 1 if tile_major else 0, cap, sel.data_ptr() if sel is not None else None,
                                                sel_count.data_ptr() if sel_count is not None else None, _stream()))
         if check_errors:
             self.ctx.check_errors()

@@ -157,6 +157,19 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.fvsr_ctx_launch_count(self.h))
 
+    def timing(self, enable: bool) -> None:
+        check(self.lib.fvsr_ctx_timing_enable(self.h, 1 if enable else 0))
+
+    def timing_read(self, kind: int, clear: bool = False):
+        ms, n = C.c_double(), C.c_int64()
+        check(self.lib.fvsr_ctx_timing_read(self.h, kind, C.byref(ms), C.byref(n), 1 if clear else 0))
+        return ms.value, n.value
+
+    def read_pairs(self) -> int:
+        v = C.c_uint64()
+        check(self.lib.fvsr_ctx_read_pairs(self.h, C.byref(v)))
+        return v.value
+
     def __del__(self):
         try:
             if getattr(self, "h", None):
