@@ -342,23 +342,55 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
   return FVSR_OK;
 }
 
-template <int D>
-int launch_attn_d(const DevGeom& g, const DevMask& dm, const AttnParams& p, long long units, cudaStream_t s) {
+template <int D, int NQ>
+int launch_attn_dq(const DevGeom& g, const DevMask& dm, const AttnParams& p, int sms, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)AttnCfg<D>::kBytes));
+    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)AttnCfg<D, NQ>::kBytes));
     configured = true;
   }
+  const long long units = p.unit_end - p.unit_begin;
   if (units <= 0) return FVSR_OK;
-  sparse_attn_kernel<D><<<(unsigned)units, 192, AttnCfg<D>::kBytes, s>>>(g, dm, p);
+  const unsigned grid = (unsigned)std::min<long long>(units, sms);  // persistent CTAs
+  sparse_attn_kernel<D, NQ><<<grid, kThreads, AttnCfg<D, NQ>::kBytes, s>>>(g, dm, p);
   return FVSR_OK;
 }
 
-int launch_attn(const DevGeom& g, const DevMask& dm, const AttnParams& p, long long units, cudaStream_t s) {
-  if (g.d == 128) return launch_attn_d<128>(g, dm, p, units, s);
-  if (g.d == 64) return launch_attn_d<64>(g, dm, p, units, s);
-  return fail(FVSR_E_CONFIG, "sparse_attention_exec: head_dim %d unsupported (64 or 128)", g.d);
+bool trows_uniform(const DevGeom& g) {
+  for (int a = 1; a < g.nq_trows; ++a)
+    if (g.q_tr_count[a] != g.q_tr_count[0]) return false;
+  return true;
+}
+
+// One persistent launch per query-tile height: NQ=64 for temporal rows holding one query
+// frame, NQ=128 for rows holding two.  unit_begin/unit_end index the unit space
+// head * (n_trows * tiles) + trow * tiles + tile and require uniform rows.
+int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnParams p, int heads,
+                     long long unit_begin, long long unit_end, cudaStream_t s) {
+  if (g.d != 64 && g.d != 128)
+    return fail(FVSR_E_CONFIG, "sparse_attention_exec: head_dim %d unsupported (64 or 128)", g.d);
+  const bool uniform = trows_uniform(g);
+  int sms = 0;
+  FVSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  SpanGuard sg(ctx, s, FVSR_TIME_ATTENTION);
+  for (int nq = 1; nq <= 2; ++nq) {
+    p.n_trows = 0;
+    for (int a = 0; a < g.nq_trows; ++a)
+      if (g.q_tr_count[a] == nq) p.trow_list[p.n_trows++] = a;
+    if (!p.n_trows) continue;
+    const long long total = (long long)heads * p.n_trows * g.n_tiles;
+    p.unit_begin = uniform ? std::max(0ll, unit_begin) : 0;
+    p.unit_end = uniform ? (unit_end < 0 ? total : std::min(unit_end, total)) : total;
+    int st;
+    if (g.d == 128)
+      st = nq == 1 ? launch_attn_dq<128, 64>(g, dm, p, sms, s) : launch_attn_dq<128, 128>(g, dm, p, sms, s);
+    else
+      st = nq == 1 ? launch_attn_dq<64, 64>(g, dm, p, sms, s) : launch_attn_dq<64, 128>(g, dm, p, sms, s);
+    FVSR_TRY(st);
+    ctx->launches += 1;
+  }
+  return FVSR_OK;
 }
 
 int check_ctx(fvsr_ctx* ctx) {
@@ -565,11 +597,8 @@ int32_t fvsr_sparse_attention_exec(fvsr_ctx* ctx, const uint16_t* q, const uint1
   p.out_tile_major = 0;
   p.err = ctx->d_err;
   p.pairs = ctx->d_pairs;
-  {
-    SpanGuard sg(ctx, s, FVSR_TIME_ATTENTION);
-    FVSR_TRY(launch_attn(g, dm, p, (long long)heads * g.nqf * g.n_tiles, s));
-  }
-  return after_launch(ctx, s, 4);
+  FVSR_TRY(launch_attention(ctx, g, dm, p, heads, 0, -1, s));
+  return after_launch(ctx, s, 3);
 }
 
 int32_t fvsr_sparsity_report(fvsr_ctx* ctx, int32_t heads, const fvsr_grid* grid_q, const fvsr_grid* grid_k,
@@ -760,9 +789,11 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
                            r->s1_layer(layer), r->part_head_stride(), cscale, topk, cap, use_sel, use_cnt, nullptr,
                            nullptr, nullptr, s));
   }
-  const long long units_total = (long long)r->heads * g.nqf * g.n_tiles;
+  const long long units_total = (long long)r->heads * g.nq_trows * g.n_tiles;
   if (unit_end < 0 || unit_end > units_total) unit_end = units_total;
   if (unit_begin < 0 || unit_begin > unit_end) return fail(FVSR_E_CONFIG, "ring_attention: bad unit range");
+  if (!trows_uniform(g) && (unit_begin != 0 || unit_end != units_total || out_layout == FVSR_OUT_TILE_MAJOR))
+    return fail(FVSR_E_CONFIG, "ring_attention: unit ranges / tile-major output need query rows of equal height");
   AttnParams p{};
   p.q = qp;
   p.q_head_stride = (long long)g.nqf * g.n_tiles * tb;
@@ -777,15 +808,11 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   p.row_begin = 0;
   p.row_end = Lq;
   p.scale_log2 = scale * 1.4426950408889634f;
-  p.unit_begin = unit_begin;
   p.out_tile_major = out_layout == FVSR_OUT_TILE_MAJOR ? 1 : 0;
   p.err = ctx->d_err;
   p.pairs = ctx->d_pairs;
-  {
-    SpanGuard sg(ctx, s, FVSR_TIME_ATTENTION);
-    FVSR_TRY(launch_attn(g, dm, p, unit_end - unit_begin, s));
-  }
-  return after_launch(ctx, s, 4);
+  FVSR_TRY(launch_attention(ctx, g, dm, p, r->heads, unit_begin, unit_end, s));
+  return after_launch(ctx, s, 3);
 }
 
 int32_t fvsr_ring_step_host(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* q_host,

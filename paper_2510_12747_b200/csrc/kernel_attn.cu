@@ -6,80 +6,127 @@
 // with a running max.  Rows outside [row_begin, row_end) are zero; a row whose selected
 // blocks hold no allowed key latches DegenerateRowError (sparse.cpp:198-200).
 //
-// Work unit: one 64-row query frame-tile (the reference's streaming q-block is one
-// frame's 8x8 tile, 64 rows).  tcgen05 issues M in {64,128} and M=64 runs at half rate,
-// so the kernel is TRANSPOSED: keys sit on the M=128 axis.
-//     S^T[128 keys x 64 q]  = K_tile[128 x d]   . Q_tile[64 x d]^T       (K-major A, K-major B)
-//     O^T[d x 64 q]        += V_tile^T[d x 128] . P^T[128 keys x 64 q]   (MN-major A, MN-major B)
-// Both MMAs are M=128, N=64 — full tensor-core rate — and a key block is exactly one
-// 128-row tile (frames 2m and 2m+1 of one spatial 8x8 tile; 64 rows when only one frame
-// of the pair is in context, in which case PV issues only the 4 valid K=16 steps).
+// Work unit: one query tile position of one head and one temporal row — NQ = 64 query
+// rows (one frame's 8x8 tile, the reference's streaming q-block) or NQ = 128 (the two
+// frames of a (2,8,8) q-block, the paper's 2-latent chunk).  tcgen05 issues M in {64,128}
+// and M=64 runs at half rate, so the kernel is TRANSPOSED: keys sit on the M=128 axis.
+//     S^T[128 keys x NQ]  = K_tile[128 x d] . Q^T                 (K-major A, K-major B)
+//     O^T[d x NQ]        += V_tile^T[d x 128] . P^T[128 keys x NQ] (MN-major A, MN-major B)
+// A key block is exactly one 128-row tile (frames 2m, 2m+1 of one 8x8 tile); a 64-row
+// block (one frame of the pair in context) issues only its 4 valid PV K-steps.
 //
-// Softmax in the transposed layout: TMEM lane j holds key j's scores for all 64 queries,
-// so thread j (4 warps = 128 lanes) owns one key row.  Per-query max/sum are column
-// reductions across threads; we avoid one per tile:
-//   * the running reference c_q only moves when some score exceeds it by > 8 (log2
-//     units, FA4-style lazy rescale); detecting that is one CTA-wide OR per tile;
-//   * on the (rare) exceed path — always on the first tile — the exact column max is a
-//     warp butterfly + smem across warps, followed by a rescale of O^T in TMEM and of the
-//     per-thread partial sums;
-//   * the denominators are per-thread partial sums (thread j sums its own key's p over
-//     tiles) reduced once at the end.
+// Softmax in the transposed layout: TMEM lane j holds key j's scores for all queries.
+// 16 softmax warps = 4 lane quarters x 4 column groups; a column group (4 warps, 128
+// lanes) owns NQ/4 query columns and keeps, per column, a running reference c (log2
+// units) and per-thread partial denominators.  The reference only moves when a score
+// exceeds it by > 8 (FA4-style lazy rescale): one OR across the group's 4 warps per tile;
+// on the rare exceed path (always on a column's first real tile) the exact column max is
+// a warp butterfly + smem, then O^T columns in TMEM and the partial sums are rescaled.
+// Denominators are reduced across lanes once per unit.
 //
-// Roles (192 threads): warps 0-3 softmax + epilogue (TMEM lanes 0-127), warp 4 producer
-// (cp.async.bulk of pre-swizzled frame-tiles), warp 5 TMEM allocator + MMA issuer.
+// Persistent CTAs (round-robin over units).  Roles, 576 threads: warps 0-15 softmax +
+// epilogue, warp 16 producer (cp.async.bulk of pre-swizzled frame-tiles), warp 17 TMEM
+// allocator + MMA issuer.  S^T and O^T are double-buffered in TMEM.
 #include "fvsr_common.cuh"
 
 namespace fvsr {
 
-constexpr int kNK = 3;  // K stages
-constexpr int kNV = 2;  // V stages
-constexpr int kNP = 2;  // P^T buffers (== S buffers)
-constexpr uint32_t kTmemCols = 256;
+constexpr int kSoftWarps = 16;
+constexpr int kThreads = kSoftWarps * 32 + 64;
+constexpr int kProducerWarp = kSoftWarps;
+constexpr int kMmaWarp = kSoftWarps + 1;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kInfoCap = 256;              // per-unit tile-info table entries
 
 struct AttnParams {
-  const uint8_t* q;         // packed q frame-tiles [heads][nqf][n_tiles]
-  long long q_head_stride;  // bytes
-  const uint8_t* k;         // packed k frame-tiles [heads][slots][n_tiles]
+  const uint8_t* q;          // packed q frame-tiles [heads][nqf][n_tiles]
+  long long q_head_stride;   // bytes
+  const uint8_t* k;          // packed k frame-tiles [heads][slots][n_tiles]
   const uint8_t* v;
-  long long kv_head_stride; // bytes
-  const int* sel;           // [heads][bnq][cap]
-  const int* sel_count;     // [heads][bnq]
+  long long kv_head_stride;  // bytes
+  const int* sel;            // [heads][bnq][cap]
+  const int* sel_count;      // [heads][bnq]
   int cap;
-  uint16_t* out;            // bf16 [heads][Lq][d]
-  long long out_head_stride;// elements
+  uint16_t* out;             // bf16 [heads][Lq][d] (token major) or [unit][NQ][d] (tile major)
+  long long out_head_stride; // elements
   long long row_begin, row_end;
-  float scale_log2;         // scale * log2(e)
-  long long unit_begin;
-  int out_tile_major;       // 1: out is [unit - unit_begin][64][d] (head-parallel gather layout)
+  float scale_log2;          // scale * log2(e)
+  int n_trows;               // q temporal rows handled by this launch
+  int trow_list[kMaxFrames]; // their indices in the geometry
+  long long unit_begin, unit_end;  // [begin, end) of this launch's unit space
+  int out_tile_major;        // 1: out is [unit - unit_begin][NQ][d]
   unsigned* err;
-  unsigned long long* pairs;// += executed (mask-allowed) token pairs, reference definition
+  unsigned long long* pairs; // += executed (mask-allowed, selected-block) token pairs
 };
 
-template <int D>
+template <int D, int NQ>
 struct AttnCfg {
-  static constexpr uint32_t kTileBytes = D * 128;        // one packed frame-tile
-  static constexpr uint32_t kQBytes = kTileBytes;        // 64 rows
-  static constexpr uint32_t kKVBytes = 2 * kTileBytes;   // 128 rows
-  static constexpr uint32_t kPBytes = 128 * 128;         // 128 keys x 64 q bf16
+  static constexpr int kNK = NQ == 64 ? 3 : 2;       // K stages
+  static constexpr int kNV = 2;                      // V stages
+  static constexpr int kNP = NQ == 64 ? 2 : 1;       // P^T buffers
+  static constexpr int kCPT = NQ / 4;                // query columns per softmax thread
+  static constexpr uint32_t kTileBytes = D * 128;    // one packed 64-row frame-tile
+  static constexpr uint32_t kQSub = NQ * 128;        // Q sub-tile stride (NQ rows x 128 B)
+  static constexpr uint32_t kQBytes = (D / 64) * kQSub;
+  static constexpr uint32_t kKVBytes = 2 * kTileBytes;  // 128 rows
+  static constexpr uint32_t kPBytes = NQ * 256;      // 128 keys x NQ bf16 (also the O staging tile)
   static constexpr uint32_t kOffQ = 0;
   static constexpr uint32_t kOffK = kOffQ + kQBytes;
   static constexpr uint32_t kOffV = kOffK + kNK * kKVBytes;
   static constexpr uint32_t kOffP = kOffV + kNV * kKVBytes;
-  static constexpr uint32_t kOffBar = kOffP + kNP * kPBytes;
-  static constexpr uint32_t kScratch = 2048;                 // barriers, softmax scratch
-  static constexpr uint32_t kBytes = kOffBar + kScratch + 1024;  // + alignment slack
+  static constexpr uint32_t kOffS = kOffP + kNP * kPBytes;  // scratch
+  static constexpr uint32_t kScratch = 5120;
+  static constexpr uint32_t kBytes = kOffS + kScratch + 1024;  // + alignment slack
+  static constexpr uint32_t kTmemCols = NQ == 64 ? 256 : 512;  // S x2 + O x2
+  static_assert(kBytes <= 232448, "shared memory budget");
 };
 
-// Butterfly reduce-scatter of 64 per-thread column values across a warp: step s keeps
-// the half selected by lane bit (4-s), so on return v[0], v[1] hold the warp-wide
-// reduction for columns 2*lane and 2*lane+1.
-template <bool kMax>
-__device__ __forceinline__ void warp_colreduce64(float (&v)[64], int lane) {
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t* r);
+template <>
+__device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+template <>
+__device__ __forceinline__ void tmem_ld<32>(uint32_t taddr, uint32_t* r) {
+  tmem_ld32(taddr, r);
+}
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t* r);
+template <>
+__device__ __forceinline__ void tmem_st<16>(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_st<32>(uint32_t taddr, const uint32_t* r) {
+  tmem_st32(taddr, r);
+}
+
+// Butterfly reduce-scatter of N per-thread column values across a warp (N in {16, 32}).
+// Step s keeps the half selected by lane bit (4-s); with N=16 a final xor-1 combine
+// merges lane pairs.  On return v[0] is the warp-wide reduction of column
+// (N == 32 ? lane : lane >> 1).
+template <int N, bool kMax>
+__device__ __forceinline__ void warp_colreduce(float (&v)[N], int lane) {
+  constexpr int kSteps = N == 32 ? 5 : 4;
 #pragma unroll
-  for (int step = 0; step < 5; ++step) {
-    const int half = 32 >> step;  // live values before this step: 2*half
+  for (int step = 0; step < kSteps; ++step) {
+    const int half = (N / 2) >> step;
     const int off = 16 >> step;
     const bool upper = (lane & off) != 0;
 #pragma unroll
@@ -90,366 +137,458 @@ __device__ __forceinline__ void warp_colreduce64(float (&v)[64], int lane) {
       v[i] = kMax ? fmaxf(keep, recv) : keep + recv;
     }
   }
+  if (N == 16) {
+    const float recv = __shfl_xor_sync(0xffffffffu, v[0], 1);
+    v[0] = kMax ? fmaxf(v[0], recv) : v[0] + recv;
+  }
 }
-__device__ __forceinline__ int colreduce_col(int lane, int i) { return (lane << 1) | i; }
 
-template <int D>
-__global__ void __launch_bounds__(192, 1) sparse_attn_kernel(DevGeom g, DevMask m, AttnParams p) {
-  using Cfg = AttnCfg<D>;
+// Per-tile key geometry, packed: bits 0-1 key frames in the block (1|2), 2-7 first k-frame
+// index, 8-19 key tile row origin kh0, 20-31 key tile col origin kw0.
+__device__ __forceinline__ uint32_t tile_info(const DevGeom& g, int kb) {
+  const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+  const int th = ktile / g.tiles_w, tw = ktile - th * g.tiles_w;
+  return (uint32_t)g.k_tr_count[ktr] | ((uint32_t)g.k_tr_first[ktr] << 2) | ((uint32_t)(8 * th) << 8) |
+         ((uint32_t)(8 * tw) << 20);
+}
+
+template <int D, int NQ>
+__global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, DevMask m, AttnParams p) {
+  using Cfg = AttnCfg<D, NQ>;
+  constexpr int kNK = Cfg::kNK, kNV = Cfg::kNV, kNP = Cfg::kNP, CPT = Cfg::kCPT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + Cfg::kOffQ;
   uint8_t* sK = smem + Cfg::kOffK;
   uint8_t* sV = smem + Cfg::kOffV;
   uint8_t* sP = smem + Cfg::kOffP;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kOffBar);
+  uint8_t* scratch = smem + Cfg::kOffS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(scratch);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;
   uint64_t* k_empty = k_full + kNK;
   uint64_t* v_full = k_empty + kNK;
   uint64_t* v_empty = v_full + kNV;
   uint64_t* s_full = v_empty + kNV;
-  uint64_t* s_empty = s_full + kNP;
-  uint64_t* p_full = s_empty + kNP;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* p_full = s_empty + 2;
   uint64_t* p_empty = p_full + kNP;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + kNP);
-  float* c_ref = reinterpret_cast<float*>(smem + Cfg::kOffBar + 256);  // [64]
-  float* alpha = c_ref + 64;                                           // [64]
-  float* red = alpha + 64;                                             // [4][64]
-  int* flags = reinterpret_cast<int*>(red + 256);                      // [2][4]
-  int* win = flags + 8;                                                // [4][8] hlo,hhi,wlo,whi
+  uint64_t* o_full = p_empty + kNP;
+  uint64_t* o_empty = o_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  float* c_s = reinterpret_cast<float*>(scratch + 256);  // [NQ] column references
+  float* alpha_s = c_s + 128;                            // [NQ] rescale factors / denominators
+  float* red = alpha_s + 128;                            // [4 cg][4 quarter][CPT]
+  int* flags = reinterpret_cast<int*>(red + 512);        // [2][4 cg][4 quarter]
+  int* win = flags + 32;                                 // [4][8]: hlo, hhi, wlo, whi per q row/col
+  uint32_t* info = reinterpret_cast<uint32_t*>(win + 32);// [kInfoCap]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long n_units = p.unit_end - p.unit_begin;
+  const int units_per_head = p.n_trows * g.n_tiles;
 
-  // ---- unit decode --------------------------------------------------------------------
-  const long long unit = p.unit_begin + blockIdx.x;
-  const int tiles_per_head = g.nqf * g.n_tiles;
-  const int head = (int)(unit / tiles_per_head);
-  const int rem = (int)(unit % tiles_per_head);
-  const int qf = rem / g.n_tiles, qtile = rem % g.n_tiles;
-  const int qtr = g.q_frame_tr[qf];
-  const int qb = qtr * g.n_tiles + qtile;
-  const int n = min(max(p.sel_count[(long long)head * g.bnq + qb], 0), p.cap);
-  const int* sel = p.sel + ((long long)head * g.bnq + qb) * p.cap;
-  // Selection ids come from the caller; every role reads them through this clamp so the
-  // barrier protocol stays consistent, and the producer latches InvariantError.
-  auto sel_at = [&](int t) {
+  // unit -> (head, q t_row, tile, selection)
+  auto decode = [&](long long u, int& head, int& qtr, int& qtile, int& n, const int*& sel) {
+    const long long ug = p.unit_begin + u;
+    head = (int)(ug / units_per_head);
+    const int rem = (int)(ug - (long long)head * units_per_head);
+    qtr = p.trow_list[rem / g.n_tiles];
+    qtile = rem % g.n_tiles;
+    const long long qb = (long long)head * g.bnq + qtr * g.n_tiles + qtile;
+    n = min(max(p.sel_count[qb], 0), p.cap);
+    sel = p.sel + qb * p.cap;
+  };
+  auto sel_at = [&](const int* sel, int t) {
     const int kb = sel[t];
     return kb < 0 ? 0 : (kb >= g.bnk ? g.bnk - 1 : kb);
   };
-  const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
 
   // ---- setup ----------------------------------------------------------------------------
-  if (warp == 5) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, Cfg::kTmemCols);
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < kNK; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
     for (int i = 0; i < kNV; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
-    for (int i = 0; i < kNP; ++i) {
-      mbar_init(s_full + i, 1); mbar_init(s_empty + i, 4);
-      mbar_init(p_full + i, 4); mbar_init(p_empty + i, 1);
+    for (int i = 0; i < kNP; ++i) { mbar_init(p_full + i, kSoftWarps); mbar_init(p_empty + i, 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(s_empty + i, kSoftWarps);
+      mbar_init(o_full + i, 1);
+      mbar_init(o_empty + i, kSoftWarps);
     }
     fence_barrier_init();
-  }
-  if (threadIdx.x < 64) c_ref[threadIdx.x] = -INFINITY;
-  if (threadIdx.x < 8) {
-    int lo, hi;
-    locality_range(m.mode, qh0 + threadIdx.x, m.extent_h, g.rows, lo, hi);
-    win[threadIdx.x] = lo; win[8 + threadIdx.x] = hi;
-    locality_range(m.mode, qw0 + threadIdx.x, m.extent_w, g.cols, lo, hi);
-    win[16 + threadIdx.x] = lo; win[24 + threadIdx.x] = hi;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem + 0u, tmem + 64u};
-  const uint32_t tO = tmem + 128u;
+  const uint32_t tS0 = tmem, tO0 = tmem + 2 * NQ;  // S buffers at [0, 2NQ), O buffers at [2NQ, 4NQ)
 
-  if (warp == 4) {
+  if (warp == kProducerWarp) {
     // ===================================== producer =====================================
-    if (lane == 0 && n > 0) {
-      mbar_arrive_expect_tx(q_full, Cfg::kQBytes);
-      bulk_g2s(sQ, p.q + head * p.q_head_stride + ((long long)qf * g.n_tiles + qtile) * Cfg::kTileBytes,
-               Cfg::kQBytes, q_full);
-      for (int t = 0; t < n; ++t) {
-        if (sel[t] < 0 || sel[t] >= g.bnk) atomicOr(p.err, kErrInvariant);
-        const int kb = sel_at(t);
-        const int ktr = kb / g.n_tiles, ktile = kb % g.n_tiles;
-        const int kcnt = g.k_tr_count[ktr], f0 = g.k_tr_first[ktr];
-        const uint8_t* srcA_k = p.k + head * p.kv_head_stride + ((long long)g.k_slot[f0] * g.n_tiles + ktile) * Cfg::kTileBytes;
-        const uint8_t* srcA_v = p.v + head * p.kv_head_stride + ((long long)g.k_slot[f0] * g.n_tiles + ktile) * Cfg::kTileBytes;
-        const uint8_t* srcB_k = nullptr;
-        const uint8_t* srcB_v = nullptr;
-        if (kcnt == 2) {
-          srcB_k = p.k + head * p.kv_head_stride + ((long long)g.k_slot[f0 + 1] * g.n_tiles + ktile) * Cfg::kTileBytes;
-          srcB_v = p.v + head * p.kv_head_stride + ((long long)g.k_slot[f0 + 1] * g.n_tiles + ktile) * Cfg::kTileBytes;
-        }
-        const int ks = t % kNK;
-        if (t >= kNK) mbar_wait(k_empty + ks, ((t / kNK) - 1) & 1);
-        mbar_arrive_expect_tx(k_full + ks, kcnt * Cfg::kTileBytes);
-        uint8_t* dk = sK + ks * Cfg::kKVBytes;
+    if (lane == 0) {
+      long long T = 0;  // global tile counter
+      int U = 0;        // units with work
+      for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int head, qtr, qtile, n;
+        const int* sel;
+        decode(u, head, qtr, qtile, n, sel);
+        if (n == 0) continue;
+        if (U >= 1) mbar_wait(q_empty, (U - 1) & 1);
+        mbar_arrive_expect_tx(q_full, Cfg::kQBytes);
+        {
+          const int f0 = g.q_tr_first[qtr];
+          const uint8_t* qa = p.q + head * p.q_head_stride + ((long long)f0 * g.n_tiles + qtile) * Cfg::kTileBytes;
 #pragma unroll
-        for (int s = 0; s < D / 64; ++s) {
-          bulk_g2s(dk + s * 16384, srcA_k + s * kSubBytes, kSubBytes, k_full + ks);
-          if (kcnt == 2) bulk_g2s(dk + s * 16384 + kSubBytes, srcB_k + s * kSubBytes, kSubBytes, k_full + ks);
+          for (int s = 0; s < D / 64; ++s) {
+            bulk_g2s(sQ + s * Cfg::kQSub, qa + s * kSubBytes, kSubBytes, q_full);
+            if (NQ == 128)
+              bulk_g2s(sQ + s * Cfg::kQSub + kSubBytes, qa + (long long)g.n_tiles * Cfg::kTileBytes + s * kSubBytes,
+                       kSubBytes, q_full);
+          }
         }
-        const int vs = t % kNV;
-        if (t >= kNV) mbar_wait(v_empty + vs, ((t / kNV) - 1) & 1);
-        mbar_arrive_expect_tx(v_full + vs, kcnt * Cfg::kTileBytes);
-        uint8_t* dv = sV + vs * Cfg::kKVBytes;
+        for (int t = 0; t < n; ++t, ++T) {
+          if (sel[t] < 0 || sel[t] >= g.bnk) atomicOr(p.err, kErrInvariant);
+          const int kb = sel_at(sel, t);
+          const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+          const int kcnt = g.k_tr_count[ktr], f0 = g.k_tr_first[ktr];
+          const long long offA =
+              head * p.kv_head_stride + ((long long)g.k_slot[f0] * g.n_tiles + ktile) * Cfg::kTileBytes;
+          const long long offB =
+              kcnt == 2 ? head * p.kv_head_stride + ((long long)g.k_slot[f0 + 1] * g.n_tiles + ktile) * Cfg::kTileBytes
+                        : 0;
+          const int ks = (int)(T % kNK);
+          if (T >= kNK) mbar_wait(k_empty + ks, (uint32_t)((T / kNK) - 1) & 1);
+          mbar_arrive_expect_tx(k_full + ks, kcnt * Cfg::kTileBytes);
+          uint8_t* dk = sK + ks * Cfg::kKVBytes;
 #pragma unroll
-        for (int s = 0; s < D / 64; ++s) {
-          bulk_g2s(dv + s * 16384, srcA_v + s * kSubBytes, kSubBytes, v_full + vs);
-          if (kcnt == 2) bulk_g2s(dv + s * 16384 + kSubBytes, srcB_v + s * kSubBytes, kSubBytes, v_full + vs);
+          for (int s = 0; s < D / 64; ++s) {
+            bulk_g2s(dk + s * 16384, p.k + offA + s * kSubBytes, kSubBytes, k_full + ks);
+            if (kcnt == 2) bulk_g2s(dk + s * 16384 + kSubBytes, p.k + offB + s * kSubBytes, kSubBytes, k_full + ks);
+          }
+          const int vs = (int)(T % kNV);
+          if (T >= kNV) mbar_wait(v_empty + vs, (uint32_t)((T / kNV) - 1) & 1);
+          mbar_arrive_expect_tx(v_full + vs, kcnt * Cfg::kTileBytes);
+          uint8_t* dv = sV + vs * Cfg::kKVBytes;
+#pragma unroll
+          for (int s = 0; s < D / 64; ++s) {
+            bulk_g2s(dv + s * 16384, p.v + offA + s * kSubBytes, kSubBytes, v_full + vs);
+            if (kcnt == 2) bulk_g2s(dv + s * 16384 + kSubBytes, p.v + offB + s * kSubBytes, kSubBytes, v_full + vs);
+          }
         }
+        ++U;
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     // ===================================== MMA issuer ===================================
-    if (lane == 0 && n > 0) {
-      constexpr uint32_t idesc_qk = umma_idesc_bf16(128, 64, 0, 0);
-      constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 64, 1, 1);
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = umma_idesc_bf16(128, NQ, 0, 0);
+      constexpr uint32_t idesc_pv = umma_idesc_bf16(128, NQ, 1, 1);
       const uint32_t aQ = smem_u32(sQ);
-      auto issue_pv = [&](int u) {
-        const int vs = u % kNV, pb = u & 1;
-        mbar_wait(v_full + vs, (u / kNV) & 1);
-        mbar_wait(p_full + pb, (u >> 1) & 1);
+      long long T = 0;
+      int U = 0;
+      auto issue_pv = [&](long long G, const int* sel, int t, uint32_t tO, bool first) {
+        const int vs = (int)(G % kNV), pb = (int)(G % kNP);
+        mbar_wait(v_full + vs, (uint32_t)(G / kNV) & 1);
+        mbar_wait(p_full + pb, (uint32_t)(G / kNP) & 1);
         tc_fence_after();
-        const int kb = sel_at(u);
+        const int kb = sel_at(sel, t);
         const int steps = g.k_tr_count[kb / g.n_tiles] == 2 ? 8 : 4;
         const uint32_t aV = smem_u32(sV + vs * Cfg::kKVBytes);
         const uint32_t aP = smem_u32(sP + pb * Cfg::kPBytes);
         for (int kk = 0; kk < steps; ++kk) {
           const uint64_t da = umma_desc_sw128(aV + kk * 2048, D == 128 ? 16384u : 0u, 1024u);
-          const uint64_t db = umma_desc_sw128(aP + kk * 2048, 0u, 1024u);
-          tc_mma_f16(tO, da, db, idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
+          const uint64_t db = umma_desc_sw128(aP + kk * 2048, 16384u, 1024u);
+          tc_mma_f16(tO, da, db, idesc_pv, (!first || kk > 0) ? 1u : 0u);
         }
         tc_commit(v_empty + vs);
         tc_commit(p_empty + pb);
       };
-      mbar_wait(q_full, 0);
-      for (int t = 0; t < n; ++t) {
-        const int ks = t % kNK, sb = t & 1;
-        mbar_wait(k_full + ks, (t / kNK) & 1);
-        if (t >= 2) mbar_wait(s_empty + sb, ((t >> 1) - 1) & 1);
-        tc_fence_after();
-        const uint32_t aK = smem_u32(sK + ks * Cfg::kKVBytes);
+      for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int head, qtr, qtile, n;
+        const int* sel;
+        decode(u, head, qtr, qtile, n, sel);
+        if (n == 0) continue;
+        const int ob = U & 1;
+        const uint32_t tO = tO0 + ob * NQ;
+        mbar_wait(q_full, U & 1);
+        if (U >= 2) mbar_wait(o_empty + ob, ((U >> 1) - 1) & 1);
+        for (int t = 0; t < n; ++t) {
+          const long long G = T + t;
+          const int ks = (int)(G % kNK), sb = (int)(G & 1);
+          mbar_wait(k_full + ks, (uint32_t)(G / kNK) & 1);
+          if (G >= 2) mbar_wait(s_empty + sb, (uint32_t)((G >> 1) - 1) & 1);
+          tc_fence_after();
+          const uint32_t aK = smem_u32(sK + ks * Cfg::kKVBytes);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t da = umma_desc_sw128(aK + (kk >> 2) * 16384 + (kk & 3) * 32, 16u, 1024u);
-          const uint64_t db = umma_desc_sw128(aQ + (kk >> 2) * kSubBytes + (kk & 3) * 32, 16u, 1024u);
-          tc_mma_f16(tS[sb], da, db, idesc_qk, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t da = umma_desc_sw128(aK + (kk >> 2) * 16384 + (kk & 3) * 32, 16u, 1024u);
+            const uint64_t db = umma_desc_sw128(aQ + (kk >> 2) * Cfg::kQSub + (kk & 3) * 32, 16u, 1024u);
+            tc_mma_f16(tS0 + sb * NQ, da, db, idesc_qk, kk > 0 ? 1u : 0u);
+          }
+          tc_commit(k_empty + ks);
+          tc_commit(s_full + sb);
+          if (t == n - 1) tc_commit(q_empty);
+          if (t >= 1) issue_pv(G - 1, sel, t - 1, tO, t == 1);
         }
-        tc_commit(k_empty + ks);
-        tc_commit(s_full + sb);
-        if (t >= 1) issue_pv(t - 1);
+        issue_pv(T + n - 1, sel, n - 1, tO, n == 1);
+        tc_commit(o_full + ob);
+        T += n;
+        ++U;
       }
-      issue_pv(n - 1);
     }
   } else {
-    // ===================================== softmax (warps 0-3) ==========================
-    const int j = threadIdx.x;  // key row == TMEM lane
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    float lpart[64];
+    // ===================================== softmax (warps 0-15) =========================
+    const int quarter = warp & 3, cg = warp >> 2;
+    const int j = quarter * 32 + lane;  // key row == TMEM lane
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const int col0 = cg * CPT;          // first query column of this thread
+    const int bar_id = 1 + cg;          // named barrier of the column group (128 threads)
+    long long T = 0;
+    int U = 0;
+    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int head, qtr, qtile, n;
+      const int* sel;
+      decode(u, head, qtr, qtile, n, sel);
+      const int qf0 = g.q_tr_first[qtr];
+      const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
+      // per-unit tables: tile infos, locality windows of the 8 query rows / cols
+      for (int i = threadIdx.x; i < min(n, kInfoCap); i += kSoftWarps * 32) info[i] = tile_info(g, sel_at(sel, i));
+      if (threadIdx.x < 8) {
+        int lo, hi;
+        locality_range(m.mode, qh0 + threadIdx.x, m.extent_h, g.rows, lo, hi);
+        win[threadIdx.x] = lo;
+        win[8 + threadIdx.x] = hi;
+        locality_range(m.mode, qw0 + threadIdx.x, m.extent_w, g.cols, lo, hi);
+        win[16 + threadIdx.x] = lo;
+        win[24 + threadIdx.x] = hi;
+      }
+      if (quarter == 0 && lane < CPT) c_s[col0 + lane] = -INFINITY;
+      named_bar_sync(5, kSoftWarps * 32);
+      // query columns of this thread that are real tokens
+      uint32_t qvalid = 0;
 #pragma unroll
-    for (int q = 0; q < 64; ++q) lpart[q] = 0.0f;
-    const int r_in_tile = j & 63;
-    // query columns that are real tokens (ragged tiles have padding rows)
-    uint32_t qv_lo = 0, qv_hi = 0;
+      for (int i = 0; i < CPT; ++i) {
+        const int qc = (col0 + i) & 63;
+        if (qh0 + (qc >> 3) < g.rows && qw0 + (qc & 7) < g.cols) qvalid |= 1u << i;
+      }
+      const uint32_t qfull = CPT == 32 ? 0xffffffffu : ((1u << CPT) - 1u);
+      unsigned long long my_pairs = 0;
+      float c[CPT], lp[CPT];
 #pragma unroll
-    for (int q = 0; q < 64; ++q) {
-      const bool ok = (qh0 + (q >> 3)) < g.rows && (qw0 + (q & 7)) < g.cols;
-      if (ok) { if (q < 32) qv_lo |= 1u << q; else qv_hi |= 1u << (q - 32); }
-    }
-    unsigned long long my_pairs = 0;
+      for (int i = 0; i < CPT; ++i) { c[i] = -INFINITY; lp[i] = 0.0f; }
+      const int ob = U & 1;
+      const uint32_t tO = tO0 + ob * NQ;
 
-    for (int t = 0; t < n; ++t) {
-      const int sb = t & 1;
-      // ---- key row j of this block: validity and allowed-query mask --------------------
-      const int kb = sel_at(t);
-      const int ktr = kb / g.n_tiles, ktile = kb % g.n_tiles;
-      const int kcnt = g.k_tr_count[ktr];
-      const int kframe = g.k_tr_first[ktr] + (j >> 6);
-      const int kh = 8 * (ktile / g.tiles_w) + (r_in_tile >> 3);
-      const int kw = 8 * (ktile % g.tiles_w) + (r_in_tile & 7);
-      const bool kvalid = (j < 64 || kcnt == 2) && kh < g.rows && kw < g.cols;
-      uint32_t mlo = 0, mhi = 0;  // bit q: query column q may attend key j
-      if (kvalid) {
-        if (m.kind == 0) {
-          mlo = mhi = 0xffffffffu;
-        } else if (m.kind == 1) {
-          uint32_t wb = 0;
+      for (int t = 0; t < n; ++t) {
+        const long long G = T + t;
+        const int sb = (int)(G & 1), pb = (int)(G % kNP);
+        // ---- key row j: validity and allowed-query mask over this thread's columns ----
+        const uint32_t inf = t < kInfoCap ? info[t] : tile_info(g, sel_at(sel, t));
+        const int kcnt = inf & 3, kf0 = (inf >> 2) & 63;
+        const int kh = (int)((inf >> 8) & 0xfff) + ((j & 63) >> 3);
+        const int kw = (int)(inf >> 20) + (j & 7);
+        const bool kvalid = (j < 64 || kcnt == 2) && kh < g.rows && kw < g.cols;
+        uint32_t mk = 0;
+        if (kvalid) {
+          if (m.kind == 0) {
+            mk = qvalid;
+          } else if (m.kind == 1) {
+            uint32_t wb = 0, hb = 0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) wb |= (kw >= win[16 + i] && kw < win[24 + i]) ? (1u << i) : 0u;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const bool hb = kh >= win[i] && kh < win[8 + i];
-            if (hb) {
-              if (i < 4) mlo |= wb << (8 * i);
-              else mhi |= wb << (8 * (i - 4));
+            for (int i = 0; i < 8; ++i) {
+              wb |= (kw >= win[16 + i] && kw < win[24 + i]) ? (1u << i) : 0u;
+              hb |= (kh >= win[i] && kh < win[8 + i]) ? (1u << i) : 0u;
             }
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) {
+              const int qc = (col0 + i) & 63;
+              if (((hb >> (qc >> 3)) & (wb >> (qc & 7)) & 1u) != 0u) mk |= 1u << i;
+            }
+            mk &= qvalid;
+          } else {
+            const long long tk = g.k_frame_tok0[kf0 + (j >> 6)] + (long long)kh * g.cols + kw;
+#pragma unroll 4
+            for (int i = 0; i < CPT; ++i) {
+              if (!((qvalid >> i) & 1u)) continue;
+              const int col = col0 + i, qc = col & 63;
+              const long long tq =
+                  g.q_frame_tok0[qf0 + (col >> 6)] + (long long)(qh0 + (qc >> 3)) * g.cols + qw0 + (qc & 7);
+              if ((m.bits[tq * m.words_per_row + (tk >> 6)] >> (tk & 63)) & 1ull) mk |= 1u << i;
+            }
+          }
+        }
+        my_pairs += __popc(mk);
+        const bool dense = mk == qfull;  // every (query, key j) pair of this thread allowed
+
+        // ---- S^T row j, this thread's columns -> registers ------------------------------
+        mbar_wait(s_full + sb, (uint32_t)(G >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[CPT];
+        tmem_ld<CPT>(tS0 + sb * NQ + col0 + lane_off, sr);
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty + sb);
+
+        float x[CPT], dmax = -INFINITY;
+        if (dense) {
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            x[i] = __uint_as_float(sr[i]) * p.scale_log2;
+            dmax = fmaxf(dmax, x[i] - c[i]);
           }
         } else {
-          const long long tk = g.k_frame_tok0[kframe] + (long long)kh * g.cols + kw;
-#pragma unroll 4
-          for (int q = 0; q < 64; ++q) {
-            const int qh = qh0 + (q >> 3), qw = qw0 + (q & 7);
-            if (qh < g.rows && qw < g.cols) {
-              const long long tq = g.q_frame_tok0[qf] + (long long)qh * g.cols + qw;
-              if ((m.bits[tq * m.words_per_row + (tk >> 6)] >> (tk & 63)) & 1ull) {
-                if (q < 32) mlo |= 1u << q; else mhi |= 1u << (q - 32);
-              }
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            const bool ok = ((mk >> i) & 1u) != 0u;
+            x[i] = ok ? __uint_as_float(sr[i]) * p.scale_log2 : -INFINITY;
+            if (ok) dmax = fmaxf(dmax, x[i] - c[i]);
+          }
+        }
+        const bool wneed = __any_sync(0xffffffffu, dmax > kRescaleThreshold);
+        if (lane == 0) flags[sb * 16 + cg * 4 + quarter] = wneed ? 1 : 0;
+        named_bar_sync(bar_id, 128);
+        const int* fl = flags + sb * 16 + cg * 4;
+        if ((fl[0] | fl[1] | fl[2] | fl[3]) != 0) {
+          // exact column max of this tile over the group's 128 key rows
+          float v[CPT];
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) v[i] = x[i];
+          warp_colreduce<CPT, true>(v, lane);
+          const int rc = CPT == 32 ? lane : (lane >> 1);
+          if (CPT == 32 || (lane & 1) == 0) red[(cg * 4 + quarter) * CPT + rc] = v[0];
+          named_bar_sync(bar_id, 128);
+          if (quarter == 0 && lane < CPT) {
+            const float* r = red + cg * 4 * CPT + lane;
+            const float mx = fmaxf(fmaxf(r[0], r[CPT]), fmaxf(r[2 * CPT], r[3 * CPT]));
+            const float cold = c_s[col0 + lane];
+            const float nw = fmaxf(cold, mx);
+            c_s[col0 + lane] = nw;
+            alpha_s[col0 + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
+          }
+          named_bar_sync(bar_id, 128);
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            c[i] = c_s[col0 + i];
+            lp[i] *= alpha_s[col0 + i];
+          }
+          if (t > 0) {
+            // O^T holds PV of this unit's tiles 0..t-1: wait for PV(G-1), rescale columns
+            mbar_wait(p_empty + ((G - 1) % kNP), (uint32_t)((G - 1) / kNP) & 1);
+            tc_fence_after();
+            if (j < D) {
+              uint32_t o[CPT];
+              tmem_ld<CPT>(tO + col0 + lane_off, o);
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < CPT; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha_s[col0 + i]);
+              tmem_st<CPT>(tO + col0 + lane_off, o);
+              tc_wait_st();
             }
           }
         }
-      }
 
-      my_pairs += __popc(mlo & qv_lo) + __popc(mhi & qv_hi);
-
-      // ---- S^T row j -> registers ----------------------------------------------------
-      mbar_wait(s_full + sb, (t >> 1) & 1);
-      tc_fence_after();
-      uint32_t sr[64];
-      tmem_ld32(tS[sb] + lane_off, sr);
-      tmem_ld32(tS[sb] + lane_off + 32u, sr + 32);
-      tc_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_empty + sb);
-
-      float x[64];
-      bool exceed = false;
+        // ---- P^T row j (bf16) and partial denominators --------------------------------
+        uint32_t pk[CPT / 2];
 #pragma unroll
-      for (int q = 0; q < 64; ++q) {
-        const bool ok = ((q < 32 ? mlo >> q : mhi >> (q - 32)) & 1u) != 0u;
-        x[q] = ok ? __uint_as_float(sr[q]) * p.scale_log2 : -INFINITY;
-        exceed |= x[q] > c_ref[q] + kRescaleThreshold;
-      }
-      const bool wneed = __any_sync(0xffffffffu, exceed);
-      if (lane == 0) flags[sb * 4 + warp] = wneed ? 1 : 0;
-      named_bar_sync(1, 128);
-      const bool need = (flags[sb * 4 + 0] | flags[sb * 4 + 1] | flags[sb * 4 + 2] | flags[sb * 4 + 3]) != 0;
-
-      if (need) {
-        float v[64];
-#pragma unroll
-        for (int q = 0; q < 64; ++q) v[q] = x[q];
-        warp_colreduce64<true>(v, lane);
-        red[warp * 64 + colreduce_col(lane, 0)] = v[0];
-        red[warp * 64 + colreduce_col(lane, 1)] = v[1];
-        named_bar_sync(1, 128);
-        if (j < 64) {
-          const float old = c_ref[j];
-          const float mx = fmaxf(fmaxf(red[j], red[64 + j]), fmaxf(red[128 + j], red[192 + j]));
-          const float nw = fmaxf(old, mx);
-          c_ref[j] = nw;
-          alpha[j] = (nw == -INFINITY) ? 1.0f : exp2f(old - nw);
+        for (int i = 0; i < CPT / 2; ++i) {
+          const float p0 = x[2 * i] == -INFINITY ? 0.0f : ex2(x[2 * i] - c[2 * i]);
+          const float p1 = x[2 * i + 1] == -INFINITY ? 0.0f : ex2(x[2 * i + 1] - c[2 * i + 1]);
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+          lp[2 * i] += __low2float(h2);
+          lp[2 * i + 1] += __high2float(h2);
+          pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
         }
-        named_bar_sync(1, 128);
+        if (G >= kNP) mbar_wait(p_empty + pb, (uint32_t)((G / kNP) - 1) & 1);
+        // MN-major B operand: [NQ/64 groups][128 key rows][128 B], 16-B chunks swizzled by row
+        uint8_t* prow = sP + pb * Cfg::kPBytes + (col0 >> 6) * 16384 + j * 128;
+        const int ch0 = (col0 & 63) >> 3;
 #pragma unroll
-        for (int q = 0; q < 64; ++q) lpart[q] *= alpha[q];
-        if (t > 0) {
-          // O^T holds PV(0..t-1): wait for PV(t-1), rescale column q by alpha[q].
-          mbar_wait(p_empty + ((t - 1) & 1), ((t - 1) >> 1) & 1);
-          tc_fence_after();
-          if (j < D) {
-            uint32_t o[64];
-            tmem_ld32(tO + lane_off, o);
-            tmem_ld32(tO + lane_off + 32u, o + 32);
-            tc_wait_ld();
+        for (int c8 = 0; c8 < CPT / 8; ++c8)
+          *reinterpret_cast<uint4*>(prow + (((ch0 + c8) ^ (j & 7)) << 4)) =
+              make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full + pb);
+      }
+
+      // ---- epilogue: denominators, normalise, store ------------------------------------
+      if (p.pairs) {
 #pragma unroll
-            for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha[q]);
-            tmem_st32(tO + lane_off, o);
-            tmem_st32(tO + lane_off + 32u, o + 32);
-            tc_wait_st();
+        for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
+        if (lane == 0 && my_pairs) atomicAdd(p.pairs, my_pairs);
+      }
+      warp_colreduce<CPT, false>(lp, lane);
+      {
+        const int rc = CPT == 32 ? lane : (lane >> 1);
+        if (CPT == 32 || (lane & 1) == 0) red[(cg * 4 + quarter) * CPT + rc] = lp[0];
+      }
+      named_bar_sync(bar_id, 128);
+      float* lsum = alpha_s;
+      if (quarter == 0 && lane < CPT) {
+        const float* r = red + cg * 4 * CPT + lane;
+        const float l = (r[0] + r[CPT]) + (r[2 * CPT] + r[3 * CPT]);
+        const int col = col0 + lane, qc = col & 63;
+        lsum[col] = l;
+        const int qh = qh0 + (qc >> 3), qw = qw0 + (qc & 7);
+        if (qh < g.rows && qw < g.cols) {
+          const long long tq = g.q_frame_tok0[qf0 + (col >> 6)] + (long long)qh * g.cols + qw;
+          if (tq >= p.row_begin && tq < p.row_end && !(l > 0.0f)) atomicOr(p.err, kErrDegenerate);
+        }
+      }
+      uint16_t* so = reinterpret_cast<uint16_t*>(sP);  // staged O tile [NQ][D] bf16
+      if (n > 0) {
+        // all PVs of this unit complete => every P^T buffer is free for staging
+        mbar_wait(o_full + ob, (uint32_t)(U >> 1) & 1);
+        tc_fence_after();
+      }
+      named_bar_sync(5, kSoftWarps * 32);  // lsum visible, staging buffer free
+      if (n > 0) {
+        if (j < D) {
+          uint32_t o[CPT];
+          tmem_ld<CPT>(tO + col0 + lane_off, o);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            const float l = lsum[col0 + i];
+            const float val = l > 0.0f ? __uint_as_float(o[i]) / l : 0.0f;
+            so[(col0 + i) * D + j] = __bfloat16_as_ushort(__float2bfloat16_rn(val));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_empty + ob);
+      } else if (j < D) {
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) so[(col0 + i) * D + j] = 0;
+      }
+      named_bar_sync(5, kSoftWarps * 32);
+      constexpr int kChunks = D / 8;
+      if (p.out_tile_major) {
+        uint16_t* outu = p.out + u * NQ * D;
+        for (int idx = threadIdx.x; idx < NQ * kChunks; idx += kSoftWarps * 32)
+          *reinterpret_cast<uint4*>(outu + idx * 8) = *reinterpret_cast<const uint4*>(so + idx * 8);
+      } else {
+        uint16_t* outh = p.out + head * p.out_head_stride;
+        for (int idx = threadIdx.x; idx < NQ * kChunks; idx += kSoftWarps * 32) {
+          const int col = idx / kChunks, ch = idx % kChunks, qc = col & 63;
+          const int qh = qh0 + (qc >> 3), qw = qw0 + (qc & 7);
+          if (qh < g.rows && qw < g.cols) {
+            const long long tq = g.q_frame_tok0[qf0 + (col >> 6)] + (long long)qh * g.cols + qw;
+            uint4 val = make_uint4(0, 0, 0, 0);
+            if (tq >= p.row_begin && tq < p.row_end) val = *reinterpret_cast<const uint4*>(so + col * D + ch * 8);
+            *reinterpret_cast<uint4*>(outh + tq * D + ch * 8) = val;
           }
         }
       }
-
-      // ---- P^T row j (bf16), partial denominators -------------------------------------
-      uint32_t pk[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float c0 = c_ref[2 * i], c1 = c_ref[2 * i + 1];
-        const float p0 = x[2 * i] == -INFINITY ? 0.0f : exp2f(x[2 * i] - c0);
-        const float p1 = x[2 * i + 1] == -INFINITY ? 0.0f : exp2f(x[2 * i + 1] - c1);
-        const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-        lpart[2 * i] += __low2float(h2);
-        lpart[2 * i + 1] += __high2float(h2);
-        pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
-      }
-      if (t >= 2) mbar_wait(p_empty + sb, ((t >> 1) - 1) & 1);
-      uint8_t* prow = sP + sb * Cfg::kPBytes + j * 128;
-#pragma unroll
-      for (int ch = 0; ch < 8; ++ch)
-        *reinterpret_cast<uint4*>(prow + ((ch ^ (j & 7)) << 4)) =
-            make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full + sb);
-    }
-
-    // ---- epilogue ------------------------------------------------------------------------
-    if (p.pairs) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
-      if (lane == 0 && my_pairs) atomicAdd(p.pairs, my_pairs);
-    }
-    warp_colreduce64<false>(lpart, lane);
-    red[warp * 64 + colreduce_col(lane, 0)] = lpart[0];
-    red[warp * 64 + colreduce_col(lane, 1)] = lpart[1];
-    named_bar_sync(1, 128);
-    float* lsum = alpha;  // reuse
-    if (j < 64) {
-      const float l = (red[j] + red[64 + j]) + (red[128 + j] + red[192 + j]);
-      lsum[j] = l;
-      const int qh = qh0 + (j >> 3), qw = qw0 + (j & 7);
-      if (qh < g.rows && qw < g.cols) {
-        const long long tq = g.q_frame_tok0[qf] + (long long)qh * g.cols + qw;
-        if (tq >= p.row_begin && tq < p.row_end && !(l > 0.0f)) atomicOr(p.err, kErrDegenerate);
-      }
-    }
-    named_bar_sync(1, 128);
-    // stage O (row-major [64 q][D] bf16) in P buffer 0, then write rows out
-    uint16_t* so = reinterpret_cast<uint16_t*>(sP);
-    if (n > 0) {
-      mbar_wait(p_empty + ((n - 1) & 1), ((n - 1) >> 1) & 1);
-      tc_fence_after();
-      if (j < D) {
-        uint32_t o[64];
-        tmem_ld32(tO + lane_off, o);
-        tmem_ld32(tO + lane_off + 32u, o + 32);
-        tc_wait_ld();
-#pragma unroll
-        for (int q = 0; q < 64; ++q) {
-          const float l = lsum[q];
-          const float val = l > 0.0f ? __uint_as_float(o[q]) / l : 0.0f;
-          so[q * D + j] = __bfloat16_as_ushort(__float2bfloat16_rn(val));
-        }
-      }
-    } else if (j < D) {
-#pragma unroll 8
-      for (int q = 0; q < 64; ++q) so[q * D + j] = 0;
-    }
-    named_bar_sync(1, 128);
-    constexpr int kChunks = D / 8;
-    if (p.out_tile_major) {
-      // unit-contiguous rows (padding rows included) for the head-parallel all-gather
-      uint16_t* outu = p.out + (long long)blockIdx.x * 64 * D;
-      for (int idx = j; idx < 64 * kChunks; idx += 128)
-        *reinterpret_cast<uint4*>(outu + idx * 8) = *reinterpret_cast<const uint4*>(so + idx * 8);
-    }
-    uint16_t* outh = p.out + head * p.out_head_stride;
-    for (int idx = j; idx < 64 * kChunks && !p.out_tile_major; idx += 128) {
-      const int q = idx / kChunks, ch = idx % kChunks;
-      const int qh = qh0 + (q >> 3), qw = qw0 + (q & 7);
-      if (qh < g.rows && qw < g.cols) {
-        const long long tq = g.q_frame_tok0[qf] + (long long)qh * g.cols + qw;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (tq >= p.row_begin && tq < p.row_end) val = *reinterpret_cast<const uint4*>(so + q * D + ch * 8);
-        *reinterpret_cast<uint4*>(outh + tq * D + ch * 8) = val;
+      named_bar_sync(5, kSoftWarps * 32);  // staging buffer and per-unit tables reusable
+      if (n > 0) {
+        T += n;
+        ++U;
       }
     }
   }
@@ -457,10 +596,12 @@ __global__ void __launch_bounds__(192, 1) sparse_attn_kernel(DevGeom g, DevMask 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc(tmem, kTmemCols);
+  if (warp == kMmaWarp) tmem_dealloc(tmem, Cfg::kTmemCols);
 }
 
-template __global__ void sparse_attn_kernel<64>(DevGeom, DevMask, AttnParams);
-template __global__ void sparse_attn_kernel<128>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<64, 64>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<128, 64>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<64, 128>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<128, 128>(DevGeom, DevMask, AttnParams);
 
 }  // namespace fvsr
