@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -332,29 +333,46 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
   p.coarse = coarse;
   p.allowed = allowed;
   p.err = ctx->d_err;
-  const size_t smem = (size_t)p.npow2 * 8 + (size_t)g.d * 4 + 2 * (size_t)g.bnk + 16;
-  if (smem > 48 * 1024) {
-    if (smem > 200 * 1024) return fail(FVSR_E_CONFIG, "too many key blocks (%d) for the selector", g.bnk);
+  // keys[QG][bnk] | pq[QG][d] | pooled-key chunk [kSelChunk][d+1] | flags[QG][bnk]
+  const size_t ld = (size_t)g.d + 1;
+  const size_t smem = (size_t)kSelQG * g.bnk * 8 + (size_t)kSelQG * g.d * 4 + kSelChunk * ld * 4 +
+                      (size_t)kSelQG * g.bnk + 64;
+  if (smem > 220 * 1024) return fail(FVSR_E_CONFIG, "too many key blocks (%d) for the selector", g.bnk);
+  if (g.d % 4 != 0) return fail(FVSR_E_CONFIG, "plan_sparse: head_dim must be a multiple of 4 (got %d)", g.d);
+  if (smem > 48 * 1024)
     FVSR_CUDA(cudaFuncSetAttribute(score_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  }
-  dim3 grid(g.bnq, heads);
-  score_select_kernel<<<grid, 256, smem, s>>>(g, dm, p);
+  dim3 grid((g.bnq + kSelQG - 1) / kSelQG, heads);
+  score_select_kernel<<<grid, kSelThreads, smem, s>>>(g, dm, p);
   return FVSR_OK;
 }
 
-template <int D, int NQ>
-int launch_attn_dq(const DevGeom& g, const DevMask& dm, const AttnParams& p, int sms, cudaStream_t s) {
+template <int D, int NQ, int SW>
+int launch_attn_dqw(const DevGeom& g, const DevMask& dm, const AttnParams& p, int sms, cudaStream_t s) {
+  using Cfg = AttnCfg<D, NQ, SW>;
   static bool configured = false;
   if (!configured) {
-    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)AttnCfg<D, NQ>::kBytes));
+    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D, NQ, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Cfg::kBytes));
     configured = true;
   }
   const long long units = p.unit_end - p.unit_begin;
   if (units <= 0) return FVSR_OK;
   const unsigned grid = (unsigned)std::min<long long>(units, sms);  // persistent CTAs
-  sparse_attn_kernel<D, NQ><<<grid, kThreads, AttnCfg<D, NQ>::kBytes, s>>>(g, dm, p);
+  sparse_attn_kernel<D, NQ, SW><<<grid, Cfg::kThreads, Cfg::kBytes, s>>>(g, dm, p);
   return FVSR_OK;
+}
+
+template <int D, int NQ>
+int launch_attn_dq(const DevGeom& g, const DevMask& dm, const AttnParams& p, int sms, cudaStream_t s) {
+  if (NQ == 64) {
+    static const int sw = [] {
+      const char* e = std::getenv("FVSR_SOFT_WARPS");  // experiments: 8 or 16 softmax warps
+      return e ? std::atoi(e) : 16;
+    }();
+    if (sw == 8) return launch_attn_dqw<D, 64, 8>(g, dm, p, sms, s);
+    return launch_attn_dqw<D, 64, 16>(g, dm, p, sms, s);
+  }
+  return launch_attn_dqw<D, 128, 16>(g, dm, p, sms, s);
 }
 
 bool trows_uniform(const DevGeom& g) {
@@ -371,6 +389,15 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
   if (g.d != 64 && g.d != 128)
     return fail(FVSR_E_CONFIG, "sparse_attention_exec: head_dim %d unsupported (64 or 128)", g.d);
   const bool uniform = trows_uniform(g);
+  if (const char* dbg = std::getenv("FVSR_ATTN_DEBUG")) p.debug = std::atoi(dbg);
+  static long long* trace = nullptr;
+  static int trace_calls = 0;
+  const bool tracing = std::getenv("FVSR_ATTN_TRACE") != nullptr && ++trace_calls == 20;
+  if (tracing) {
+    if (!trace) cudaMalloc(&trace, kTraceEvents * kTraceTiles * sizeof(long long));
+    cudaMemsetAsync(trace, 0, kTraceEvents * kTraceTiles * sizeof(long long), s);
+    p.trace = trace;
+  }
   int sms = 0;
   FVSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
   SpanGuard sg(ctx, s, FVSR_TIME_ATTENTION);
@@ -389,6 +416,22 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
       st = nq == 1 ? launch_attn_dq<64, 64>(g, dm, p, sms, s) : launch_attn_dq<64, 128>(g, dm, p, sms, s);
     FVSR_TRY(st);
     ctx->launches += 1;
+  }
+  if (tracing) {  // experiments only: per-tile pipeline timeline of CTA 0
+    std::vector<long long> h(kTraceEvents * kTraceTiles);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    const char* names[kTraceEvents] = {"K",    "QK",   "S0",  "P0",  "PV",    "V",     "vote",  "rare",
+                                       "exps", "pbuf", "sts", "fence", "QKmma", "QKcmt", "PVmma", "PVcmt"};
+    const long long base = h[0];
+    std::fprintf(stderr, "trace (cycles from first K issue), tiles 0..60\n  G");
+    for (int e = 0; e < kTraceEvents; ++e) std::fprintf(stderr, "%9s", names[e]);
+    std::fprintf(stderr, "\n");
+    for (int G = 0; G < 60; ++G) {
+      std::fprintf(stderr, "%3d", G);
+      for (int e = 0; e < kTraceEvents; ++e) std::fprintf(stderr, "%9lld", h[e * kTraceTiles + G] ? h[e * kTraceTiles + G] - base : -1);
+      std::fprintf(stderr, "\n");
+    }
   }
   return FVSR_OK;
 }
@@ -696,10 +739,24 @@ int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t fra
   g.n_tiles = r->n_tiles;
   g.d = r->d;
   const long long N = (long long)r->rows * r->cols;
-  const int slots1[1] = {slot};
   SpanGuard sg(ctx, s, FVSR_TIME_APPEND);
-  launch_pack(k, N * r->d, r->heads, 1, g, r->k_layer(layer), r->kv_head_stride(), slots1, s);
-  launch_pack(v, N * r->d, r->heads, 1, g, r->v_layer(layer), r->kv_head_stride(), slots1, s);
+  // one pass: K -> swizzled ring slot + pooled partials (S1 continues the even partner), V -> slot
+  PackPoolArgs a{};
+  a.src = k;
+  a.src2 = v;
+  a.src_head_stride = N * r->d;
+  a.dst = r->k_layer(layer);
+  a.dst2 = r->v_layer(layer);
+  a.dst_head_stride = r->kv_head_stride();
+  a.s0 = r->s0_layer(layer);
+  a.s1 = r->s1_layer(layer);
+  a.part_head_stride = r->part_head_stride();
+  a.ext_s0 = r->s0_layer(layer);
+  a.rows = r->rows;
+  a.cols = r->cols;
+  a.tiles_w = r->tiles_w;
+  a.n_tiles = r->n_tiles;
+  a.d = r->d;
   PoolGroups pg{};
   pg.first[0] = 0;
   pg.count[0] = 1;
@@ -707,12 +764,10 @@ int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t fra
   SlotList sl{};
   sl.s[0] = slot;
   dim3 grid(r->n_tiles, 1, r->heads);
-  pool_partials_kernel<<<grid, std::min(256, r->d), 0, s>>>(k, N * r->d, r->rows, r->cols, r->tiles_w, r->n_tiles,
-                                                            r->d, pg, sl, r->s0_layer(layer), r->s1_layer(layer),
-                                                            r->part_head_stride(), r->s0_layer(layer));
+  pack_pool_kernel<<<grid, 64, 0, s>>>(a, pg, sl);
   r->used[layer][slot] = 1;
   c.emplace_back(frame_id, slot);
-  return after_launch(ctx, s, 3);
+  return after_launch(ctx, s, 1);
 }
 
 int32_t fvsr_ring_evict_sliding(fvsr_ring* r, int32_t layer) {
@@ -781,9 +836,29 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
 
   {
     SpanGuard sg(ctx, s, FVSR_TIME_MASK_BUILDER);
-    launch_pack(q, Lq * d, r->heads, g.nqf, g, qp, (long long)g.nqf * g.n_tiles * tb, nullptr, s);
-    launch_pool_trows(q, Lq * d, r->heads, g.q_tr_first, g.q_tr_count, g.nq_trows, g, nullptr, qs0, qs1,
-                      (long long)g.nqf * g.n_tiles * d, s);
+    // one pass over Q: swizzled query tiles for the tensor cores + pooled partials for the plan
+    PackPoolArgs a{};
+    a.src = q;
+    a.src_head_stride = Lq * d;
+    a.dst = qp;
+    a.dst_head_stride = (long long)g.nqf * g.n_tiles * tb;
+    a.s0 = qs0;
+    a.s1 = qs1;
+    a.part_head_stride = (long long)g.nqf * g.n_tiles * d;
+    a.rows = g.rows;
+    a.cols = g.cols;
+    a.tiles_w = g.tiles_w;
+    a.n_tiles = g.n_tiles;
+    a.d = d;
+    PoolGroups pg{};
+    SlotList sl{};
+    for (int t = 0; t < g.nq_trows; ++t) {
+      pg.first[t] = g.q_tr_first[t];
+      pg.count[t] = g.q_tr_count[t];
+      pg.ext_slot[t] = -1;
+    }
+    for (int i = 0; i < g.nqf; ++i) sl.s[i] = i;
+    pack_pool_kernel<<<dim3(g.n_tiles, g.nq_trows, r->heads), 64, 0, s>>>(a, pg, sl);
     const float cscale = 1.0f / std::sqrt(static_cast<float>(d));
     FVSR_TRY(launch_select(ctx, g, dm, r->heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, r->s0_layer(layer),
                            r->s1_layer(layer), r->part_head_stride(), cscale, topk, cap, use_sel, use_cnt, nullptr,

@@ -113,23 +113,23 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
-// Wait for the phase with the given parity to complete.  A watchdog turns a protocol
-// deadlock into a trap (~10 s) instead of a hung device.
+// Wait for the phase with the given parity to complete.  The suspend-time hint lets the
+// hardware park the waiting thread until the phase flips instead of spinning (a spinning
+// waiter steals issue slots from the warps doing the work).  A watchdog turns a protocol
+// deadlock into a trap instead of a hung device.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
-  long long t0 = 0;
   for (int it = 0;; ++it) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.b32 %0, 1, 0, P1;\n\t}"
         : "=r"(done)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(0x989680u)
         : "memory");
     if (done) return;
-    if (it == 0) t0 = clock64();
-    else if ((it & 1023) == 0 && clock64() - t0 > 20000000000ll) __trap();
+    if (it > (1 << 22)) __trap();
   }
 }
 // 1D bulk copy global -> shared, completion counted on `bar` in bytes.
@@ -138,6 +138,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// One lane of the (fully active) warp returns true.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");

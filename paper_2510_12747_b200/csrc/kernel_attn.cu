@@ -16,25 +16,22 @@
 // block (one frame of the pair in context) issues only its 4 valid PV K-steps.
 //
 // Softmax in the transposed layout: TMEM lane j holds key j's scores for all queries.
-// 16 softmax warps = 4 lane quarters x 4 column groups; a column group (4 warps, 128
-// lanes) owns NQ/4 query columns and keeps, per column, a running reference c (log2
-// units) and per-thread partial denominators.  The reference only moves when a score
-// exceeds it by > 8 (FA4-style lazy rescale): one OR across the group's 4 warps per tile;
+// Softmax warps = 4 lane quarters x NQ/32 column groups; a column group (4 warps, 128
+// lanes) owns 32 query columns and keeps, per column, a running reference c (log2 units)
+// and per-thread partial denominators.  The reference only moves when a score exceeds it
+// by > 8 (FA4-style lazy rescale), decided by one bar.red.or across the group per tile;
 // on the rare exceed path (always on a column's first real tile) the exact column max is
 // a warp butterfly + smem, then O^T columns in TMEM and the partial sums are rescaled.
 // Denominators are reduced across lanes once per unit.
 //
-// Persistent CTAs (round-robin over units).  Roles, 576 threads: warps 0-15 softmax +
-// epilogue, warp 16 producer (cp.async.bulk of pre-swizzled frame-tiles), warp 17 TMEM
-// allocator + MMA issuer.  S^T and O^T are double-buffered in TMEM.
+// Persistent CTAs (round-robin over units).  Roles: softmax warps [0, SW), warp SW
+// Q/K producer, SW+1 MMA issuer (+ TMEM allocator), SW+2 V producer; producers and the
+// MMA issuer run warp-wide (uniform registers) and elect one lane to issue.  S^T has NS
+// TMEM buffers so QK runs NS-1 tiles ahead of PV; O^T is double-buffered across units.
 #include "fvsr_common.cuh"
 
 namespace fvsr {
 
-constexpr int kSoftWarps = 16;
-constexpr int kThreads = kSoftWarps * 32 + 64;
-constexpr int kProducerWarp = kSoftWarps;
-constexpr int kMmaWarp = kSoftWarps + 1;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kInfoCap = 256;              // per-unit tile-info table entries
 
@@ -57,14 +54,34 @@ struct AttnParams {
   int out_tile_major;        // 1: out is [unit - unit_begin][NQ][d]
   unsigned* err;
   unsigned long long* pairs; // += executed (mask-allowed, selected-block) token pairs
+  int debug;                 // experiments only (FVSR_ATTN_DEBUG): 1 skip softmax math, 2 skip K/V loads
+  long long* trace;          // experiments only (FVSR_ATTN_TRACE): per-tile clock64 stamps of CTA 0
 };
 
-template <int D, int NQ>
+// trace slots [event][tile]: 0 K issued, 1 QK issued, 2 S ready (softmax warp 0), 3 P done
+// (warp 0), 4 PV issued, 5 V issued, 6-11 S ready / P done of softmax warps 3/4/7, 12/13 QK
+// MMAs / commits issued, 14/15 PV MMAs / commits issued.
+constexpr int kTraceTiles = 512;
+constexpr int kTraceEvents = 16;
+__device__ __forceinline__ void trace_at(const AttnParams& p, int ev, long long G) {
+  if (p.trace && blockIdx.x == 0 && G < kTraceTiles) p.trace[ev * kTraceTiles + G] = clock64();
+}
+
+template <int D, int NQ, int SWARPS>
 struct AttnCfg {
+  static constexpr int kSW = SWARPS;                 // softmax warps: 4 lane quarters x column groups
+  static constexpr int kCG = SWARPS / 4;             // column groups
+  static constexpr int kCPT = NQ / kCG;              // query columns per softmax thread (16 or 32)
+  static_assert(kCPT == 16 || kCPT == 32, "columns per thread");
+  static constexpr int kProducerWarp = kSW;          // Q and K tiles
+  static constexpr int kMmaWarp = kSW + 1;
+  static constexpr int kVProducerWarp = kSW + 2;     // V tiles (decoupled so K runs ahead)
+  static constexpr int kThreads = kSW * 32 + 96;
+  static constexpr int kNS = NQ == 64 ? 4 : 2;       // S^T buffers in TMEM
+  static constexpr int kLA = kNS - 1;                // QK look-ahead over PV
   static constexpr int kNK = NQ == 64 ? 3 : 2;       // K stages
   static constexpr int kNV = 2;                      // V stages
   static constexpr int kNP = NQ == 64 ? 2 : 1;       // P^T buffers
-  static constexpr int kCPT = NQ / 4;                // query columns per softmax thread
   static constexpr uint32_t kTileBytes = D * 128;    // one packed 64-row frame-tile
   static constexpr uint32_t kQSub = NQ * 128;        // Q sub-tile stride (NQ rows x 128 B)
   static constexpr uint32_t kQBytes = (D / 64) * kQSub;
@@ -77,7 +94,8 @@ struct AttnCfg {
   static constexpr uint32_t kOffS = kOffP + kNP * kPBytes;  // scratch
   static constexpr uint32_t kScratch = 5120;
   static constexpr uint32_t kBytes = kOffS + kScratch + 1024;  // + alignment slack
-  static constexpr uint32_t kTmemCols = NQ == 64 ? 256 : 512;  // S x2 + O x2
+  static constexpr uint32_t kTmemCols = 512;         // S x NS + O x 2
+  static_assert(kNS * NQ + 2 * NQ <= 512, "TMEM budget");
   static_assert(kBytes <= 232448, "shared memory budget");
 };
 
@@ -85,6 +103,43 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// Barrier over `n` threads that also ORs a predicate across them.
+__device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t n, bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred pi, po;\n\tsetp.ne.u32 pi, %1, 0;\n\t"
+      "bar.red.or.pred po, %2, %3, pi;\n\tselp.u32 %0, 1, 0, po;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)v), "r"(id), "r"(n)
+      : "memory");
+  return r != 0;
+}
+
+// Butterfly reduce-scatter of N (16 or 32) per-thread column values across a warp: step s
+// keeps the half selected by lane bit (4-s); with N=16 a final xor-1 combine merges lane
+// pairs.  On return v[0] is the warp-wide reduction of column (N == 32 ? lane : lane >> 1).
+template <int N, bool kMax>
+__device__ __forceinline__ void warp_colreduce(float (&v)[N], int lane) {
+  constexpr int kSteps = N == 32 ? 5 : 4;
+#pragma unroll
+  for (int step = 0; step < kSteps; ++step) {
+    const int half = (N / 2) >> step;
+    const int off = 16 >> step;
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float keep = upper ? v[half + i] : v[i];
+      const float send = upper ? v[i] : v[half + i];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, off);
+      v[i] = kMax ? fmaxf(keep, recv) : keep + recv;
+    }
+  }
+  if (N == 16) {
+    const float recv = __shfl_xor_sync(0xffffffffu, v[0], 1);
+    v[0] = kMax ? fmaxf(v[0], recv) : v[0] + recv;
+  }
 }
 
 template <int N>
@@ -117,30 +172,17 @@ __device__ __forceinline__ void tmem_st<32>(uint32_t taddr, const uint32_t* r) {
   tmem_st32(taddr, r);
 }
 
-// Butterfly reduce-scatter of N per-thread column values across a warp (N in {16, 32}).
-// Step s keeps the half selected by lane bit (4-s); with N=16 a final xor-1 combine
-// merges lane pairs.  On return v[0] is the warp-wide reduction of column
-// (N == 32 ? lane : lane >> 1).
-template <int N, bool kMax>
-__device__ __forceinline__ void warp_colreduce(float (&v)[N], int lane) {
-  constexpr int kSteps = N == 32 ? 5 : 4;
+// max of N values as a balanced tree (ILP instead of a serial chain)
+template <int N>
+__device__ __forceinline__ float tree_max(const float (&v)[N]) {
+  float t[N / 2];
 #pragma unroll
-  for (int step = 0; step < kSteps; ++step) {
-    const int half = (N / 2) >> step;
-    const int off = 16 >> step;
-    const bool upper = (lane & off) != 0;
+  for (int i = 0; i < N / 2; ++i) t[i] = fmaxf(v[2 * i], v[2 * i + 1]);
 #pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const float keep = upper ? v[half + i] : v[i];
-      const float send = upper ? v[i] : v[half + i];
-      const float recv = __shfl_xor_sync(0xffffffffu, send, off);
-      v[i] = kMax ? fmaxf(keep, recv) : keep + recv;
-    }
-  }
-  if (N == 16) {
-    const float recv = __shfl_xor_sync(0xffffffffu, v[0], 1);
-    v[0] = kMax ? fmaxf(v[0], recv) : v[0] + recv;
-  }
+  for (int w = N / 4; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) t[i] = fmaxf(t[2 * i], t[2 * i + 1]);
+  return t[0];
 }
 
 // Per-tile key geometry, packed: bits 0-1 key frames in the block (1|2), 2-7 first k-frame
@@ -152,12 +194,15 @@ __device__ __forceinline__ uint32_t tile_info(const DevGeom& g, int kb) {
          ((uint32_t)(8 * tw) << 20);
 }
 
-template <int D, int NQ>
-__global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, DevMask m, AttnParams p) {
-  using Cfg = AttnCfg<D, NQ>;
-  constexpr int kNK = Cfg::kNK, kNV = Cfg::kNV, kNP = Cfg::kNP, CPT = Cfg::kCPT;
+template <int D, int NQ, int SWARPS>
+__global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
+    sparse_attn_kernel(DevGeom g, DevMask m, AttnParams p) {
+  using Cfg = AttnCfg<D, NQ, SWARPS>;
+  constexpr int SW = Cfg::kSW, kNS = Cfg::kNS, kLA = Cfg::kLA, CPT = Cfg::kCPT;
+  constexpr int kNK = Cfg::kNK, kNV = Cfg::kNV, kNP = Cfg::kNP;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment for SWIZZLE_128B, by offset so the compiler keeps the shared space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem + Cfg::kOffQ;
   uint8_t* sK = smem + Cfg::kOffK;
   uint8_t* sV = smem + Cfg::kOffV;
@@ -171,17 +216,16 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
   uint64_t* v_full = k_empty + kNK;
   uint64_t* v_empty = v_full + kNV;
   uint64_t* s_full = v_empty + kNV;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
+  uint64_t* s_empty = s_full + kNS;
+  uint64_t* p_full = s_empty + kNS;
   uint64_t* p_empty = p_full + kNP;
   uint64_t* o_full = p_empty + kNP;
   uint64_t* o_empty = o_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
   float* c_s = reinterpret_cast<float*>(scratch + 256);  // [NQ] column references
   float* alpha_s = c_s + 128;                            // [NQ] rescale factors / denominators
-  float* red = alpha_s + 128;                            // [4 cg][4 quarter][CPT]
-  int* flags = reinterpret_cast<int*>(red + 512);        // [2][4 cg][4 quarter]
-  int* win = flags + 32;                                 // [4][8]: hlo, hhi, wlo, whi per q row/col
+  float* red = alpha_s + 128;                            // [CG][4 quarter][CPT]
+  int* win = reinterpret_cast<int*>(red + 512);          // [4][8]: hlo, hhi, wlo, whi per q row/col
   uint32_t* info = reinterpret_cast<uint32_t*>(win + 32);// [kInfoCap]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -205,147 +249,220 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
   };
 
   // ---- setup ----------------------------------------------------------------------------
-  if (warp == kMmaWarp) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  if (warp == Cfg::kMmaWarp) tmem_alloc(tmem_slot, Cfg::kTmemCols);
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int i = 0; i < kNK; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
     for (int i = 0; i < kNV; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
-    for (int i = 0; i < kNP; ++i) { mbar_init(p_full + i, kSoftWarps); mbar_init(p_empty + i, 1); }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(s_full + i, 1);
-      mbar_init(s_empty + i, kSoftWarps);
-      mbar_init(o_full + i, 1);
-      mbar_init(o_empty + i, kSoftWarps);
-    }
+    for (int i = 0; i < kNS; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, SW); }
+    for (int i = 0; i < kNP; ++i) { mbar_init(p_full + i, SW); mbar_init(p_empty + i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, SW); }
     fence_barrier_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS0 = tmem, tO0 = tmem + 2 * NQ;  // S buffers at [0, 2NQ), O buffers at [2NQ, 4NQ)
+  const uint32_t tS0 = tmem, tO0 = tmem + kNS * NQ;  // S buffers at [0, NS*NQ), O buffers after
 
-  if (warp == kProducerWarp) {
-    // ===================================== producer =====================================
-    if (lane == 0) {
-      long long T = 0;  // global tile counter
-      int U = 0;        // units with work
-      for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
-        int head, qtr, qtile, n;
-        const int* sel;
-        decode(u, head, qtr, qtile, n, sel);
-        if (n == 0) continue;
-        if (U >= 1) mbar_wait(q_empty, (U - 1) & 1);
+  // Per-lane metadata of tile (base + lane) of a unit's selection, fetched warp-wide once per
+  // 32 tiles and broadcast per tile with shuffles (no per-tile global round trip).
+  struct TileMeta {
+    int kcnt;
+    long long offA, offB;
+  };
+  auto fetch_meta = [&](const int* sel, int n, int base, int head) {
+    TileMeta mt{1, 0, 0};
+    const int t = base + lane;
+    if (t < n) {
+      if (sel[t] < 0 || sel[t] >= g.bnk) atomicOr(p.err, kErrInvariant);
+      const int kb = sel_at(sel, t);
+      const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+      const int f0 = g.k_tr_first[ktr];
+      mt.kcnt = g.k_tr_count[ktr];
+      mt.offA = head * p.kv_head_stride + ((long long)g.k_slot[f0] * g.n_tiles + ktile) * Cfg::kTileBytes;
+      mt.offB = mt.kcnt == 2
+                    ? head * p.kv_head_stride + ((long long)g.k_slot[f0 + 1] * g.n_tiles + ktile) * Cfg::kTileBytes
+                    : mt.offA;
+    }
+    return mt;
+  };
+  auto bcast_meta = [&](const TileMeta& mt, int src) {
+    TileMeta r;
+    r.kcnt = __shfl_sync(0xffffffffu, mt.kcnt, src);
+    r.offA = (long long)__shfl_sync(0xffffffffu, (unsigned long long)mt.offA, src);
+    r.offB = (long long)__shfl_sync(0xffffffffu, (unsigned long long)mt.offB, src);
+    return r;
+  };
+  // K or V tile -> stage: frame A rows 0-63, frame B rows 64-127 of each 64-channel sub-tile
+  auto load_kv = [&](const uint8_t* base_ptr, uint8_t* dst, const TileMeta& mt, uint64_t* bar) {
+    mbar_arrive_expect_tx(bar, mt.kcnt * Cfg::kTileBytes);
+#pragma unroll
+    for (int s = 0; s < D / 64; ++s) {
+      bulk_g2s(dst + s * 16384, base_ptr + mt.offA + s * kSubBytes, kSubBytes, bar);
+      if (mt.kcnt == 2) bulk_g2s(dst + s * 16384 + kSubBytes, base_ptr + mt.offB + s * kSubBytes, kSubBytes, bar);
+    }
+  };
+
+  if (warp == Cfg::kProducerWarp) {
+    // ================================ Q / K producer (warp-wide) =========================
+    long long T = 0;  // global tile counter
+    int U = 0;        // units with work
+    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int head, qtr, qtile, n;
+      const int* sel;
+      decode(u, head, qtr, qtile, n, sel);
+      if (n == 0) continue;
+      if (U >= 1) mbar_wait(q_empty, (U - 1) & 1);
+      if (elect_one()) {
         mbar_arrive_expect_tx(q_full, Cfg::kQBytes);
-        {
-          const int f0 = g.q_tr_first[qtr];
-          const uint8_t* qa = p.q + head * p.q_head_stride + ((long long)f0 * g.n_tiles + qtile) * Cfg::kTileBytes;
+        const int f0 = g.q_tr_first[qtr];
+        const uint8_t* qa = p.q + head * p.q_head_stride + ((long long)f0 * g.n_tiles + qtile) * Cfg::kTileBytes;
 #pragma unroll
-          for (int s = 0; s < D / 64; ++s) {
-            bulk_g2s(sQ + s * Cfg::kQSub, qa + s * kSubBytes, kSubBytes, q_full);
-            if (NQ == 128)
-              bulk_g2s(sQ + s * Cfg::kQSub + kSubBytes, qa + (long long)g.n_tiles * Cfg::kTileBytes + s * kSubBytes,
-                       kSubBytes, q_full);
+        for (int s = 0; s < D / 64; ++s) {
+          bulk_g2s(sQ + s * Cfg::kQSub, qa + s * kSubBytes, kSubBytes, q_full);
+          if (NQ == 128)
+            bulk_g2s(sQ + s * Cfg::kQSub + kSubBytes, qa + (long long)g.n_tiles * Cfg::kTileBytes + s * kSubBytes,
+                     kSubBytes, q_full);
+        }
+      }
+      __syncwarp();
+      TileMeta mine{};
+      for (int t = 0; t < n; ++t, ++T) {
+        if ((t & 31) == 0) mine = fetch_meta(sel, n, t, head);
+        const TileMeta mt = bcast_meta(mine, t & 31);
+        const int ks = (int)(T % kNK);
+        if (T >= kNK) mbar_wait(k_empty + ks, (uint32_t)((T / kNK) - 1) & 1);
+        if (elect_one()) {
+          if ((p.debug & 2) && T >= kNK) {  // experiment: no K traffic after the first stages
+            mbar_arrive(k_full + ks);
+          } else {
+            trace_at(p, 0, T);
+            load_kv(p.k, sK + ks * Cfg::kKVBytes, mt, k_full + ks);
           }
         }
-        for (int t = 0; t < n; ++t, ++T) {
-          if (sel[t] < 0 || sel[t] >= g.bnk) atomicOr(p.err, kErrInvariant);
-          const int kb = sel_at(sel, t);
-          const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
-          const int kcnt = g.k_tr_count[ktr], f0 = g.k_tr_first[ktr];
-          const long long offA =
-              head * p.kv_head_stride + ((long long)g.k_slot[f0] * g.n_tiles + ktile) * Cfg::kTileBytes;
-          const long long offB =
-              kcnt == 2 ? head * p.kv_head_stride + ((long long)g.k_slot[f0 + 1] * g.n_tiles + ktile) * Cfg::kTileBytes
-                        : 0;
-          const int ks = (int)(T % kNK);
-          if (T >= kNK) mbar_wait(k_empty + ks, (uint32_t)((T / kNK) - 1) & 1);
-          mbar_arrive_expect_tx(k_full + ks, kcnt * Cfg::kTileBytes);
-          uint8_t* dk = sK + ks * Cfg::kKVBytes;
-#pragma unroll
-          for (int s = 0; s < D / 64; ++s) {
-            bulk_g2s(dk + s * 16384, p.k + offA + s * kSubBytes, kSubBytes, k_full + ks);
-            if (kcnt == 2) bulk_g2s(dk + s * 16384 + kSubBytes, p.k + offB + s * kSubBytes, kSubBytes, k_full + ks);
-          }
-          const int vs = (int)(T % kNV);
-          if (T >= kNV) mbar_wait(v_empty + vs, (uint32_t)((T / kNV) - 1) & 1);
-          mbar_arrive_expect_tx(v_full + vs, kcnt * Cfg::kTileBytes);
-          uint8_t* dv = sV + vs * Cfg::kKVBytes;
-#pragma unroll
-          for (int s = 0; s < D / 64; ++s) {
-            bulk_g2s(dv + s * 16384, p.v + offA + s * kSubBytes, kSubBytes, v_full + vs);
-            if (kcnt == 2) bulk_g2s(dv + s * 16384 + kSubBytes, p.v + offB + s * kSubBytes, kSubBytes, v_full + vs);
+        __syncwarp();
+      }
+      ++U;
+    }
+  } else if (warp == Cfg::kVProducerWarp) {
+    // ================================ V producer (warp-wide) =============================
+    long long T = 0;
+    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int head, qtr, qtile, n;
+      const int* sel;
+      decode(u, head, qtr, qtile, n, sel);
+      TileMeta mine{};
+      for (int t = 0; t < n; ++t, ++T) {
+        if ((t & 31) == 0) mine = fetch_meta(sel, n, t, head);
+        const TileMeta mt = bcast_meta(mine, t & 31);
+        const int vs = (int)(T % kNV);
+        if (T >= kNV) mbar_wait(v_empty + vs, (uint32_t)((T / kNV) - 1) & 1);
+        if (elect_one()) {
+          if ((p.debug & 2) && T >= kNV) {
+            mbar_arrive(v_full + vs);
+          } else {
+            trace_at(p, 5, T);
+            load_kv(p.v, sV + vs * Cfg::kKVBytes, mt, v_full + vs);
           }
         }
-        ++U;
+        __syncwarp();
       }
     }
-  } else if (warp == kMmaWarp) {
-    // ===================================== MMA issuer ===================================
-    if (lane == 0) {
-      constexpr uint32_t idesc_qk = umma_idesc_bf16(128, NQ, 0, 0);
-      constexpr uint32_t idesc_pv = umma_idesc_bf16(128, NQ, 1, 1);
-      const uint32_t aQ = smem_u32(sQ);
-      long long T = 0;
-      int U = 0;
-      auto issue_pv = [&](long long G, const int* sel, int t, uint32_t tO, bool first) {
-        const int vs = (int)(G % kNV), pb = (int)(G % kNP);
-        mbar_wait(v_full + vs, (uint32_t)(G / kNV) & 1);
-        mbar_wait(p_full + pb, (uint32_t)(G / kNP) & 1);
-        tc_fence_after();
-        const int kb = sel_at(sel, t);
-        const int steps = g.k_tr_count[kb / g.n_tiles] == 2 ? 8 : 4;
-        const uint32_t aV = smem_u32(sV + vs * Cfg::kKVBytes);
-        const uint32_t aP = smem_u32(sP + pb * Cfg::kPBytes);
-        for (int kk = 0; kk < steps; ++kk) {
-          const uint64_t da = umma_desc_sw128(aV + kk * 2048, D == 128 ? 16384u : 0u, 1024u);
-          const uint64_t db = umma_desc_sw128(aP + kk * 2048, 16384u, 1024u);
-          tc_mma_f16(tO, da, db, idesc_pv, (!first || kk > 0) ? 1u : 0u);
+  } else if (warp == Cfg::kMmaWarp) {
+    // ================================ MMA issuer (warp-wide, elected lane issues) =========
+    constexpr uint32_t idesc_qk = umma_idesc_bf16(128, NQ, 0, 0);
+    constexpr uint32_t idesc_pv = umma_idesc_bf16(128, NQ, 1, 1);
+    const uint32_t aQ = smem_u32(sQ);
+    long long T = 0;
+    int U = 0;
+    auto issue_pv = [&](long long G, bool full, uint32_t tO, bool first) {
+      const int vs = (int)(G % kNV), pb = (int)(G % kNP);
+      mbar_wait(v_full + vs, (uint32_t)(G / kNV) & 1);
+      mbar_wait(p_full + pb, (uint32_t)(G / kNP) & 1);
+      tc_fence_after();
+      const uint32_t aV = smem_u32(sV + vs * Cfg::kKVBytes);
+      const uint32_t aP = smem_u32(sP + pb * Cfg::kPBytes);
+      if (elect_one()) {
+        trace_at(p, 4, G);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          if (kk < 4 || full) {  // a 64-row key block has 4 valid K=16 steps
+            const uint64_t da = umma_desc_sw128(aV + kk * 2048, D == 128 ? 16384u : 0u, 1024u);
+            const uint64_t db = umma_desc_sw128(aP + kk * 2048, 16384u, 1024u);
+            tc_mma_f16(tO, da, db, idesc_pv, (!first || kk > 0) ? 1u : 0u);
+          }
         }
+        trace_at(p, 14, G);
         tc_commit(v_empty + vs);
         tc_commit(p_empty + pb);
+        trace_at(p, 15, G);
+      }
+      __syncwarp();
+    };
+    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int head, qtr, qtile, n;
+      const int* sel;
+      decode(u, head, qtr, qtile, n, sel);
+      if (n == 0) continue;
+      const int ob = U & 1;
+      const uint32_t tO = tO0 + ob * NQ;
+      mbar_wait(q_full, U & 1);
+      uint32_t fullmask = 0, prevmask = 0;  // bit i: tile (chunk base + i) is a 128-row block
+      auto is_full = [&](int tp, int t) {
+        const uint32_t msk = (tp >> 5) == (t >> 5) ? fullmask : prevmask;
+        return ((msk >> (tp & 31)) & 1u) != 0u;
       };
-      for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
-        int head, qtr, qtile, n;
-        const int* sel;
-        decode(u, head, qtr, qtile, n, sel);
-        if (n == 0) continue;
-        const int ob = U & 1;
-        const uint32_t tO = tO0 + ob * NQ;
-        mbar_wait(q_full, U & 1);
-        if (U >= 2) mbar_wait(o_empty + ob, ((U >> 1) - 1) & 1);
-        for (int t = 0; t < n; ++t) {
-          const long long G = T + t;
-          const int ks = (int)(G % kNK), sb = (int)(G & 1);
-          mbar_wait(k_full + ks, (uint32_t)(G / kNK) & 1);
-          if (G >= 2) mbar_wait(s_empty + sb, (uint32_t)((G >> 1) - 1) & 1);
-          tc_fence_after();
-          const uint32_t aK = smem_u32(sK + ks * Cfg::kKVBytes);
+      for (int t = 0; t < n; ++t) {
+        if ((t & 31) == 0) {
+          prevmask = fullmask;
+          const int tt = t + lane;
+          fullmask = __ballot_sync(0xffffffffu, tt < n && g.k_tr_count[sel_at(sel, tt) / g.n_tiles] == 2);
+        }
+        if (t >= kLA) {
+          if (t == kLA && U >= 2) mbar_wait(o_empty + ob, ((U >> 1) - 1) & 1);  // epilogue of unit U-2 done
+          issue_pv(T + t - kLA, is_full(t - kLA, t), tO, t == kLA);
+        }
+        const long long G = T + t;
+        const int ks = (int)(G % kNK), sb = (int)(G % kNS);
+        mbar_wait(k_full + ks, (uint32_t)(G / kNK) & 1);
+        if (G >= kNS) mbar_wait(s_empty + sb, (uint32_t)((G / kNS) - 1) & 1);
+        tc_fence_after();
+        const uint32_t aK = smem_u32(sK + ks * Cfg::kKVBytes);
+        if (elect_one()) {
+          trace_at(p, 1, G);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint64_t da = umma_desc_sw128(aK + (kk >> 2) * 16384 + (kk & 3) * 32, 16u, 1024u);
             const uint64_t db = umma_desc_sw128(aQ + (kk >> 2) * Cfg::kQSub + (kk & 3) * 32, 16u, 1024u);
             tc_mma_f16(tS0 + sb * NQ, da, db, idesc_qk, kk > 0 ? 1u : 0u);
           }
+          trace_at(p, 12, G);
           tc_commit(k_empty + ks);
           tc_commit(s_full + sb);
           if (t == n - 1) tc_commit(q_empty);
-          if (t >= 1) issue_pv(G - 1, sel, t - 1, tO, t == 1);
+          trace_at(p, 13, G);
         }
-        issue_pv(T + n - 1, sel, n - 1, tO, n == 1);
-        tc_commit(o_full + ob);
-        T += n;
-        ++U;
+        __syncwarp();
       }
+      for (int tp = n > kLA ? n - kLA : 0; tp < n; ++tp) {
+        if (tp == 0 && U >= 2) mbar_wait(o_empty + ob, ((U >> 1) - 1) & 1);
+        issue_pv(T + tp, is_full(tp, n - 1), tO, tp == 0);
+      }
+      if (elect_one()) tc_commit(o_full + ob);
+      __syncwarp();
+      T += n;
+      ++U;
     }
   } else {
-    // ===================================== softmax (warps 0-15) =========================
+    // ===================================== softmax warps ================================
     const int quarter = warp & 3, cg = warp >> 2;
     const int j = quarter * 32 + lane;  // key row == TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const int col0 = cg * CPT;          // first query column of this thread
+    const int col0 = cg * CPT;          // first of this thread's CPT query columns
     const int bar_id = 1 + cg;          // named barrier of the column group (128 threads)
+    constexpr int kAllBar = 7;          // named barrier of all softmax warps
     long long T = 0;
     int U = 0;
     for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -355,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
       const int qf0 = g.q_tr_first[qtr];
       const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
       // per-unit tables: tile infos, locality windows of the 8 query rows / cols
-      for (int i = threadIdx.x; i < min(n, kInfoCap); i += kSoftWarps * 32) info[i] = tile_info(g, sel_at(sel, i));
+      for (int i = threadIdx.x; i < min(n, kInfoCap); i += SW * 32) info[i] = tile_info(g, sel_at(sel, i));
       if (threadIdx.x < 8) {
         int lo, hi;
         locality_range(m.mode, qh0 + threadIdx.x, m.extent_h, g.rows, lo, hi);
@@ -366,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
         win[24 + threadIdx.x] = hi;
       }
       if (quarter == 0 && lane < CPT) c_s[col0 + lane] = -INFINITY;
-      named_bar_sync(5, kSoftWarps * 32);
+      named_bar_sync(kAllBar, SW * 32);
       // query columns of this thread that are real tokens
       uint32_t qvalid = 0;
 #pragma unroll
@@ -375,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
         if (qh0 + (qc >> 3) < g.rows && qw0 + (qc & 7) < g.cols) qvalid |= 1u << i;
       }
       const uint32_t qfull = CPT == 32 ? 0xffffffffu : ((1u << CPT) - 1u);
-      unsigned long long my_pairs = 0;
+      uint32_t my_pairs = 0;  // <= tiles * CPT per thread per unit
       float c[CPT], lp[CPT];
 #pragma unroll
       for (int i = 0; i < CPT; ++i) { c[i] = -INFINITY; lp[i] = 0.0f; }
@@ -384,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
 
       for (int t = 0; t < n; ++t) {
         const long long G = T + t;
-        const int sb = (int)(G & 1), pb = (int)(G % kNP);
+        const int sb = (int)(G % kNS), pb = (int)(G % kNP);
         // ---- key row j: validity and allowed-query mask over this thread's columns ----
         const uint32_t inf = t < kInfoCap ? info[t] : tile_info(g, sel_at(sel, t));
         const int kcnt = inf & 3, kf0 = (inf >> 2) & 63;
@@ -421,10 +538,9 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
           }
         }
         my_pairs += __popc(mk);
-        const bool dense = mk == qfull;  // every (query, key j) pair of this thread allowed
 
         // ---- S^T row j, this thread's columns -> registers ------------------------------
-        mbar_wait(s_full + sb, (uint32_t)(G >> 1) & 1);
+        mbar_wait(s_full + sb, (uint32_t)(G / kNS) & 1);
         tc_fence_after();
         uint32_t sr[CPT];
         tmem_ld<CPT>(tS0 + sb * NQ + col0 + lane_off, sr);
@@ -432,77 +548,81 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty + sb);
+        if (threadIdx.x == 0) trace_at(p, 2, G);
 
-        float x[CPT], dmax = -INFINITY;
-        if (dense) {
+        uint32_t pk[CPT / 2];
+        if (p.debug & 1) {  // experiment: no softmax math
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) {
-            x[i] = __uint_as_float(sr[i]) * p.scale_log2;
-            dmax = fmaxf(dmax, x[i] - c[i]);
-          }
+          for (int i = 0; i < CPT / 2; ++i) pk[i] = 0x3f803f80u;  // bf16 pair (1, 1)
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) lp[i] += 1.0f;
         } else {
+          // d = s*scale*log2(e) - c  (one FFMA); masked entries -> -inf (ex2 -> 0)
+          float d[CPT];
+          if (mk == qfull) {
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) {
-            const bool ok = ((mk >> i) & 1u) != 0u;
-            x[i] = ok ? __uint_as_float(sr[i]) * p.scale_log2 : -INFINITY;
-            if (ok) dmax = fmaxf(dmax, x[i] - c[i]);
+            for (int i = 0; i < CPT; ++i) d[i] = fmaf(__uint_as_float(sr[i]), p.scale_log2, -c[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < CPT; ++i)
+              d[i] = ((mk >> i) & 1u) ? fmaf(__uint_as_float(sr[i]), p.scale_log2, -c[i]) : -INFINITY;
           }
-        }
-        const bool wneed = __any_sync(0xffffffffu, dmax > kRescaleThreshold);
-        if (lane == 0) flags[sb * 16 + cg * 4 + quarter] = wneed ? 1 : 0;
-        named_bar_sync(bar_id, 128);
-        const int* fl = flags + sb * 16 + cg * 4;
-        if ((fl[0] | fl[1] | fl[2] | fl[3]) != 0) {
-          // exact column max of this tile over the group's 128 key rows
-          float v[CPT];
+          const bool need = bar_red_or(bar_id, 128, tree_max<CPT>(d) > kRescaleThreshold);
+          if (threadIdx.x == 0) trace_at(p, 6, G);
+          if (need) {
+            // exact column max of this tile over the group's 128 key rows
+            float v[CPT];
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) v[i] = x[i];
-          warp_colreduce<CPT, true>(v, lane);
-          const int rc = CPT == 32 ? lane : (lane >> 1);
-          if (CPT == 32 || (lane & 1) == 0) red[(cg * 4 + quarter) * CPT + rc] = v[0];
-          named_bar_sync(bar_id, 128);
-          if (quarter == 0 && lane < CPT) {
-            const float* r = red + cg * 4 * CPT + lane;
-            const float mx = fmaxf(fmaxf(r[0], r[CPT]), fmaxf(r[2 * CPT], r[3 * CPT]));
-            const float cold = c_s[col0 + lane];
-            const float nw = fmaxf(cold, mx);
-            c_s[col0 + lane] = nw;
-            alpha_s[col0 + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
-          }
-          named_bar_sync(bar_id, 128);
+            for (int i = 0; i < CPT; ++i) v[i] = ((mk >> i) & 1u) ? __uint_as_float(sr[i]) * p.scale_log2 : -INFINITY;
+            warp_colreduce<CPT, true>(v, lane);
+            const int rc = CPT == 32 ? lane : (lane >> 1);
+            if (CPT == 32 || (lane & 1) == 0) red[(cg * 4 + quarter) * CPT + rc] = v[0];
+            named_bar_sync(bar_id, 128);
+            if (quarter == 0 && lane < CPT) {
+              const float* r = red + cg * 4 * CPT + lane;
+              const float mx = fmaxf(fmaxf(r[0], r[CPT]), fmaxf(r[2 * CPT], r[3 * CPT]));
+              const float cold = c_s[col0 + lane];
+              const float nw = fmaxf(cold, mx);
+              c_s[col0 + lane] = nw;
+              alpha_s[col0 + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
+            }
+            named_bar_sync(bar_id, 128);
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) {
-            c[i] = c_s[col0 + i];
-            lp[i] *= alpha_s[col0 + i];
-          }
-          if (t > 0) {
-            // O^T holds PV of this unit's tiles 0..t-1: wait for PV(G-1), rescale columns
-            mbar_wait(p_empty + ((G - 1) % kNP), (uint32_t)((G - 1) / kNP) & 1);
-            tc_fence_after();
-            if (j < D) {
-              uint32_t o[CPT];
-              tmem_ld<CPT>(tO + col0 + lane_off, o);
-              tc_wait_ld();
+            for (int i = 0; i < CPT; ++i) {
+              const float cn = c_s[col0 + i];
+              lp[i] *= alpha_s[col0 + i];
+              d[i] = ((mk >> i) & 1u) ? fmaf(__uint_as_float(sr[i]), p.scale_log2, -cn) : -INFINITY;
+              c[i] = cn;
+            }
+            if (t > 0) {
+              // O^T holds PV of this unit's tiles 0..t-1: wait for PV(G-1), rescale columns
+              mbar_wait(p_empty + ((G - 1) % kNP), (uint32_t)((G - 1) / kNP) & 1);
+              tc_fence_after();
+              if (j < D) {
+                uint32_t o[CPT];
+                tmem_ld<CPT>(tO + col0 + lane_off, o);
+                tc_wait_ld();
 #pragma unroll
-              for (int i = 0; i < CPT; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha_s[col0 + i]);
-              tmem_st<CPT>(tO + col0 + lane_off, o);
-              tc_wait_st();
+                for (int i = 0; i < CPT; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha_s[col0 + i]);
+                tmem_st<CPT>(tO + col0 + lane_off, o);
+                tc_wait_st();
+              }
             }
           }
-        }
-
-        // ---- P^T row j (bf16) and partial denominators --------------------------------
-        uint32_t pk[CPT / 2];
+          if (threadIdx.x == 0) trace_at(p, 7, G);
+          // ---- P^T row j (bf16) and partial denominators (fp32) -------------------------
 #pragma unroll
-        for (int i = 0; i < CPT / 2; ++i) {
-          const float p0 = x[2 * i] == -INFINITY ? 0.0f : ex2(x[2 * i] - c[2 * i]);
-          const float p1 = x[2 * i + 1] == -INFINITY ? 0.0f : ex2(x[2 * i + 1] - c[2 * i + 1]);
-          const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-          lp[2 * i] += __low2float(h2);
-          lp[2 * i + 1] += __high2float(h2);
-          pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
+          for (int i = 0; i < CPT / 2; ++i) {
+            const float p0 = ex2(d[2 * i]), p1 = ex2(d[2 * i + 1]);
+            lp[2 * i] += p0;
+            lp[2 * i + 1] += p1;
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+            pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
         }
+        if (threadIdx.x == 0) trace_at(p, 8, G);
         if (G >= kNP) mbar_wait(p_empty + pb, (uint32_t)((G / kNP) - 1) & 1);
+        if (threadIdx.x == 0) trace_at(p, 9, G);
         // MN-major B operand: [NQ/64 groups][128 key rows][128 B], 16-B chunks swizzled by row
         uint8_t* prow = sP + pb * Cfg::kPBytes + (col0 >> 6) * 16384 + j * 128;
         const int ch0 = (col0 & 63) >> 3;
@@ -510,17 +630,20 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
         for (int c8 = 0; c8 < CPT / 8; ++c8)
           *reinterpret_cast<uint4*>(prow + (((ch0 + c8) ^ (j & 7)) << 4)) =
               make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+        if (threadIdx.x == 0) trace_at(p, 10, G);
         fence_proxy_async_smem();
+        if (threadIdx.x == 0) trace_at(p, 11, G);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full + pb);
+        if (threadIdx.x == 0) trace_at(p, 3, G);
       }
 
       // ---- epilogue: denominators, normalise, store ------------------------------------
       if (p.pairs) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
-        if (lane == 0 && my_pairs) atomicAdd(p.pairs, my_pairs);
+        if (lane == 0 && my_pairs) atomicAdd(p.pairs, (unsigned long long)my_pairs);
       }
       warp_colreduce<CPT, false>(lp, lane);
       {
@@ -546,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
         mbar_wait(o_full + ob, (uint32_t)(U >> 1) & 1);
         tc_fence_after();
       }
-      named_bar_sync(5, kSoftWarps * 32);  // lsum visible, staging buffer free
+      named_bar_sync(kAllBar, SW * 32);  // lsum visible, staging buffer free
       if (n > 0) {
         if (j < D) {
           uint32_t o[CPT];
@@ -566,15 +689,15 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
 #pragma unroll
         for (int i = 0; i < CPT; ++i) so[(col0 + i) * D + j] = 0;
       }
-      named_bar_sync(5, kSoftWarps * 32);
+      named_bar_sync(kAllBar, SW * 32);
       constexpr int kChunks = D / 8;
       if (p.out_tile_major) {
         uint16_t* outu = p.out + u * NQ * D;
-        for (int idx = threadIdx.x; idx < NQ * kChunks; idx += kSoftWarps * 32)
+        for (int idx = threadIdx.x; idx < NQ * kChunks; idx += SW * 32)
           *reinterpret_cast<uint4*>(outu + idx * 8) = *reinterpret_cast<const uint4*>(so + idx * 8);
       } else {
         uint16_t* outh = p.out + head * p.out_head_stride;
-        for (int idx = threadIdx.x; idx < NQ * kChunks; idx += kSoftWarps * 32) {
+        for (int idx = threadIdx.x; idx < NQ * kChunks; idx += SW * 32) {
           const int col = idx / kChunks, ch = idx % kChunks, qc = col & 63;
           const int qh = qh0 + (qc >> 3), qw = qw0 + (qc & 7);
           if (qh < g.rows && qw < g.cols) {
@@ -585,7 +708,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
           }
         }
       }
-      named_bar_sync(5, kSoftWarps * 32);  // staging buffer and per-unit tables reusable
+      named_bar_sync(kAllBar, SW * 32);  // staging buffer and per-unit tables reusable
       if (n > 0) {
         T += n;
         ++U;
@@ -596,12 +719,14 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_attn_kernel(DevGeom g, Dev
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == kMmaWarp) tmem_dealloc(tmem, Cfg::kTmemCols);
+  if (warp == Cfg::kMmaWarp) tmem_dealloc(tmem, Cfg::kTmemCols);
 }
 
-template __global__ void sparse_attn_kernel<64, 64>(DevGeom, DevMask, AttnParams);
-template __global__ void sparse_attn_kernel<128, 64>(DevGeom, DevMask, AttnParams);
-template __global__ void sparse_attn_kernel<64, 128>(DevGeom, DevMask, AttnParams);
-template __global__ void sparse_attn_kernel<128, 128>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<64, 64, 8>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<128, 64, 8>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<64, 64, 16>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<128, 64, 16>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<64, 128, 16>(DevGeom, DevMask, AttnParams);
+template __global__ void sparse_attn_kernel<128, 128, 16>(DevGeom, DevMask, AttnParams);
 
 }  // namespace fvsr

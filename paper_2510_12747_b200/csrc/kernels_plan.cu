@@ -125,6 +125,96 @@ __global__ void __launch_bounds__(256) pool_partials_kernel(const uint16_t* __re
 }
 
 // ---------------------------------------------------------------------------------------
+// Fused pack + pool: one pass over a frame list writes the swizzled frame-tiles and the
+// exact-order partial sums (S0 / S1 as in pool_partials_kernel).  An optional second tensor
+// (V) is packed alongside without pooling.  One CTA per (tile, t_row group, head); thread t
+// owns channels 2t, 2t+1 (bf16x2 loads, 128 B per warp per token row).
+// ---------------------------------------------------------------------------------------
+struct PackPoolArgs {
+  const uint16_t* src;   // pooled + packed, [heads][frames * rows * cols][d]
+  const uint16_t* src2;  // packed only (may be null)
+  long long src_head_stride;  // elements (both sources)
+  uint8_t* dst;
+  uint8_t* dst2;
+  long long dst_head_stride;  // bytes
+  float* s0;
+  float* s1;
+  long long part_head_stride;  // elements
+  const float* ext_s0;         // partner S0 for single-frame groups (ring appends), may be null
+  int rows, cols, tiles_w, n_tiles, d;
+};
+
+__global__ void __launch_bounds__(64) pack_pool_kernel(PackPoolArgs a, PoolGroups groups, SlotList slots) {
+  const int tile = blockIdx.x, grp = blockIdx.y, head = blockIdx.z;
+  const int c = 2 * threadIdx.x;
+  if (c >= a.d) return;
+  const int th = tile / a.tiles_w, tw = tile % a.tiles_w;
+  const int hc = min(8, a.rows - 8 * th), wc = min(8, a.cols - 8 * tw);
+  const long long N = (long long)a.rows * a.cols;
+  const uint32_t tile_bytes = (uint32_t)a.d * 128u;
+  const int f0 = groups.first[grp], cnt = groups.count[grp], es = groups.ext_slot[grp];
+  const bool ext = cnt == 1 && es >= 0 && a.ext_s0 != nullptr;
+  const long long po = (long long)tile * a.d + c;
+  float s1x = 0.0f, s1y = 0.0f;
+  if (ext) {
+    const float* e = a.ext_s0 + head * a.part_head_stride + (long long)es * a.n_tiles * a.d + po;
+    s1x = e[0];
+    s1y = e[1];
+  }
+  for (int fi = 0; fi < cnt; ++fi) {
+    const int f = f0 + fi, slot = slots.s[f];
+    const bool cont = fi == 1 || ext;  // S1 accumulates this frame too
+    const long long so = head * a.src_head_stride + (long long)f * N * a.d + c;
+    const long long to = head * a.dst_head_stride + ((long long)slot * a.n_tiles + tile) * tile_bytes;
+    float s0x = 0.0f, s0y = 0.0f;
+    const uint16_t* __restrict__ src = a.src + so;
+    const uint16_t* __restrict__ src2 = a.src2 ? a.src2 + so : nullptr;
+    uint8_t* __restrict__ dst = a.dst + to;
+    uint8_t* __restrict__ dst2 = a.dst2 ? a.dst2 + to : nullptr;
+    constexpr int kBatch = 16;  // token rows in flight per thread
+    for (int r0 = 0; r0 < 64; r0 += kBatch) {
+      uint32_t v[kBatch], v2[kBatch];
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        const int r = r0 + i;
+        const bool valid = (r >> 3) < hc && (r & 7) < wc;
+        const long long tok = (long long)(8 * th + (r >> 3)) * a.cols + 8 * tw + (r & 7);
+        v[i] = valid ? __ldg(reinterpret_cast<const unsigned int*>(src + tok * a.d)) : 0u;
+        v2[i] = (valid && src2) ? __ldg(reinterpret_cast<const unsigned int*>(src2 + tok * a.d)) : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        const int r = r0 + i;
+        const uint32_t off = tile_byte_offset(r, c);
+        *reinterpret_cast<uint32_t*>(dst + off) = v[i];
+        if (dst2) *reinterpret_cast<uint32_t*>(dst2 + off) = v2[i];
+        if ((r >> 3) < hc && (r & 7) < wc) {
+          const float x = __uint_as_float(v[i] << 16), y = __uint_as_float(v[i] & 0xffff0000u);
+          s0x = __fadd_rn(s0x, x);
+          s0y = __fadd_rn(s0y, y);
+          if (cont) {
+            s1x = __fadd_rn(s1x, x);
+            s1y = __fadd_rn(s1y, y);
+          }
+        }
+      }
+    }
+    float* S0 = a.s0 + head * a.part_head_stride + (long long)slot * a.n_tiles * a.d + po;
+    S0[0] = s0x;
+    S0[1] = s0y;
+    if (cont) {
+      float* S1 = a.s1 + head * a.part_head_stride + (long long)slot * a.n_tiles * a.d + po;
+      S1[0] = s1x;
+      S1[1] = s1y;
+    }
+    if (fi == 0 && cnt == 2) {  // frame B continues frame A's sequence
+      s1x = s0x;
+      s1y = s0y;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // Coarse-allowed predicate for a (q-block, k-block) pair: "some token pair is allowed"
 // (coarse_allowed_mask, P/src/sparse.cpp:47-70).
 // ---------------------------------------------------------------------------------------
@@ -238,123 +328,168 @@ struct SelectParams {
   unsigned* err;
 };
 
-__global__ void __launch_bounds__(256) score_select_kernel(DevGeom g, DevMask m, SelectParams p) {
-  extern __shared__ __align__(16) uint8_t sm_raw[];
-  const int qb = blockIdx.x, head = blockIdx.y;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int d = g.d;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(sm_raw);              // [npow2]
-  float* pq = reinterpret_cast<float*>(keys + p.npow2);              // [d]
-  uint8_t* allow_f = reinterpret_cast<uint8_t*>(pq + d);             // [bnk]
-  uint8_t* sel_f = allow_f + g.bnk;                                  // [bnk]
-  __shared__ int s_nallowed;
-  __shared__ int s_warp[8];
-  __shared__ int s_running;
-  __shared__ unsigned s_err;
-  if (tid == 0) { s_nallowed = 0; s_running = 0; s_err = 0; }
+// One CTA per (head, kSelQG consecutive q-blocks), kSelThreads threads.  Pooled key rows
+// are staged once per CTA in chunks of kSelChunk blocks (warp-coalesced float4 loads, row
+// stride d+1 floats so column walks are conflict-free).  Each thread owns one key row of
+// the chunk and kSelQG/2... interleaved q-blocks, accumulating their dot products as
+// independent sequential chains (exact reference order per score, ILP across scores).
+// Selection: warp w handles q-block w; top-k by exact rank counting — rank(i) =
+// #{j : key_j > key_i} over 64-bit (orderable score, ~id) keys, i.e. the position in the
+// reference's stable_sort(score desc, id asc) — then a ballot compaction in id order.
+constexpr int kSelThreads = 256;
+constexpr int kSelQG = 8;        // q-blocks per CTA (one selection warp each)
+constexpr int kSelChunk = 128;   // key blocks staged per pass
+constexpr int kSelQPerThr = kSelQG * kSelChunk / kSelThreads;  // 4 scores per thread per chunk
 
-  const int qtr = qb / g.n_tiles, qtile = qb % g.n_tiles;
-  const int qcnt = g.q_tr_count[qtr];
-  const int qf = g.q_tr_first[qtr] + qcnt - 1;
-  const float* qsrc = (qcnt == 2 ? p.q_s1 : p.q_s0) + head * p.q_head_stride + ((long long)qf * g.n_tiles + qtile) * d;
-  const float inv_q = __fdiv_rn(1.0f, (float)(qcnt * tile_h_count(g, qtile) * tile_w_count(g, qtile)));
-  for (int c = tid; c < d; c += nthr) {
+__global__ void __launch_bounds__(kSelThreads) score_select_kernel(DevGeom g, DevMask m, SelectParams p) {
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  const int qb0 = blockIdx.x * kSelQG, head = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int d = g.d, bnk = g.bnk, ld = d + 1;
+  const int nq = min(kSelQG, g.bnq - qb0);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sm_raw);              // [kSelQG][bnk]
+  float* pq = reinterpret_cast<float*>(keys + kSelQG * bnk);         // [kSelQG][d]
+  float* pk = pq + kSelQG * d;                                       // [kSelChunk][d+1]
+  uint8_t* sel_f = reinterpret_cast<uint8_t*>(pk + kSelChunk * ld);  // [kSelQG][bnk]
+  __shared__ unsigned s_err;
+  if (tid == 0) s_err = 0;
+
+  for (int idx = tid; idx < nq * d; idx += kSelThreads) {
+    const int qq = idx / d, c = idx - qq * d;
+    const int qb = qb0 + qq;
+    const int qtr = qb / g.n_tiles, qtile = qb % g.n_tiles;
+    const int qcnt = g.q_tr_count[qtr];
+    const int qf = g.q_tr_first[qtr] + qcnt - 1;
+    const float* qsrc = (qcnt == 2 ? p.q_s1 : p.q_s0) + head * p.q_head_stride + ((long long)qf * g.n_tiles + qtile) * d;
+    const float inv_q = __fdiv_rn(1.0f, (float)(qcnt * tile_h_count(g, qtile) * tile_w_count(g, qtile)));
     const float v = __fmul_rn(qsrc[c], inv_q);
     if (!isfinite(v)) s_err = kErrShape;
-    pq[c] = v;
+    pq[qq * d + c] = v;
   }
-  __syncthreads();
 
-  int local_allowed = 0;
-  for (int kb = tid; kb < p.npow2; kb += nthr) {
-    if (kb >= g.bnk) { keys[kb] = 0; continue; }
-    const int ktr = kb / g.n_tiles, ktile = kb % g.n_tiles;
-    const int kcnt = g.k_tr_count[ktr];
-    const int kf = g.k_tr_first[ktr] + kcnt - 1;
-    const float* ksrc = (kcnt == 2 ? p.k_s1 : p.k_s0) + head * p.k_head_stride +
-                        ((long long)g.k_slot[kf] * g.n_tiles + ktile) * d;
-    const float inv_k = __fdiv_rn(1.0f, (float)(kcnt * tile_h_count(g, ktile) * tile_w_count(g, ktile)));
-    float dot = 0.0f;
+  // ---- coarse scores, chunk by chunk ----------------------------------------------------
+  for (int kb0 = 0; kb0 < bnk; kb0 += kSelChunk) {
+    const int nk = min(kSelChunk, bnk - kb0);
+    __syncthreads();  // previous chunk consumed; pq visible on the first pass
     bool fin = true;
-    for (int c = 0; c < d; ++c) {
-      const float pk = __fmul_rn(ksrc[c], inv_k);
-      fin = fin && isfinite(pk);
-      dot = __fadd_rn(dot, __fmul_rn(pq[c], pk));
+#pragma unroll 4
+    for (int r = warp; r < nk; r += kSelThreads / 32) {  // warp per pooled row
+      const int kb = kb0 + r;
+      const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+      const int kcnt = g.k_tr_count[ktr];
+      const int kf = g.k_tr_first[ktr] + kcnt - 1;
+      const float* row = (kcnt == 2 ? p.k_s1 : p.k_s0) + head * p.k_head_stride +
+                         ((long long)g.k_slot[kf] * g.n_tiles + ktile) * d;
+      const float inv_k = __fdiv_rn(1.0f, (float)(kcnt * tile_h_count(g, ktile) * tile_w_count(g, ktile)));
+      for (int c4 = lane; c4 < d / 4; c4 += 32) {
+        const float4 v = *reinterpret_cast<const float4*>(row + 4 * c4);
+        const float a = __fmul_rn(v.x, inv_k), b = __fmul_rn(v.y, inv_k);
+        const float e = __fmul_rn(v.z, inv_k), f = __fmul_rn(v.w, inv_k);
+        fin = fin && isfinite(a) && isfinite(b) && isfinite(e) && isfinite(f);
+        float* dst = pk + r * ld + 4 * c4;
+        dst[0] = a; dst[1] = b; dst[2] = e; dst[3] = f;
+      }
     }
     if (!fin) s_err = kErrShape;
-    const float s = __fmul_rn(dot, p.scale);
-    const bool al = coarse_allowed(g, m, qtr, qtile, ktr, ktile);
-    const long long o = ((long long)head * g.bnq + qb) * g.bnk + kb;
-    if (p.coarse) p.coarse[o] = s;
-    if (p.allowed) p.allowed[o] = al ? 1 : 0;
-    allow_f[kb] = al ? 1 : 0;
-    sel_f[kb] = 0;
-    keys[kb] = al ? order_key(s, kb) : 0ull;
-    local_allowed += al ? 1 : 0;
-  }
-  if (local_allowed) atomicAdd(&s_nallowed, local_allowed);
-  __syncthreads();
-
-  // bitonic sort, descending
-  for (int k = 2; k <= p.npow2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < p.npow2; i += nthr) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t a = keys[i], b = keys[ixj];
-          const bool desc = (i & k) == 0;
-          if (desc ? (a < b) : (a > b)) { keys[i] = b; keys[ixj] = a; }
-        }
+    __syncthreads();
+    // thread -> key row r = tid % kSelChunk, q-blocks qq = tid / kSelChunk + 2i
+    const int r = tid % kSelChunk, qbase = tid / kSelChunk;
+    if (r < nk) {
+      const float* row = pk + r * ld;
+      float acc[kSelQPerThr];
+#pragma unroll
+      for (int i = 0; i < kSelQPerThr; ++i) acc[i] = 0.0f;
+#pragma unroll 4
+      for (int c = 0; c < d; ++c) {
+        const float kv = row[c];
+#pragma unroll
+        for (int i = 0; i < kSelQPerThr; ++i)
+          acc[i] = __fadd_rn(acc[i], __fmul_rn(pq[(qbase + 2 * i) * d + c], kv));
       }
-      __syncthreads();
-    }
-  }
-
-  // selection: diagonal first (if coarse-allowed), then best-first skipping it
-  int dg = -1;
-  if (g.q_tr_diag[qtr] >= 0) dg = g.q_tr_diag[qtr] * g.n_tiles + qtile;
-  if (dg >= 0 && !allow_f[dg]) dg = -1;
-  if (tid == 0) {
-    long long cnt = 0;
-    if (dg >= 0) { sel_f[dg] = 1; cnt = 1; }
-    for (int i = 0; i < s_nallowed && cnt < p.topk; ++i) {
-      const int id = (int)(0xFFFFFFFFu - (uint32_t)(keys[i] & 0xFFFFFFFFull));
-      if (id != dg) { sel_f[id] = 1; ++cnt; }
+      const int kb = kb0 + r;
+      const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+#pragma unroll
+      for (int i = 0; i < kSelQPerThr; ++i) {
+        const int qq = qbase + 2 * i;
+        if (qq >= nq) continue;
+        const int qb = qb0 + qq;
+        const int qtr = qb / g.n_tiles, qtile = qb % g.n_tiles;
+        const float sc = __fmul_rn(acc[i], p.scale);
+        const bool al = coarse_allowed(g, m, qtr, qtile, ktr, ktile);
+        const long long o = ((long long)head * g.bnq + qb) * bnk + kb;
+        if (p.coarse) p.coarse[o] = sc;
+        if (p.allowed) p.allowed[o] = al ? 1 : 0;
+        keys[qq * bnk + kb] = al ? order_key(sc, kb) : 0ull;
+      }
     }
   }
   __syncthreads();
 
-  // ordered compaction of sel_f -> ascending ids
-  int* out = p.sel + ((long long)head * g.bnq + qb) * p.cap;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
-  for (int base = 0; base < g.bnk; base += nthr) {
-    const int kb = base + tid;
-    const bool f = kb < g.bnk && sel_f[kb];
-    const unsigned bal = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) s_warp[warp] = __popc(bal);
-    __syncthreads();
-    int before = s_running;
-    for (int w = 0; w < warp; ++w) before += s_warp[w];
-    if (f) {
-      const int pos = before + __popc(bal & ((1u << lane) - 1u));
-      if (pos < p.cap) out[pos] = kb;
+  // ---- selection by rank, one warp per q-block: diagonal first, then the best k' others ---
+  if (warp < nq) {
+    const int qq = warp, qb = qb0 + qq;
+    const int qtr = qb / g.n_tiles, qtile = qb % g.n_tiles;
+    const uint64_t* kq = keys + qq * bnk;
+    uint8_t* sf = sel_f + qq * bnk;
+    int dg = -1;
+    if (g.q_tr_diag[qtr] >= 0) dg = g.q_tr_diag[qtr] * g.n_tiles + qtile;
+    if (dg >= 0 && kq[dg] == 0ull) dg = -1;
+    const uint64_t kdg = dg >= 0 ? kq[dg] : ~0ull;
+    const long long kprime = p.topk - (dg >= 0 ? 1 : 0);
+    // 8 register-held candidates per lane per pass: each shared key read feeds 8 compares
+    for (int i0 = 0; i0 < bnk; i0 += 32 * 8) {
+      uint64_t kc[8];
+      int rank[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int i = i0 + v * 32 + lane;
+        kc[v] = i < bnk ? kq[i] : 0ull;
+        rank[v] = 0;
+      }
+#pragma unroll 2
+      for (int jj = 0; jj < bnk; ++jj) {
+        const uint64_t kj = kq[jj];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) rank[v] += kj > kc[v] ? 1 : 0;
+      }
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int i = i0 + v * 32 + lane;
+        if (i >= bnk) continue;
+        bool s = false;
+        if (kc[v] != 0ull) {
+          if (i == dg) {
+            s = true;
+          } else {
+            const int r = rank[v] - ((dg >= 0 && kdg > kc[v]) ? 1 : 0);  // among non-diagonal candidates
+            s = r < kprime;
+          }
+        }
+        sf[i] = s ? 1 : 0;
+      }
     }
-    __syncthreads();
-    if (tid == 0) {
-      int tot = 0;
-      for (int w = 0; w < nwarps; ++w) tot += s_warp[w];
-      s_running += tot;
+    __syncwarp();
+    int* out = p.sel + ((long long)head * g.bnq + qb) * p.cap;
+    int total = 0;
+    for (int base = 0; base < bnk; base += 32) {
+      const int kb = base + lane;
+      const bool f = kb < bnk && sf[kb];
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (f) {
+        const int pos = total + __popc(bal & ((1u << lane) - 1u));
+        if (pos < p.cap) out[pos] = kb;
+      }
+      total += __popc(bal);
     }
-    __syncthreads();
+    for (int i = total + lane; i < p.cap; i += 32) out[i] = -1;
+    if (lane == 0) {
+      p.sel_count[(long long)head * g.bnq + qb] = total;
+      if (p.diag) p.diag[(long long)head * g.bnq + qb] = dg;
+      if (total > p.cap) atomicOr(p.err, kErrInvariant);
+    }
   }
-  const int total = s_running;
-  for (int i = total + tid; i < p.cap; i += nthr) out[i] = -1;
-  if (tid == 0) {
-    p.sel_count[(long long)head * g.bnq + qb] = total;
-    if (p.diag) p.diag[(long long)head * g.bnq + qb] = dg;
-    if (total > p.cap) atomicOr(p.err, kErrInvariant);
-    if (s_err) atomicOr(p.err, s_err);
-  }
+  __syncthreads();
+  if (tid == 0 && s_err) atomicOr(p.err, s_err);
 }
 
 // ---------------------------------------------------------------------------------------
