@@ -83,6 +83,9 @@ struct fvsr_ctx {
   // staging for fvsr_ring_step_host
   void* stage = nullptr;
   size_t stage_bytes = 0;
+  // coarse block scores for the top-k pass (plan / ring attention without a user buffer)
+  float* d_scores = nullptr;
+  size_t scores_cap = 0;
 };
 
 struct fvsr_ring {
@@ -247,6 +250,32 @@ int after_launch(fvsr_ctx* ctx, cudaStream_t s, int nlaunch) {
   return FVSR_OK;
 }
 
+int launch_pack_pool(const PackPoolArgs& a, const PoolGroups& pg, const SlotList& sl, dim3 grid, int max_cnt,
+                     cudaStream_t s) {
+  if (a.d % 8 != 0) return fail(FVSR_E_CONFIG, "pack_pool: head_dim must be a multiple of 8 (got %d)", a.d);
+  if ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.src2)) % 16 != 0)
+    return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
+  const size_t smem = pack_pool_smem(a.d, max_cnt, a.src2 != nullptr);
+  static size_t configured = 48 * 1024;
+  if (smem > configured) {
+    FVSR_CUDA(cudaFuncSetAttribute(pack_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  pack_pool_kernel<<<grid, kPPThreads, smem, s>>>(a, pg, sl);
+  return FVSR_OK;
+}
+
+int ctx_reserve_scores(fvsr_ctx* ctx, size_t n) {
+  if (ctx->scores_cap >= n) return FVSR_OK;
+  if (ctx->d_scores) cudaFree(ctx->d_scores);
+  ctx->d_scores = nullptr;
+  ctx->scores_cap = 0;
+  if (cudaMalloc(&ctx->d_scores, n * sizeof(float)) != cudaSuccess)
+    return fail(FVSR_E_CUDA, "cudaMalloc(%zu) for coarse scores failed", n * sizeof(float));
+  ctx->scores_cap = n;
+  return FVSR_OK;
+}
+
 int npow2(int n) {
   int p = 1;
   while (p < n) p <<= 1;
@@ -333,16 +362,29 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
   p.coarse = coarse;
   p.allowed = allowed;
   p.err = ctx->d_err;
-  // keys[QG][bnk] | pq[QG][d] | pooled-key chunk [kSelChunk][d+1] | flags[QG][bnk]
-  const size_t ld = (size_t)g.d + 1;
-  const size_t smem = (size_t)kSelQG * g.bnk * 8 + (size_t)kSelQG * g.d * 4 + kSelChunk * ld * 4 +
-                      (size_t)kSelQG * g.bnk + 64;
-  if (smem > 220 * 1024) return fail(FVSR_E_CONFIG, "too many key blocks (%d) for the selector", g.bnk);
+  // coarse scores -> workspace (L2-resident, heads*bnq*bnk floats), then per-row top-k
+  const size_t n_scores = (size_t)heads * g.bnq * g.bnk;
+  float* scores = coarse;
+  if (!scores) {
+    if (ctx_reserve_scores(ctx, n_scores) != FVSR_OK) return FVSR_E_CUDA;
+    scores = ctx->d_scores;
+  }
+  p.coarse = nullptr;  // the score kernel writes `scores` directly
   if (g.d % 4 != 0) return fail(FVSR_E_CONFIG, "plan_sparse: head_dim must be a multiple of 4 (got %d)", g.d);
-  if (smem > 48 * 1024)
-    FVSR_CUDA(cudaFuncSetAttribute(score_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((g.bnq + kSelQG - 1) / kSelQG, heads);
-  score_select_kernel<<<grid, kSelThreads, smem, s>>>(g, dm, p);
+  const size_t smem_sc = (size_t)(kScQ + kScK) * (g.d + 4) * 4;
+  if (smem_sc > 48 * 1024)
+    FVSR_CUDA(cudaFuncSetAttribute(coarse_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sc));
+  dim3 gs((g.bnk + kScK - 1) / kScK, (g.bnq + kScQ - 1) / kScQ, heads);
+  coarse_score_kernel<<<gs, kScThreads, smem_sc, s>>>(g, dm, p, scores);
+  dim3 gt((g.bnq + kTopkWarps - 1) / kTopkWarps, heads);
+  if (g.bnk <= 32 * 8)
+    topk_select_kernel<8><<<gt, kTopkWarps * 32, 0, s>>>(g, dm, p, scores);
+  else if (g.bnk <= 32 * 32)
+    topk_select_kernel<32><<<gt, kTopkWarps * 32, 0, s>>>(g, dm, p, scores);
+  else if (g.bnk <= 32 * 128)
+    topk_select_kernel<128><<<gt, kTopkWarps * 32, 0, s>>>(g, dm, p, scores);
+  else
+    return fail(FVSR_E_CONFIG, "too many key blocks (%d > 4096) for the selector", g.bnk);
   return FVSR_OK;
 }
 
@@ -487,6 +529,7 @@ void fvsr_ctx_destroy(fvsr_ctx* ctx) {
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->stage) cudaFree(ctx->stage);
+  if (ctx->d_scores) cudaFree(ctx->d_scores);
   delete ctx;
 }
 
@@ -587,7 +630,7 @@ int32_t fvsr_plan_sparse(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k, in
   const float scale = 1.0f / std::sqrt(static_cast<float>(d));  // sparse.cpp:97
   FVSR_TRY(launch_select(ctx, g, dm, heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, ks0, ks1,
                          (long long)g.nkf * g.n_tiles * d, scale, topk, cap, sel, sel_count, diag, coarse, allowed, s));
-  return after_launch(ctx, s, 3);
+  return after_launch(ctx, s, 4);
 }
 
 int32_t fvsr_sparse_attention_exec(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v,
@@ -763,8 +806,7 @@ int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t fra
   pg.ext_slot[0] = partner;
   SlotList sl{};
   sl.s[0] = slot;
-  dim3 grid(r->n_tiles, 1, r->heads);
-  pack_pool_kernel<<<grid, 64, 0, s>>>(a, pg, sl);
+  FVSR_TRY(launch_pack_pool(a, pg, sl, dim3(r->n_tiles, 1, r->heads), 1, s));
   r->used[layer][slot] = 1;
   c.emplace_back(frame_id, slot);
   return after_launch(ctx, s, 1);
@@ -858,7 +900,9 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
       pg.ext_slot[t] = -1;
     }
     for (int i = 0; i < g.nqf; ++i) sl.s[i] = i;
-    pack_pool_kernel<<<dim3(g.n_tiles, g.nq_trows, r->heads), 64, 0, s>>>(a, pg, sl);
+    int max_cnt = 1;
+    for (int t = 0; t < g.nq_trows; ++t) max_cnt = std::max(max_cnt, g.q_tr_count[t]);
+    FVSR_TRY(launch_pack_pool(a, pg, sl, dim3(g.n_tiles, g.nq_trows, r->heads), max_cnt, s));
     const float cscale = 1.0f / std::sqrt(static_cast<float>(d));
     FVSR_TRY(launch_select(ctx, g, dm, r->heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, r->s0_layer(layer),
                            r->s1_layer(layer), r->part_head_stride(), cscale, topk, cap, use_sel, use_cnt, nullptr,
@@ -887,7 +931,7 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   p.err = ctx->d_err;
   p.pairs = ctx->d_pairs;
   FVSR_TRY(launch_attention(ctx, g, dm, p, r->heads, unit_begin, unit_end, s));
-  return after_launch(ctx, s, 3);
+  return after_launch(ctx, s, 4);
 }
 
 int32_t fvsr_ring_step_host(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* q_host,

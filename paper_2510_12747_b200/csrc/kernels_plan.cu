@@ -2,7 +2,9 @@
 //
 //   pack_frames_kernel   flat [heads][L][d] bf16  ->  swizzled frame-tiles (fvsr_common.cuh)
 //   pool_partials_kernel exact sequential fp32 block sums per frame-tile      (HBM-bound)
-//   score_select_kernel  coarse scores, coarse-allowed, top-k with forced diagonal
+//   pack_pool_kernel     fused pack + pooled partial sums (ring append / query pooling)
+//   coarse_score_kernel  coarse block scores, one thread per (q-block, k-block)
+//   topk_select_kernel   coarse-allowed, top-k with forced diagonal, one warp per q-block
 //   sparsity_count_kernel executed / dense token pairs, selected / allowed block pairs
 //
 // Bit-exactness of the plan (P = /root/reference/proj):
@@ -15,10 +17,10 @@
 //   * matmul (P/src/tensor.cpp:121-151) accumulates each coarse score over channels in
 //     ascending order from 0.0f with separate multiply and add: __fmul_rn / __fadd_rn,
 //     one thread per (q-block, k-block) pair, then __fmul_rn by 1/sqrt(d) (sparse.cpp:97-99).
-//   * selection (sparse.cpp:103-130): candidates ordered by (score desc, id asc) — we
-//     bitonic-sort 64-bit keys (orderable(score) << 32 | ~id) with -0.0 canonicalised to
-//     +0.0 (they compare equal in the reference), force the diagonal block first, fill to
-//     k, emit ascending ids.
+//   * selection (sparse.cpp:103-130): candidates ordered by (score desc, id asc) — we rank
+//     64-bit keys (orderable(score) << 32 | ~id) with -0.0 canonicalised to +0.0 (they
+//     compare equal in the reference), force the diagonal block first, take the k-1 best
+//     others by a threshold search over the unique keys, emit ascending ids.
 #include "fvsr_common.cuh"
 
 namespace fvsr {
@@ -127,8 +129,13 @@ __global__ void __launch_bounds__(256) pool_partials_kernel(const uint16_t* __re
 // ---------------------------------------------------------------------------------------
 // Fused pack + pool: one pass over a frame list writes the swizzled frame-tiles and the
 // exact-order partial sums (S0 / S1 as in pool_partials_kernel).  An optional second tensor
-// (V) is packed alongside without pooling.  One CTA per (tile, t_row group, head); thread t
-// owns channels 2t, 2t+1 (bf16x2 loads, 128 B per warp per token row).
+// (V) is packed alongside without pooling.  One CTA (kPPThreads) per (tile, t_row group,
+// head).  A tile row of 8 tokens is 8*d*2 contiguous bytes in the token-major source, so
+// one elected thread stages the group's tiles into shared memory with one cp.async.bulk per
+// tile row (all loads of the CTA in flight at once, no registers held); then threads
+// < d/2 pool channels 2t, 2t+1 in token order from shared memory while every thread writes
+// the swizzled tiles with coalesced 16-byte stores (thread i writes destination chunk i;
+// the source chunk is the inverse swizzle).  Requires d % 8 == 0 (16-byte rows).
 // ---------------------------------------------------------------------------------------
 struct PackPoolArgs {
   const uint16_t* src;   // pooled + packed, [heads][frames * rows * cols][d]
@@ -144,72 +151,110 @@ struct PackPoolArgs {
   int rows, cols, tiles_w, n_tiles, d;
 };
 
-__global__ void __launch_bounds__(64) pack_pool_kernel(PackPoolArgs a, PoolGroups groups, SlotList slots) {
+constexpr int kPPThreads = 128;
+
+// shared bytes: [cnt frames][1 or 2 tensors][64 rows][d] bf16 + barrier
+inline size_t pack_pool_smem(int d, int max_cnt, bool two) {
+  return (size_t)max_cnt * (two ? 2 : 1) * 64 * d * 2 + 16;
+}
+
+__global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_constant__ PackPoolArgs a,
+                                                               const __grid_constant__ PoolGroups groups,
+                                                               const __grid_constant__ SlotList slots) {
+  extern __shared__ __align__(128) uint8_t sm_pp[];
   const int tile = blockIdx.x, grp = blockIdx.y, head = blockIdx.z;
-  const int c = 2 * threadIdx.x;
-  if (c >= a.d) return;
-  const int th = tile / a.tiles_w, tw = tile % a.tiles_w;
+  const int tid = threadIdx.x;
+  const int d = a.d;
+  const int th = tile / a.tiles_w, tw = tile - th * a.tiles_w;
   const int hc = min(8, a.rows - 8 * th), wc = min(8, a.cols - 8 * tw);
   const long long N = (long long)a.rows * a.cols;
-  const uint32_t tile_bytes = (uint32_t)a.d * 128u;
+  const uint32_t tile_bytes = (uint32_t)d * 128u;
   const int f0 = groups.first[grp], cnt = groups.count[grp], es = groups.ext_slot[grp];
-  const bool ext = cnt == 1 && es >= 0 && a.ext_s0 != nullptr;
-  const long long po = (long long)tile * a.d + c;
-  float s1x = 0.0f, s1y = 0.0f;
-  if (ext) {
-    const float* e = a.ext_s0 + head * a.part_head_stride + (long long)es * a.n_tiles * a.d + po;
-    s1x = e[0];
-    s1y = e[1];
+  const int nt = a.src2 ? 2 : 1;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm_pp + (size_t)cnt * nt * tile_bytes);
+  auto stage = [&](int fi, int t) -> uint8_t* { return sm_pp + (size_t)(fi * nt + t) * tile_bytes; };
+  const bool full = hc == 8 && wc == 8;
+  if (!full) {  // edge tile: rows / columns past the frame are zero
+    for (int i = tid; i < cnt * nt * (int)tile_bytes / 16; i += kPPThreads)
+      reinterpret_cast<uint4*>(sm_pp)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
   }
-  for (int fi = 0; fi < cnt; ++fi) {
-    const int f = f0 + fi, slot = slots.s[f];
-    const bool cont = fi == 1 || ext;  // S1 accumulates this frame too
-    const long long so = head * a.src_head_stride + (long long)f * N * a.d + c;
-    const long long to = head * a.dst_head_stride + ((long long)slot * a.n_tiles + tile) * tile_bytes;
-    float s0x = 0.0f, s0y = 0.0f;
-    const uint16_t* __restrict__ src = a.src + so;
-    const uint16_t* __restrict__ src2 = a.src2 ? a.src2 + so : nullptr;
-    uint8_t* __restrict__ dst = a.dst + to;
-    uint8_t* __restrict__ dst2 = a.dst2 ? a.dst2 + to : nullptr;
-    constexpr int kBatch = 16;  // token rows in flight per thread
-    for (int r0 = 0; r0 < 64; r0 += kBatch) {
-      uint32_t v[kBatch], v2[kBatch];
-#pragma unroll
-      for (int i = 0; i < kBatch; ++i) {
-        const int r = r0 + i;
-        const bool valid = (r >> 3) < hc && (r & 7) < wc;
-        const long long tok = (long long)(8 * th + (r >> 3)) * a.cols + 8 * tw + (r & 7);
-        v[i] = valid ? __ldg(reinterpret_cast<const unsigned int*>(src + tok * a.d)) : 0u;
-        v2[i] = (valid && src2) ? __ldg(reinterpret_cast<const unsigned int*>(src2 + tok * a.d)) : 0u;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    fence_proxy_async_smem();
+    const uint32_t row_bytes = (uint32_t)wc * d * 2;
+    mbar_arrive_expect_tx(bar, row_bytes * hc * cnt * nt);
+    for (int fi = 0; fi < cnt; ++fi)
+      for (int t = 0; t < nt; ++t) {
+        const uint16_t* src = (t == 0 ? a.src : a.src2) + head * a.src_head_stride + (long long)(f0 + fi) * N * d;
+        for (int rh = 0; rh < hc; ++rh) {
+          const long long tok = (long long)(8 * th + rh) * a.cols + 8 * tw;
+          bulk_g2s(stage(fi, t) + rh * 8 * d * 2, src + tok * d, row_bytes, bar);
+        }
       }
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // pooling (exact token order; rows past the frame are skipped, not added as zeros)
+  if (2 * tid < d) {
+    const int c = 2 * tid;
+    const long long po = (long long)tile * d + c;
+    const bool ext = cnt == 1 && es >= 0 && a.ext_s0 != nullptr;
+    float s1x = 0.0f, s1y = 0.0f;
+    if (ext) {
+      const float* e = a.ext_s0 + head * a.part_head_stride + (long long)es * a.n_tiles * d + po;
+      s1x = e[0];
+      s1y = e[1];
+    }
+    for (int fi = 0; fi < cnt; ++fi) {
+      const int slot = slots.s[f0 + fi];
+      const bool cont = fi == 1 || ext;
+      const uint8_t* st = stage(fi, 0);
+      float s0x = 0.0f, s0y = 0.0f;
+      for (int rh = 0; rh < hc; ++rh) {
 #pragma unroll
-      for (int i = 0; i < kBatch; ++i) {
-        const int r = r0 + i;
-        const uint32_t off = tile_byte_offset(r, c);
-        *reinterpret_cast<uint32_t*>(dst + off) = v[i];
-        if (dst2) *reinterpret_cast<uint32_t*>(dst2 + off) = v2[i];
-        if ((r >> 3) < hc && (r & 7) < wc) {
-          const float x = __uint_as_float(v[i] << 16), y = __uint_as_float(v[i] & 0xffff0000u);
-          s0x = __fadd_rn(s0x, x);
-          s0y = __fadd_rn(s0y, y);
-          if (cont) {
-            s1x = __fadd_rn(s1x, x);
-            s1y = __fadd_rn(s1y, y);
+        for (int rw = 0; rw < 8; ++rw) {
+          if (rw < wc) {
+            const uint32_t v = *reinterpret_cast<const uint32_t*>(st + ((rh * 8 + rw) * d + c) * 2);
+            const float x = __uint_as_float(v << 16), y = __uint_as_float(v & 0xffff0000u);
+            s0x = __fadd_rn(s0x, x);
+            s0y = __fadd_rn(s0y, y);
+            if (cont) {
+              s1x = __fadd_rn(s1x, x);
+              s1y = __fadd_rn(s1y, y);
+            }
           }
         }
       }
+      float* S0 = a.s0 + head * a.part_head_stride + (long long)slot * a.n_tiles * d + po;
+      S0[0] = s0x;
+      S0[1] = s0y;
+      if (cont) {
+        float* S1 = a.s1 + head * a.part_head_stride + (long long)slot * a.n_tiles * d + po;
+        S1[0] = s1x;
+        S1[1] = s1y;
+      }
+      if (fi == 0 && cnt == 2) {  // frame B continues frame A's sequence
+        s1x = s0x;
+        s1y = s0y;
+      }
     }
-    float* S0 = a.s0 + head * a.part_head_stride + (long long)slot * a.n_tiles * a.d + po;
-    S0[0] = s0x;
-    S0[1] = s0y;
-    if (cont) {
-      float* S1 = a.s1 + head * a.part_head_stride + (long long)slot * a.n_tiles * a.d + po;
-      S1[0] = s1x;
-      S1[1] = s1y;
-    }
-    if (fi == 0 && cnt == 2) {  // frame B continues frame A's sequence
-      s1x = s0x;
-      s1y = s0y;
+  }
+  // packing: destination chunk i (16 B) of a tile <- source (row r, channel chunk)
+  const int chunks = (int)tile_bytes / 16;
+  for (int fi = 0; fi < cnt; ++fi) {
+    const int slot = slots.s[f0 + fi];
+    const long long to = head * a.dst_head_stride + ((long long)slot * a.n_tiles + tile) * tile_bytes;
+    for (int t = 0; t < nt; ++t) {
+      const uint8_t* st = stage(fi, t);
+      uint8_t* dst = (t == 0 ? a.dst : a.dst2) + to;
+      for (int i = tid; i < chunks; i += kPPThreads) {
+        const int panel = i >> 9, r = (i >> 3) & 63, j = i & 7;
+        const int c = panel * 64 + ((j ^ (r & 7)) << 3);
+        const uint4 v = *reinterpret_cast<const uint4*>(st + (r * d + c) * 2);
+        *reinterpret_cast<uint4*>(dst + (size_t)i * 16) = v;
+      }
     }
   }
 }
@@ -266,6 +311,13 @@ __device__ inline bool coarse_allowed(const DevGeom& g, const DevMask& m, int qt
            range_overlap(m.mode, qw0, tile_w_count(g, qtile), kw0, tile_w_count(g, ktile), m.extent_w, g.cols);
   }
   return bitmask_pair_any(g, m, qtr, qtile, ktr, ktile, false, nullptr);
+}
+
+// out-of-line variant for mask kinds other than "all" (keeps the selector's unrolled
+// candidate loop small; kind 0 never calls it)
+__device__ __noinline__ bool coarse_allowed_masked(const DevGeom& g, const DevMask& m, int qtr, int qtile, int ktr,
+                                                   int ktile) {
+  return coarse_allowed(g, m, qtr, qtile, ktr, ktile);
 }
 
 // number of allowed (q, k) coordinate pairs along one axis for locality
@@ -328,169 +380,225 @@ struct SelectParams {
   unsigned* err;
 };
 
-// One CTA per (head, kSelQG consecutive q-blocks), kSelThreads threads.  Pooled key rows
-// are staged once per CTA in chunks of kSelChunk blocks (warp-coalesced float4 loads, row
-// stride d+1 floats so column walks are conflict-free).  Each thread owns one key row of
-// the chunk and kSelQG/2... interleaved q-blocks, accumulating their dot products as
-// independent sequential chains (exact reference order per score, ILP across scores).
-// Selection: warp w handles q-block w; top-k by exact rank counting — rank(i) =
-// #{j : key_j > key_i} over 64-bit (orderable score, ~id) keys, i.e. the position in the
-// reference's stable_sort(score desc, id asc) — then a ballot compaction in id order.
-constexpr int kSelThreads = 256;
-constexpr int kSelQG = 8;        // q-blocks per CTA (one selection warp each)
-constexpr int kSelChunk = 128;   // key blocks staged per pass
-constexpr int kSelQPerThr = kSelQG * kSelChunk / kSelThreads;  // 4 scores per thread per chunk
-
-__global__ void __launch_bounds__(kSelThreads) score_select_kernel(DevGeom g, DevMask m, SelectParams p) {
-  extern __shared__ __align__(16) uint8_t sm_raw[];
-  const int qb0 = blockIdx.x * kSelQG, head = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int d = g.d, bnk = g.bnk, ld = d + 1;
-  const int nq = min(kSelQG, g.bnq - qb0);
-  uint64_t* keys = reinterpret_cast<uint64_t*>(sm_raw);              // [kSelQG][bnk]
-  float* pq = reinterpret_cast<float*>(keys + kSelQG * bnk);         // [kSelQG][d]
-  float* pk = pq + kSelQG * d;                                       // [kSelChunk][d+1]
-  uint8_t* sel_f = reinterpret_cast<uint8_t*>(pk + kSelChunk * ld);  // [kSelQG][bnk]
-  __shared__ unsigned s_err;
-  if (tid == 0) s_err = 0;
-
-  for (int idx = tid; idx < nq * d; idx += kSelThreads) {
-    const int qq = idx / d, c = idx - qq * d;
-    const int qb = qb0 + qq;
-    const int qtr = qb / g.n_tiles, qtile = qb % g.n_tiles;
-    const int qcnt = g.q_tr_count[qtr];
-    const int qf = g.q_tr_first[qtr] + qcnt - 1;
-    const float* qsrc = (qcnt == 2 ? p.q_s1 : p.q_s0) + head * p.q_head_stride + ((long long)qf * g.n_tiles + qtile) * d;
-    const float inv_q = __fdiv_rn(1.0f, (float)(qcnt * tile_h_count(g, qtile) * tile_w_count(g, qtile)));
-    const float v = __fmul_rn(qsrc[c], inv_q);
-    if (!isfinite(v)) s_err = kErrShape;
-    pq[qq * d + c] = v;
-  }
-
-  // ---- coarse scores, chunk by chunk ----------------------------------------------------
-  for (int kb0 = 0; kb0 < bnk; kb0 += kSelChunk) {
-    const int nk = min(kSelChunk, bnk - kb0);
-    __syncthreads();  // previous chunk consumed; pq visible on the first pass
-    bool fin = true;
-#pragma unroll 4
-    for (int r = warp; r < nk; r += kSelThreads / 32) {  // warp per pooled row
-      const int kb = kb0 + r;
-      const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
-      const int kcnt = g.k_tr_count[ktr];
-      const int kf = g.k_tr_first[ktr] + kcnt - 1;
-      const float* row = (kcnt == 2 ? p.k_s1 : p.k_s0) + head * p.k_head_stride +
-                         ((long long)g.k_slot[kf] * g.n_tiles + ktile) * d;
-      const float inv_k = __fdiv_rn(1.0f, (float)(kcnt * tile_h_count(g, ktile) * tile_w_count(g, ktile)));
-      for (int c4 = lane; c4 < d / 4; c4 += 32) {
-        const float4 v = *reinterpret_cast<const float4*>(row + 4 * c4);
-        const float a = __fmul_rn(v.x, inv_k), b = __fmul_rn(v.y, inv_k);
-        const float e = __fmul_rn(v.z, inv_k), f = __fmul_rn(v.w, inv_k);
-        fin = fin && isfinite(a) && isfinite(b) && isfinite(e) && isfinite(f);
-        float* dst = pk + r * ld + 4 * c4;
-        dst[0] = a; dst[1] = b; dst[2] = e; dst[3] = f;
-      }
-    }
-    if (!fin) s_err = kErrShape;
-    __syncthreads();
-    // thread -> key row r = tid % kSelChunk, q-blocks qq = tid / kSelChunk + 2i
-    const int r = tid % kSelChunk, qbase = tid / kSelChunk;
-    if (r < nk) {
-      const float* row = pk + r * ld;
-      float acc[kSelQPerThr];
-#pragma unroll
-      for (int i = 0; i < kSelQPerThr; ++i) acc[i] = 0.0f;
-#pragma unroll 4
-      for (int c = 0; c < d; ++c) {
-        const float kv = row[c];
-#pragma unroll
-        for (int i = 0; i < kSelQPerThr; ++i)
-          acc[i] = __fadd_rn(acc[i], __fmul_rn(pq[(qbase + 2 * i) * d + c], kv));
-      }
-      const int kb = kb0 + r;
-      const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
-#pragma unroll
-      for (int i = 0; i < kSelQPerThr; ++i) {
-        const int qq = qbase + 2 * i;
-        if (qq >= nq) continue;
-        const int qb = qb0 + qq;
-        const int qtr = qb / g.n_tiles, qtile = qb % g.n_tiles;
-        const float sc = __fmul_rn(acc[i], p.scale);
-        const bool al = coarse_allowed(g, m, qtr, qtile, ktr, ktile);
-        const long long o = ((long long)head * g.bnq + qb) * bnk + kb;
-        if (p.coarse) p.coarse[o] = sc;
-        if (p.allowed) p.allowed[o] = al ? 1 : 0;
-        keys[qq * bnk + kb] = al ? order_key(sc, kb) : 0ull;
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- selection by rank, one warp per q-block: diagonal first, then the best k' others ---
-  if (warp < nq) {
-    const int qq = warp, qb = qb0 + qq;
-    const int qtr = qb / g.n_tiles, qtile = qb % g.n_tiles;
-    const uint64_t* kq = keys + qq * bnk;
-    uint8_t* sf = sel_f + qq * bnk;
-    int dg = -1;
-    if (g.q_tr_diag[qtr] >= 0) dg = g.q_tr_diag[qtr] * g.n_tiles + qtile;
-    if (dg >= 0 && kq[dg] == 0ull) dg = -1;
-    const uint64_t kdg = dg >= 0 ? kq[dg] : ~0ull;
-    const long long kprime = p.topk - (dg >= 0 ? 1 : 0);
-    // 8 register-held candidates per lane per pass: each shared key read feeds 8 compares
-    for (int i0 = 0; i0 < bnk; i0 += 32 * 8) {
-      uint64_t kc[8];
-      int rank[8];
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const int i = i0 + v * 32 + lane;
-        kc[v] = i < bnk ? kq[i] : 0ull;
-        rank[v] = 0;
-      }
-#pragma unroll 2
-      for (int jj = 0; jj < bnk; ++jj) {
-        const uint64_t kj = kq[jj];
-#pragma unroll
-        for (int v = 0; v < 8; ++v) rank[v] += kj > kc[v] ? 1 : 0;
-      }
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const int i = i0 + v * 32 + lane;
-        if (i >= bnk) continue;
-        bool s = false;
-        if (kc[v] != 0ull) {
-          if (i == dg) {
-            s = true;
-          } else {
-            const int r = rank[v] - ((dg >= 0 && kdg > kc[v]) ? 1 : 0);  // among non-diagonal candidates
-            s = r < kprime;
-          }
-        }
-        sf[i] = s ? 1 : 0;
-      }
-    }
-    __syncwarp();
-    int* out = p.sel + ((long long)head * g.bnq + qb) * p.cap;
-    int total = 0;
-    for (int base = 0; base < bnk; base += 32) {
-      const int kb = base + lane;
-      const bool f = kb < bnk && sf[kb];
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      if (f) {
-        const int pos = total + __popc(bal & ((1u << lane) - 1u));
-        if (pos < p.cap) out[pos] = kb;
-      }
-      total += __popc(bal);
-    }
-    for (int i = total + lane; i < p.cap; i += 32) out[i] = -1;
-    if (lane == 0) {
-      p.sel_count[(long long)head * g.bnq + qb] = total;
-      if (p.diag) p.diag[(long long)head * g.bnq + qb] = dg;
-      if (total > p.cap) atomicOr(p.err, kErrInvariant);
-    }
-  }
-  __syncthreads();
-  if (tid == 0 && s_err) atomicOr(p.err, s_err);
+__device__ inline uint32_t order_score(float s) {  // order_key's upper half; 0 = no candidate
+  uint32_t u = __float_as_uint(s == 0.0f ? 0.0f : s);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+
+// Coarse scores over shared-memory tiles of kScQ pooled queries x kScK pooled keys, row
+// stride d+4 floats (16-byte aligned rows; the 4-float skew spreads the 8 rows one LDS.128
+// wavefront touches over all banks).  Thread t owns queries 2*(t/16) + {0,1} and keys
+// t%16 + 16*{0..3}: 8 independent exact chains, 6 LDS.128 per 4 channels.  Every chain is
+// the reference's sequential fp32 order (see file header): channels ascending, separate
+// multiply and add from 0.0f, then the 1/sqrt(d) multiply.
+constexpr int kScQ = 16, kScK = 64, kScThreads = 128;
+
+__device__ inline void chain4(float& acc, const float4& a, const float4& b) {
+  acc = __fadd_rn(acc, __fmul_rn(a.x, b.x));
+  acc = __fadd_rn(acc, __fmul_rn(a.y, b.y));
+  acc = __fadd_rn(acc, __fmul_rn(a.z, b.z));
+  acc = __fadd_rn(acc, __fmul_rn(a.w, b.w));
+}
+
+__global__ void __launch_bounds__(kScThreads) coarse_score_kernel(DevGeom g, DevMask m, SelectParams p,
+                                                                 float* __restrict__ scores) {
+  extern __shared__ __align__(16) float smf[];
+  const int d = g.d, ld = d + 4, d4 = d >> 2;
+  float* pq = smf;              // [kScQ][d+4]
+  float* pk = smf + kScQ * ld;  // [kScK][d+4]
+  const int kb0 = blockIdx.x * kScK, qb0 = blockIdx.y * kScQ, head = blockIdx.z;
+  const int tid = threadIdx.x;
+  // per staged row: source pointer and 1/count (rows past the grid stage zeros)
+  __shared__ const float* row_src[kScQ + kScK];
+  __shared__ float row_inv[kScQ + kScK];
+  if (tid < kScQ + kScK) {
+    const int r = tid;
+    const float* src = nullptr;
+    int cnt_tok = 1;
+    if (r < kScQ) {
+      const int qb = qb0 + r;
+      if (qb < g.bnq) {
+        const int qtr = qb / g.n_tiles, qtile = qb - qtr * g.n_tiles;
+        const int qcnt = g.q_tr_count[qtr];
+        const int qf = g.q_tr_first[qtr] + qcnt - 1;
+        src = (qcnt == 2 ? p.q_s1 : p.q_s0) + head * p.q_head_stride + ((long long)qf * g.n_tiles + qtile) * d;
+        cnt_tok = qcnt * tile_h_count(g, qtile) * tile_w_count(g, qtile);
+      }
+    } else {
+      const int kb = kb0 + r - kScQ;
+      if (kb < g.bnk) {
+        const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+        const int kcnt = g.k_tr_count[ktr];
+        const int kf = g.k_tr_first[ktr] + kcnt - 1;
+        src = (kcnt == 2 ? p.k_s1 : p.k_s0) + head * p.k_head_stride +
+              ((long long)g.k_slot[kf] * g.n_tiles + ktile) * d;
+        cnt_tok = kcnt * tile_h_count(g, ktile) * tile_w_count(g, ktile);
+      }
+    }
+    row_src[r] = src;
+    row_inv[r] = __fdiv_rn(1.0f, (float)cnt_tok);
+  }
+  __syncthreads();
+  // stage: warp w copies rows w, w+4, ...; lane = float4 column; kB rows in flight
+  bool fin = true;
+  constexpr int kB = 10, kRows = kScQ + kScK, kWarps = kScThreads / 32;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int c4 = lane; c4 < d4; c4 += 32) {
+#pragma unroll 1
+    for (int r0 = warp; r0 < kRows; r0 += kB * kWarps) {
+      float4 v[kB];
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const int r = r0 + j * kWarps;
+        const float* src = r < kRows ? row_src[r] : nullptr;
+        v[j] = src ? __ldg(reinterpret_cast<const float4*>(src) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const int r = r0 + j * kWarps;
+        if (r < kRows) {
+          const float inv = row_inv[r];
+          float4 w = v[j];
+          w.x = __fmul_rn(w.x, inv);
+          w.y = __fmul_rn(w.y, inv);
+          w.z = __fmul_rn(w.z, inv);
+          w.w = __fmul_rn(w.w, inv);
+          fin = fin && isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w);
+          *reinterpret_cast<float4*>(smf + r * ld + c4 * 4) = w;
+        }
+      }
+    }
+  }
+  if (!fin) atomicOr(p.err, kErrShape);
+  __syncthreads();
+  const int kq = tid & 15, qg = tid >> 4;
+  const float* q0 = pq + (2 * qg) * ld;
+  const float* q1 = q0 + ld;
+  const float* k0 = pk + kq * ld;
+  float acc[2][4] = {};
+#pragma unroll 4
+  for (int c = 0; c < d; c += 4) {
+    const float4 a0 = *reinterpret_cast<const float4*>(q0 + c);
+    const float4 a1 = *reinterpret_cast<const float4*>(q1 + c);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 b = *reinterpret_cast<const float4*>(k0 + 16 * j * ld + c);
+      chain4(acc[0][j], a0, b);
+      chain4(acc[1][j], a1, b);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int qb = qb0 + 2 * qg + i;
+    if (qb >= g.bnq) continue;
+    float* row = scores + ((long long)head * g.bnq + qb) * g.bnk;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int kb = kb0 + kq + 16 * j;
+      if (kb < g.bnk) row[kb] = __fmul_rn(acc[i][j], p.scale);
+    }
+  }
+}
+
+// Top-k per (head, q-block): one warp each, the row's candidates held in registers
+// (NPER per lane, key block kb = 32*i + lane).  Candidates are the coarse-allowed key
+// blocks other than the diagonal, ranked by (score desc, id asc) == the reference's
+// stable_sort (sparse.cpp:103-130).  The diagonal block (if allowed) is forced first and
+// counts toward k.  Threshold T = the kprime-th largest orderable score, by a 32-round
+// bitwise search whose counts are ballot popcounts (no shuffles); all candidates above T
+// are taken, and the lowest ids among those equal to T fill the rest — exactly the
+// stable-sort prefix.  A ballot compaction emits ascending ids.
+constexpr int kTopkWarps = 8;
+
+template <int NPER>
+__global__ void __launch_bounds__(kTopkWarps * 32) topk_select_kernel(const __grid_constant__ DevGeom g,
+                                                                     const __grid_constant__ DevMask m,
+                                                                     const __grid_constant__ SelectParams p,
+                                                                     const float* __restrict__ scores) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int qb = blockIdx.x * kTopkWarps + warp;
+  if (qb >= g.bnq) return;
+  const int head = blockIdx.y;
+  const int bnk = g.bnk;
+  const int qtr = qb / g.n_tiles, qtile = qb - qtr * g.n_tiles;
+  const long long row = (long long)head * g.bnq + qb;
+  const float* sc = scores + row * bnk;
+  int dg = -1;
+  if (g.q_tr_diag[qtr] >= 0) dg = g.q_tr_diag[qtr] * g.n_tiles + qtile;
+  uint32_t os[NPER];
+  float sv[NPER];
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {  // all loads in flight before any use
+    const int kb = 32 * i + lane;
+    sv[i] = kb < bnk ? __ldg(sc + kb) : 0.0f;
+  }
+  bool dg_ok = false;
+  int n_cand = 0;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int kb = 32 * i + lane;
+    bool al = kb < bnk;
+    if (m.kind != 0 && al) {
+      const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+      al = coarse_allowed_masked(g, m, qtr, qtile, ktr, ktile);
+    }
+    if (kb < bnk) {
+      if (p.coarse) p.coarse[row * bnk + kb] = sv[i];
+      if (p.allowed) p.allowed[row * bnk + kb] = al ? 1 : 0;
+    }
+    if (al && kb == dg) dg_ok = true;
+    os[i] = (al && kb != dg) ? order_score(sv[i]) : 0u;
+    n_cand += __popc(__ballot_sync(0xffffffffu, os[i] != 0u));
+  }
+  if (!__any_sync(0xffffffffu, dg_ok)) dg = -1;
+  const long long kp64 = p.topk - (dg >= 0 ? 1 : 0);
+  const int kprime = kp64 > (long long)INT32_MAX ? INT32_MAX : (int)kp64;
+  uint32_t T = 1u;  // every candidate
+  int take_eq = 1 << 30;
+  if (kprime <= 0) {
+    T = 0xFFFFFFFFu;
+    take_eq = 0;
+  } else if (kprime < n_cand) {
+    uint32_t prefix = 0u;
+#pragma unroll 1
+    for (int bit = 31; bit >= 0; --bit) {
+      const uint32_t trial = prefix | (1u << bit);
+      int cnt = 0;
+#pragma unroll
+      for (int i = 0; i < NPER; ++i) cnt += __popc(__ballot_sync(0xffffffffu, os[i] >= trial));
+      if (cnt >= kprime) prefix = trial;
+    }
+    T = prefix;
+    int gt = 0;
+#pragma unroll
+    for (int i = 0; i < NPER; ++i) gt += __popc(__ballot_sync(0xffffffffu, os[i] > T));
+    take_eq = kprime - gt;
+  }
+  int* out = p.sel + row * p.cap;
+  const unsigned lt = (1u << lane) - 1u;
+  int total = 0, eq_seen = 0;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int kb = 32 * i + lane;
+    const bool eq = os[i] != 0u && os[i] == T;
+    const unsigned be = __ballot_sync(0xffffffffu, eq);
+    const bool f = (os[i] != 0u && os[i] > T) || (eq && eq_seen + __popc(be & lt) < take_eq) || (kb == dg);
+    eq_seen += __popc(be);
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (f) {
+      const int pos = total + __popc(bal & lt);
+      if (pos < p.cap) out[pos] = kb;
+    }
+    total += __popc(bal);
+  }
+  for (int i = total + lane; i < p.cap; i += 32) out[i] = -1;
+  if (lane == 0) {
+    p.sel_count[row] = total;
+    if (p.diag) p.diag[row] = dg;
+    if (total > p.cap) atomicOr(p.err, kErrInvariant);
+  }
+}
+
 
 // ---------------------------------------------------------------------------------------
 // sparsity accounting (sparsity_report, P/src/sparse.cpp:256-285): one CTA per (q-block, head)
