@@ -42,6 +42,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", SRC]
+    if os.environ.get("FVSR_ATTN_INSTRUMENT"):  # experiments: per-tile timelines, debug short-cuts
+        cmd.insert(1, "-DFVSR_ATTN_INSTRUMENT=1")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

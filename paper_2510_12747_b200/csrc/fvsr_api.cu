@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -388,33 +389,27 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
   return FVSR_OK;
 }
 
-template <int D, int NQ, int SW>
-int launch_attn_dqw(const DevGeom& g, const DevMask& dm, const AttnParams& p, int sms, cudaStream_t s) {
-  using Cfg = AttnCfg<D, NQ, SW>;
+template <int D, int NQ, int MK>
+int launch_attn_dqm(const DevGeom& g, const DevMask& dm, const AttnParams& p, int sms, cudaStream_t s) {
+  using Cfg = AttnCfg<D, NQ, 16>;
   static bool configured = false;
   if (!configured) {
-    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D, NQ, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D, NQ, 16, MK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)Cfg::kBytes));
     configured = true;
   }
   const long long units = p.unit_end - p.unit_begin;
   if (units <= 0) return FVSR_OK;
   const unsigned grid = (unsigned)std::min<long long>(units, sms);  // persistent CTAs
-  sparse_attn_kernel<D, NQ, SW><<<grid, Cfg::kThreads, Cfg::kBytes, s>>>(g, dm, p);
+  sparse_attn_kernel<D, NQ, 16, MK><<<grid, Cfg::kThreads, Cfg::kBytes, s>>>(g, dm, p);
   return FVSR_OK;
 }
 
 template <int D, int NQ>
 int launch_attn_dq(const DevGeom& g, const DevMask& dm, const AttnParams& p, int sms, cudaStream_t s) {
-  if (NQ == 64) {
-    static const int sw = [] {
-      const char* e = std::getenv("FVSR_SOFT_WARPS");  // experiments: 8 or 16 softmax warps
-      return e ? std::atoi(e) : 16;
-    }();
-    if (sw == 8) return launch_attn_dqw<D, 64, 8>(g, dm, p, sms, s);
-    return launch_attn_dqw<D, 64, 16>(g, dm, p, sms, s);
-  }
-  return launch_attn_dqw<D, 128, 16>(g, dm, p, sms, s);
+  if (dm.kind == 0) return launch_attn_dqm<D, NQ, 0>(g, dm, p, sms, s);
+  if (dm.kind == 1) return launch_attn_dqm<D, NQ, 1>(g, dm, p, sms, s);
+  return launch_attn_dqm<D, NQ, 2>(g, dm, p, sms, s);
 }
 
 bool trows_uniform(const DevGeom& g) {
@@ -431,13 +426,16 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
   if (g.d != 64 && g.d != 128)
     return fail(FVSR_E_CONFIG, "sparse_attention_exec: head_dim %d unsupported (64 or 128)", g.d);
   const bool uniform = trows_uniform(g);
-  if (const char* dbg = std::getenv("FVSR_ATTN_DEBUG")) p.debug = std::atoi(dbg);
+  // experiments (builds with -DFVSR_ATTN_INSTRUMENT=1 only): debug short-cuts, timelines
+  if (kInstrument)
+    if (const char* dbg = std::getenv("FVSR_ATTN_DEBUG")) p.debug = std::atoi(dbg);
   static long long* trace = nullptr;
   static int trace_calls = 0;
-  const bool tracing = std::getenv("FVSR_ATTN_TRACE") != nullptr && ++trace_calls == 20;
+  const bool tracing = kInstrument && std::getenv("FVSR_ATTN_TRACE") != nullptr && ++trace_calls == 20;
   if (tracing) {
-    if (!trace) cudaMalloc(&trace, kTraceEvents * kTraceTiles * sizeof(long long));
-    cudaMemsetAsync(trace, 0, kTraceEvents * kTraceTiles * sizeof(long long), s);
+    const size_t tn = kTraceEvents * kTraceTiles + 1024 * kTraceCtaSlots;
+    if (!trace) cudaMalloc(&trace, tn * sizeof(long long));
+    cudaMemsetAsync(trace, 0, tn * sizeof(long long), s);
     p.trace = trace;
   }
   int sms = 0;
@@ -460,11 +458,12 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
     ctx->launches += 1;
   }
   if (tracing) {  // experiments only: per-tile pipeline timeline of CTA 0
-    std::vector<long long> h(kTraceEvents * kTraceTiles);
+    std::vector<long long> h(kTraceEvents * kTraceTiles + 1024 * kTraceCtaSlots);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
     const char* names[kTraceEvents] = {"K",    "QK",   "S0",  "P0",  "PV",    "V",     "vote",  "rare",
-                                       "exps", "pbuf", "sts", "fence", "QKmma", "QKcmt", "PVmma", "PVcmt"};
+                                       "exps", "pbuf", "sts", "fence", "QKmma", "QKcmt", "PVmma", "PVcmt",
+                                       "wV",   "wP",   "wK",  "wS"};
     const long long base = h[0];
     std::fprintf(stderr, "trace (cycles from first K issue), tiles 0..60\n  G");
     for (int e = 0; e < kTraceEvents; ++e) std::fprintf(stderr, "%9s", names[e]);
@@ -474,6 +473,32 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
       for (int e = 0; e < kTraceEvents; ++e) std::fprintf(stderr, "%9lld", h[e * kTraceTiles + G] ? h[e * kTraceTiles + G] - base : -1);
       std::fprintf(stderr, "\n");
     }
+    // per-CTA unit timeline (globaltimer ns)
+    const long long* ct = h.data() + kTraceEvents * kTraceTiles;
+    long long t0 = LLONG_MAX, tend = 0;
+    for (int b = 0; b < sms; ++b) if (ct[b * kTraceCtaSlots]) t0 = std::min(t0, ct[b * kTraceCtaSlots]);
+    std::vector<double> unit_us, end_us, start_us;
+    for (int b = 0; b < sms; ++b) {
+      const long long* r = ct + b * kTraceCtaSlots;
+      start_us.push_back((r[0] - t0) * 1e-3);
+      long long prev = r[0];
+      for (int k = 1; k < kTraceCtaSlots && r[k]; ++k) { unit_us.push_back((r[k] - prev) * 1e-3); prev = r[k]; }
+      end_us.push_back((prev - t0) * 1e-3);
+      tend = std::max(tend, prev);
+    }
+    std::sort(unit_us.begin(), unit_us.end());
+    std::sort(end_us.begin(), end_us.end());
+    std::sort(start_us.begin(), start_us.end());
+    auto pct = [](const std::vector<double>& v, double q) { return v.empty() ? 0.0 : v[(size_t)(q * (v.size() - 1))]; };
+    std::fprintf(stderr, "cta timeline: makespan %.1f us; start p0/p50/p100 %.1f/%.1f/%.1f; end p0/p50/p100 %.1f/%.1f/%.1f\n",
+                 (tend - t0) * 1e-3, pct(start_us, 0), pct(start_us, .5), pct(start_us, 1), pct(end_us, 0),
+                 pct(end_us, .5), pct(end_us, 1));
+    std::fprintf(stderr, "unit us: n=%zu p0 %.1f p10 %.1f p50 %.1f p90 %.1f p100 %.1f\n", unit_us.size(), pct(unit_us, 0),
+                 pct(unit_us, .1), pct(unit_us, .5), pct(unit_us, .9), pct(unit_us, 1));
+    const long long* r0 = ct;
+    std::fprintf(stderr, "cta0 units:");
+    for (int k = 1; k < kTraceCtaSlots && r0[k]; ++k) std::fprintf(stderr, " %.1f", (r0[k] - r0[k - 1]) * 1e-3);
+    std::fprintf(stderr, "\n");
   }
   return FVSR_OK;
 }

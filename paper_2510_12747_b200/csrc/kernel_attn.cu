@@ -62,9 +62,25 @@ struct AttnParams {
 // (warp 0), 4 PV issued, 5 V issued, 6-11 S ready / P done of softmax warps 3/4/7, 12/13 QK
 // MMAs / commits issued, 14/15 PV MMAs / commits issued.
 constexpr int kTraceTiles = 512;
-constexpr int kTraceEvents = 16;
-__device__ __forceinline__ void trace_at(const AttnParams& p, int ev, long long G) {
-  if (p.trace && blockIdx.x == 0 && G < kTraceTiles) p.trace[ev * kTraceTiles + G] = clock64();
+constexpr int kTraceEvents = 20;
+constexpr int kTraceCtaSlots = 8;  // per CTA: [0] start, [1..7] unit ends (globaltimer ns)
+// Instrumentation (per-tile timeline, debug short-cuts) only exists in builds with
+// -DFVSR_ATTN_INSTRUMENT=1; the production kernel carries none of it.
+#ifndef FVSR_ATTN_INSTRUMENT
+#define FVSR_ATTN_INSTRUMENT 0
+#endif
+constexpr bool kInstrument = FVSR_ATTN_INSTRUMENT != 0;
+__device__ __forceinline__ void trace_at(const AttnParams& p, int ev, int G) {
+  if (kInstrument && p.trace && blockIdx.x == 0 && G < kTraceTiles) p.trace[ev * kTraceTiles + G] = clock64();
+}
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_cta(const AttnParams& p, int slot) {
+  if (kInstrument && p.trace && slot < kTraceCtaSlots)
+    p.trace[kTraceEvents * kTraceTiles + blockIdx.x * kTraceCtaSlots + slot] = globaltimer();
 }
 
 template <int D, int NQ, int SWARPS>
@@ -74,11 +90,11 @@ struct AttnCfg {
   static constexpr int kCPT = NQ / kCG;              // query columns per softmax thread (16 or 32)
   static_assert(kCPT == 16 || kCPT == 32, "columns per thread");
   static constexpr int kProducerWarp = kSW;          // Q and K tiles
-  static constexpr int kMmaWarp = kSW + 1;
+  static constexpr int kQkWarp = kSW + 1;            // QK^T issuer (+ TMEM allocator)
   static constexpr int kVProducerWarp = kSW + 2;     // V tiles (decoupled so K runs ahead)
-  static constexpr int kThreads = kSW * 32 + 96;
+  static constexpr int kPvWarp = kSW + 3;            // PV issuer (own program order: QK never waits on P)
+  static constexpr int kThreads = kSW * 32 + 128;
   static constexpr int kNS = NQ == 64 ? 4 : 2;       // S^T buffers in TMEM
-  static constexpr int kLA = kNS - 1;                // QK look-ahead over PV
   static constexpr int kNK = NQ == 64 ? 3 : 2;       // K stages
   static constexpr int kNV = 2;                      // V stages
   static constexpr int kNP = NQ == 64 ? 2 : 1;       // P^T buffers
@@ -194,11 +210,14 @@ __device__ __forceinline__ uint32_t tile_info(const DevGeom& g, int kb) {
          ((uint32_t)(8 * tw) << 20);
 }
 
-template <int D, int NQ, int SWARPS>
+// MK: token-mask kind (0 all-allowed, 1 locality window, 2 explicit bitmask), fixed at
+// compile time so the per-tile mask logic of the other kinds costs nothing.
+template <int D, int NQ, int SWARPS, int MK>
 __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
-    sparse_attn_kernel(DevGeom g, DevMask m, AttnParams p) {
+    sparse_attn_kernel(const __grid_constant__ DevGeom g, const __grid_constant__ DevMask m,
+                       const __grid_constant__ AttnParams p) {
   using Cfg = AttnCfg<D, NQ, SWARPS>;
-  constexpr int SW = Cfg::kSW, kNS = Cfg::kNS, kLA = Cfg::kLA, CPT = Cfg::kCPT;
+  constexpr int SW = Cfg::kSW, kNS = Cfg::kNS, CPT = Cfg::kCPT;
   constexpr int kNK = Cfg::kNK, kNV = Cfg::kNV, kNP = Cfg::kNP;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for SWIZZLE_128B, by offset so the compiler keeps the shared space
@@ -209,17 +228,19 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
   uint8_t* sP = smem + Cfg::kOffP;
   uint8_t* scratch = smem + Cfg::kOffS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(scratch);
+  // Barrier protocol (two waits and two commits per tile in the MMA warp):
+  //   qk_go[G % NS]   K(G) landed (producer expect_tx + TMA bytes) and S buffer free
+  //                   (softmax arrivals after reading S(G - NS); pre-arrived at start)
+  //   s_full[G % NS]  QK(G) complete (commit); also frees K stage G % NK for the producer
+  //   pv_go[G % 2]    V(G) landed (V producer expect_tx + TMA bytes) and P(G) written
+  //   pv_done[G % 2]  PV(G) complete (commit); frees V stage and P buffer
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;
-  uint64_t* k_empty = k_full + kNK;
-  uint64_t* v_full = k_empty + kNK;
-  uint64_t* v_empty = v_full + kNV;
-  uint64_t* s_full = v_empty + kNV;
-  uint64_t* s_empty = s_full + kNS;
-  uint64_t* p_full = s_empty + kNS;
-  uint64_t* p_empty = p_full + kNP;
-  uint64_t* o_full = p_empty + kNP;
+  uint64_t* qk_go = bars + 2;
+  uint64_t* s_full = qk_go + kNS;
+  uint64_t* pv_go = s_full + kNS;
+  uint64_t* pv_done = pv_go + 2;
+  uint64_t* o_full = pv_done + 2;
   uint64_t* o_empty = o_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
   float* c_s = reinterpret_cast<float*>(scratch + 256);  // [NQ] column references
@@ -249,14 +270,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
   };
 
   // ---- setup ----------------------------------------------------------------------------
-  if (warp == Cfg::kMmaWarp) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  if (threadIdx.x == 0) trace_cta(p, 0);
+  if (warp == Cfg::kQkWarp) tmem_alloc(tmem_slot, Cfg::kTmemCols);
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int i = 0; i < kNK; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
-    for (int i = 0; i < kNV; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
-    for (int i = 0; i < kNS; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, SW); }
-    for (int i = 0; i < kNP; ++i) { mbar_init(p_full + i, SW); mbar_init(p_empty + i, 1); }
+    for (int i = 0; i < kNS; ++i) { mbar_init(qk_go + i, SW + 1); mbar_init(s_full + i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(pv_go + i, SW + 1); mbar_init(pv_done + i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, SW); }
     fence_barrier_init();
   }
@@ -307,7 +327,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
 
   if (warp == Cfg::kProducerWarp) {
     // ================================ Q / K producer (warp-wide) =========================
-    long long T = 0;  // global tile counter
+    int T = 0;  // global tile counter
     int U = 0;        // units with work
     for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
       int head, qtr, qtile, n;
@@ -333,13 +353,14 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
         if ((t & 31) == 0) mine = fetch_meta(sel, n, t, head);
         const TileMeta mt = bcast_meta(mine, t & 31);
         const int ks = (int)(T % kNK);
-        if (T >= kNK) mbar_wait(k_empty + ks, (uint32_t)((T / kNK) - 1) & 1);
+        // K stage ks is free once QK(T - NK) completed
+        if (T >= kNK) mbar_wait(s_full + (T - kNK) % kNS, (uint32_t)((T - kNK) / kNS) & 1);
         if (elect_one()) {
-          if ((p.debug & 2) && T >= kNK) {  // experiment: no K traffic after the first stages
-            mbar_arrive(k_full + ks);
+          if ((kInstrument && (p.debug & 2)) && T >= kNK) {  // experiment: no K traffic after the first stages
+            mbar_arrive(qk_go + T % kNS);
           } else {
             trace_at(p, 0, T);
-            load_kv(p.k, sK + ks * Cfg::kKVBytes, mt, k_full + ks);
+            load_kv(p.k, sK + ks * Cfg::kKVBytes, mt, qk_go + T % kNS);
           }
         }
         __syncwarp();
@@ -348,7 +369,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
     }
   } else if (warp == Cfg::kVProducerWarp) {
     // ================================ V producer (warp-wide) =============================
-    long long T = 0;
+    int T = 0;
     for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
       int head, qtr, qtile, n;
       const int* sel;
@@ -358,78 +379,40 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
         if ((t & 31) == 0) mine = fetch_meta(sel, n, t, head);
         const TileMeta mt = bcast_meta(mine, t & 31);
         const int vs = (int)(T % kNV);
-        if (T >= kNV) mbar_wait(v_empty + vs, (uint32_t)((T / kNV) - 1) & 1);
+        // V stage vs is free once PV(T - NV) completed
+        if (T >= kNV) mbar_wait(pv_done + (T - kNV) % 2, (uint32_t)((T - kNV) / 2) & 1);
         if (elect_one()) {
-          if ((p.debug & 2) && T >= kNV) {
-            mbar_arrive(v_full + vs);
+          if ((kInstrument && (p.debug & 2)) && T >= kNV) {
+            mbar_arrive(pv_go + T % 2);
           } else {
             trace_at(p, 5, T);
-            load_kv(p.v, sV + vs * Cfg::kKVBytes, mt, v_full + vs);
+            load_kv(p.v, sV + vs * Cfg::kKVBytes, mt, pv_go + T % 2);
           }
         }
         __syncwarp();
       }
     }
-  } else if (warp == Cfg::kMmaWarp) {
-    // ================================ MMA issuer (warp-wide, elected lane issues) =========
+  } else if (warp == Cfg::kQkWarp) {
+    // ================================ QK^T issuer (warp-wide, elected lane issues) =========
+    // S^T(G) = K(G) . Q^T into S buffer G % NS once K(G) landed and the buffer is free
+    // (qk_go); runs ahead of the softmax by up to NS tiles, independent of PV progress.
     constexpr uint32_t idesc_qk = umma_idesc_bf16(128, NQ, 0, 0);
-    constexpr uint32_t idesc_pv = umma_idesc_bf16(128, NQ, 1, 1);
     const uint32_t aQ = smem_u32(sQ);
-    long long T = 0;
-    int U = 0;
-    auto issue_pv = [&](long long G, bool full, uint32_t tO, bool first) {
-      const int vs = (int)(G % kNV), pb = (int)(G % kNP);
-      mbar_wait(v_full + vs, (uint32_t)(G / kNV) & 1);
-      mbar_wait(p_full + pb, (uint32_t)(G / kNP) & 1);
-      tc_fence_after();
-      const uint32_t aV = smem_u32(sV + vs * Cfg::kKVBytes);
-      const uint32_t aP = smem_u32(sP + pb * Cfg::kPBytes);
-      if (elect_one()) {
-        trace_at(p, 4, G);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          if (kk < 4 || full) {  // a 64-row key block has 4 valid K=16 steps
-            const uint64_t da = umma_desc_sw128(aV + kk * 2048, D == 128 ? 16384u : 0u, 1024u);
-            const uint64_t db = umma_desc_sw128(aP + kk * 2048, 16384u, 1024u);
-            tc_mma_f16(tO, da, db, idesc_pv, (!first || kk > 0) ? 1u : 0u);
-          }
-        }
-        trace_at(p, 14, G);
-        tc_commit(v_empty + vs);
-        tc_commit(p_empty + pb);
-        trace_at(p, 15, G);
-      }
-      __syncwarp();
-    };
+    const uint32_t aK0 = smem_u32(sK);
+    int G = 0, U = 0, sb = 0, ks = 0;
+    uint32_t sph = 0;
     for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
       int head, qtr, qtile, n;
       const int* sel;
       decode(u, head, qtr, qtile, n, sel);
       if (n == 0) continue;
-      const int ob = U & 1;
-      const uint32_t tO = tO0 + ob * NQ;
       mbar_wait(q_full, U & 1);
-      uint32_t fullmask = 0, prevmask = 0;  // bit i: tile (chunk base + i) is a 128-row block
-      auto is_full = [&](int tp, int t) {
-        const uint32_t msk = (tp >> 5) == (t >> 5) ? fullmask : prevmask;
-        return ((msk >> (tp & 31)) & 1u) != 0u;
-      };
-      for (int t = 0; t < n; ++t) {
-        if ((t & 31) == 0) {
-          prevmask = fullmask;
-          const int tt = t + lane;
-          fullmask = __ballot_sync(0xffffffffu, tt < n && g.k_tr_count[sel_at(sel, tt) / g.n_tiles] == 2);
-        }
-        if (t >= kLA) {
-          if (t == kLA && U >= 2) mbar_wait(o_empty + ob, ((U >> 1) - 1) & 1);  // epilogue of unit U-2 done
-          issue_pv(T + t - kLA, is_full(t - kLA, t), tO, t == kLA);
-        }
-        const long long G = T + t;
-        const int ks = (int)(G % kNK), sb = (int)(G % kNS);
-        mbar_wait(k_full + ks, (uint32_t)(G / kNK) & 1);
-        if (G >= kNS) mbar_wait(s_empty + sb, (uint32_t)((G / kNS) - 1) & 1);
+      for (int t = 0; t < n; ++t, ++G) {
+        if (lane == 0) trace_at(p, 18, G);
+        mbar_wait(qk_go + sb, sph);
+        if (lane == 0) trace_at(p, 19, G);
         tc_fence_after();
-        const uint32_t aK = smem_u32(sK + ks * Cfg::kKVBytes);
+        const uint32_t aK = aK0 + ks * Cfg::kKVBytes;
         if (elect_one()) {
           trace_at(p, 1, G);
 #pragma unroll
@@ -439,20 +422,64 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
             tc_mma_f16(tS0 + sb * NQ, da, db, idesc_qk, kk > 0 ? 1u : 0u);
           }
           trace_at(p, 12, G);
-          tc_commit(k_empty + ks);
           tc_commit(s_full + sb);
           if (t == n - 1) tc_commit(q_empty);
           trace_at(p, 13, G);
         }
         __syncwarp();
+        if (++sb == kNS) { sb = 0; sph ^= 1u; }
+        if (++ks == kNK) ks = 0;
       }
-      for (int tp = n > kLA ? n - kLA : 0; tp < n; ++tp) {
-        if (tp == 0 && U >= 2) mbar_wait(o_empty + ob, ((U >> 1) - 1) & 1);
-        issue_pv(T + tp, is_full(tp, n - 1), tO, tp == 0);
+      ++U;
+    }
+  } else if (warp == Cfg::kPvWarp) {
+    // ================================ PV issuer (warp-wide, elected lane issues) ==========
+    // O^T += V(G)^T . P(G)^T once V(G) landed and the softmax wrote P(G) (pv_go).
+    constexpr uint32_t idesc_pv = umma_idesc_bf16(128, NQ, 1, 1);
+    const uint32_t aV0 = smem_u32(sV), aP0 = smem_u32(sP);
+    int G = 0, U = 0, vs = 0, pb = 0, gb = 0;
+    uint32_t gph = 0;
+    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int head, qtr, qtile, n;
+      const int* sel;
+      decode(u, head, qtr, qtile, n, sel);
+      if (n == 0) continue;
+      const int ob = U & 1;
+      const uint32_t tO = tO0 + ob * NQ;
+      if (U >= 2) mbar_wait(o_empty + ob, ((U >> 1) - 1) & 1);  // epilogue of unit U-2 done
+      uint32_t fullmask = 0;  // bit i: tile (chunk base + i) is a 128-row block
+      for (int t = 0; t < n; ++t, ++G) {
+        if ((t & 31) == 0) {
+          const int tt = t + lane;
+          fullmask = __ballot_sync(0xffffffffu, tt < n && g.k_tr_count[sel_at(sel, tt) / g.n_tiles] == 2);
+        }
+        const bool full = ((fullmask >> (t & 31)) & 1u) != 0u;
+        if (lane == 0) trace_at(p, 16, G);
+        mbar_wait(pv_go + gb, gph);
+        if (lane == 0) trace_at(p, 17, G);
+        tc_fence_after();
+        const uint32_t aV = aV0 + vs * Cfg::kKVBytes;
+        const uint32_t aP = aP0 + pb * Cfg::kPBytes;
+        if (elect_one()) {
+          trace_at(p, 4, G);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            if (kk < 4 || full) {  // a 64-row key block has 4 valid K=16 steps
+              const uint64_t da = umma_desc_sw128(aV + kk * 2048, D == 128 ? 16384u : 0u, 1024u);
+              const uint64_t db = umma_desc_sw128(aP + kk * 2048, 16384u, 1024u);
+              tc_mma_f16(tO, da, db, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          trace_at(p, 14, G);
+          tc_commit(pv_done + gb);
+          if (t == n - 1) tc_commit(o_full + ob);
+          trace_at(p, 15, G);
+        }
+        __syncwarp();
+        if (++gb == 2) { gb = 0; gph ^= 1u; }
+        if (++vs == kNV) vs = 0;
+        if (++pb == kNP) pb = 0;
       }
-      if (elect_one()) tc_commit(o_full + ob);
-      __syncwarp();
-      T += n;
       ++U;
     }
   } else {
@@ -463,6 +490,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
     const int col0 = cg * CPT;          // first of this thread's CPT query columns
     const int bar_id = 1 + cg;          // named barrier of the column group (128 threads)
     constexpr int kAllBar = 7;          // named barrier of all softmax warps
+    if (lane == 0)
+      for (int i = 0; i < kNS; ++i) mbar_arrive(qk_go + i);  // every S buffer starts free
     long long T = 0;
     int U = 0;
     for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -500,8 +529,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
       const uint32_t tO = tO0 + ob * NQ;
 
       for (int t = 0; t < n; ++t) {
-        const long long G = T + t;
-        const int sb = (int)(G % kNS), pb = (int)(G % kNP);
+        const int G = T + t;
+        const int sb = G % kNS, pb = G % kNP;
         // ---- key row j: validity and allowed-query mask over this thread's columns ----
         const uint32_t inf = t < kInfoCap ? info[t] : tile_info(g, sel_at(sel, t));
         const int kcnt = inf & 3, kf0 = (inf >> 2) & 63;
@@ -510,9 +539,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
         const bool kvalid = (j < 64 || kcnt == 2) && kh < g.rows && kw < g.cols;
         uint32_t mk = 0;
         if (kvalid) {
-          if (m.kind == 0) {
+          if (MK == 0) {
             mk = qvalid;
-          } else if (m.kind == 1) {
+          } else if (MK == 1) {
             uint32_t wb = 0, hb = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -547,11 +576,11 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
         tc_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(s_empty + sb);
+        if (lane == 0) mbar_arrive(qk_go + sb);  // S buffer free for QK(G + NS)
         if (threadIdx.x == 0) trace_at(p, 2, G);
 
         uint32_t pk[CPT / 2];
-        if (p.debug & 1) {  // experiment: no softmax math
+        if (kInstrument && (p.debug & 1)) {  // experiment: no softmax math
 #pragma unroll
           for (int i = 0; i < CPT / 2; ++i) pk[i] = 0x3f803f80u;  // bf16 pair (1, 1)
 #pragma unroll
@@ -596,7 +625,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
             }
             if (t > 0) {
               // O^T holds PV of this unit's tiles 0..t-1: wait for PV(G-1), rescale columns
-              mbar_wait(p_empty + ((G - 1) % kNP), (uint32_t)((G - 1) / kNP) & 1);
+              mbar_wait(pv_done + (G - 1) % 2, (uint32_t)((G - 1) / 2) & 1);
               tc_fence_after();
               if (j < D) {
                 uint32_t o[CPT];
@@ -621,7 +650,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
           }
         }
         if (threadIdx.x == 0) trace_at(p, 8, G);
-        if (G >= kNP) mbar_wait(p_empty + pb, (uint32_t)((G / kNP) - 1) & 1);
+        if (G >= kNP) mbar_wait(pv_done + (G - kNP) % 2, (uint32_t)((G - kNP) / 2) & 1);
         if (threadIdx.x == 0) trace_at(p, 9, G);
         // MN-major B operand: [NQ/64 groups][128 key rows][128 B], 16-B chunks swizzled by row
         uint8_t* prow = sP + pb * Cfg::kPBytes + (col0 >> 6) * 16384 + j * 128;
@@ -635,7 +664,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
         if (threadIdx.x == 0) trace_at(p, 11, G);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full + pb);
+        if (lane == 0) mbar_arrive(pv_go + G % 2);
         if (threadIdx.x == 0) trace_at(p, 3, G);
       }
 
@@ -709,6 +738,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
         }
       }
       named_bar_sync(kAllBar, SW * 32);  // staging buffer and per-unit tables reusable
+      if (threadIdx.x == 0) trace_cta(p, 1 + U);
       if (n > 0) {
         T += n;
         ++U;
@@ -719,14 +749,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == Cfg::kMmaWarp) tmem_dealloc(tmem, Cfg::kTmemCols);
+  if (warp == Cfg::kQkWarp) tmem_dealloc(tmem, Cfg::kTmemCols);
 }
 
-template __global__ void sparse_attn_kernel<64, 64, 8>(DevGeom, DevMask, AttnParams);
-template __global__ void sparse_attn_kernel<128, 64, 8>(DevGeom, DevMask, AttnParams);
-template __global__ void sparse_attn_kernel<64, 64, 16>(DevGeom, DevMask, AttnParams);
-template __global__ void sparse_attn_kernel<128, 64, 16>(DevGeom, DevMask, AttnParams);
-template __global__ void sparse_attn_kernel<64, 128, 16>(DevGeom, DevMask, AttnParams);
-template __global__ void sparse_attn_kernel<128, 128, 16>(DevGeom, DevMask, AttnParams);
 
 }  // namespace fvsr
