@@ -391,17 +391,17 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
 
 template <int D, int NQ, int MK>
 int launch_attn_dqm(const DevGeom& g, const DevMask& dm, const AttnParams& p, int sms, cudaStream_t s) {
-  using Cfg = AttnCfg<D, NQ, 16>;
+  using Cfg = AttnCfg<D, NQ>;
   static bool configured = false;
   if (!configured) {
-    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D, NQ, 16, MK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D, NQ, MK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)Cfg::kBytes));
     configured = true;
   }
   const long long units = p.unit_end - p.unit_begin;
   if (units <= 0) return FVSR_OK;
   const unsigned grid = (unsigned)std::min<long long>(units, sms);  // persistent CTAs
-  sparse_attn_kernel<D, NQ, 16, MK><<<grid, Cfg::kThreads, Cfg::kBytes, s>>>(g, dm, p);
+  sparse_attn_kernel<D, NQ, MK><<<grid, Cfg::kThreads, Cfg::kBytes, s>>>(g, dm, p);
   return FVSR_OK;
 }
 
@@ -463,7 +463,8 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
     cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
     const char* names[kTraceEvents] = {"K",    "QK",   "S0",  "P0",  "PV",    "V",     "vote",  "rare",
                                        "exps", "pbuf", "sts", "fence", "QKmma", "QKcmt", "PVmma", "PVcmt",
-                                       "wV",   "wP",   "wK",  "wS"};
+                                       "wV",   "wP",   "wK",  "wS",    "ld0",   "vt0",   "ex0",   "st0",
+                                       "ld1",  "vt1",  "ex1", "st1"};
     const long long base = h[0];
     std::fprintf(stderr, "trace (cycles from first K issue), tiles 0..60\n  G");
     for (int e = 0; e < kTraceEvents; ++e) std::fprintf(stderr, "%9s", names[e]);
@@ -482,7 +483,7 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
       const long long* r = ct + b * kTraceCtaSlots;
       start_us.push_back((r[0] - t0) * 1e-3);
       long long prev = r[0];
-      for (int k = 1; k < kTraceCtaSlots && r[k]; ++k) { unit_us.push_back((r[k] - prev) * 1e-3); prev = r[k]; }
+      for (int k = 1; k < kTraceCtaSlots / 2 && r[k]; ++k) { unit_us.push_back((r[k] - prev) * 1e-3); prev = r[k]; }
       end_us.push_back((prev - t0) * 1e-3);
       tend = std::max(tend, prev);
     }
@@ -496,8 +497,10 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
     std::fprintf(stderr, "unit us: n=%zu p0 %.1f p10 %.1f p50 %.1f p90 %.1f p100 %.1f\n", unit_us.size(), pct(unit_us, 0),
                  pct(unit_us, .1), pct(unit_us, .5), pct(unit_us, .9), pct(unit_us, 1));
     const long long* r0 = ct;
-    std::fprintf(stderr, "cta0 units:");
-    for (int k = 1; k < kTraceCtaSlots && r0[k]; ++k) std::fprintf(stderr, " %.1f", (r0[k] - r0[k - 1]) * 1e-3);
+    std::fprintf(stderr, "cta0 units (us / kcycles / MHz):");
+    for (int k = 1; k < kTraceCtaSlots / 2 && r0[k]; ++k)
+      std::fprintf(stderr, " %.1f/%.1f/%.0f", (r0[k] - r0[k - 1]) * 1e-3, (r0[8 + k] - r0[8 + k - 1]) * 1e-3,
+                   (double)(r0[8 + k] - r0[8 + k - 1]) / (double)(r0[k] - r0[k - 1]) * 1e3);
     std::fprintf(stderr, "\n");
   }
   return FVSR_OK;

@@ -62,8 +62,8 @@ struct AttnParams {
 // (warp 0), 4 PV issued, 5 V issued, 6-11 S ready / P done of softmax warps 3/4/7, 12/13 QK
 // MMAs / commits issued, 14/15 PV MMAs / commits issued.
 constexpr int kTraceTiles = 512;
-constexpr int kTraceEvents = 20;
-constexpr int kTraceCtaSlots = 8;  // per CTA: [0] start, [1..7] unit ends (globaltimer ns)
+constexpr int kTraceEvents = 28;
+constexpr int kTraceCtaSlots = 16;  // per CTA: [0] start, [1..7] unit ends (globaltimer ns); +8: clock64
 // Instrumentation (per-tile timeline, debug short-cuts) only exists in builds with
 // -DFVSR_ATTN_INSTRUMENT=1; the production kernel carries none of it.
 #ifndef FVSR_ATTN_INSTRUMENT
@@ -79,16 +79,20 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 __device__ __forceinline__ void trace_cta(const AttnParams& p, int slot) {
-  if (kInstrument && p.trace && slot < kTraceCtaSlots)
+  if (kInstrument && p.trace && slot < kTraceCtaSlots / 2) {
     p.trace[kTraceEvents * kTraceTiles + blockIdx.x * kTraceCtaSlots + slot] = globaltimer();
+    p.trace[kTraceEvents * kTraceTiles + blockIdx.x * kTraceCtaSlots + 8 + slot] = clock64();
+  }
 }
 
-template <int D, int NQ, int SWARPS>
+template <int D, int NQ>
 struct AttnCfg {
-  static constexpr int kSW = SWARPS;                 // softmax warps: 4 lane quarters x column groups
-  static constexpr int kCG = SWARPS / 4;             // column groups
-  static constexpr int kCPT = NQ / kCG;              // query columns per softmax thread (16 or 32)
-  static_assert(kCPT == 16 || kCPT == 32, "columns per thread");
+  static constexpr int kSW = 8;                      // softmax warps (12 warps total: 168 registers)
+  static constexpr int kGroups = NQ == 64 ? 2 : 1;   // ping-pong softmax groups (tile parity)
+  static constexpr int kWG = kSW / kGroups;          // warps per group
+  static constexpr int kCGg = kWG / 4;               // column groups per group (4 lane quarters each)
+  static constexpr int kCPT = NQ / kCGg;             // query columns per softmax thread
+  static_assert(kCPT == 64, "columns per thread");
   static constexpr int kProducerWarp = kSW;          // Q and K tiles
   static constexpr int kQkWarp = kSW + 1;            // QK^T issuer (+ TMEM allocator)
   static constexpr int kVProducerWarp = kSW + 2;     // V tiles (decoupled so K runs ahead)
@@ -97,7 +101,8 @@ struct AttnCfg {
   static constexpr int kNS = NQ == 64 ? 4 : 2;       // S^T buffers in TMEM
   static constexpr int kNK = NQ == 64 ? 3 : 2;       // K stages
   static constexpr int kNV = 2;                      // V stages
-  static constexpr int kNP = NQ == 64 ? 2 : 1;       // P^T buffers
+  static constexpr int kNP = NQ == 64 ? 2 : 1;       // P^T buffers (one per group for NQ=64)
+  static constexpr int kOB = 2;                      // O^T buffers per group (double-buffered units)
   static constexpr uint32_t kTileBytes = D * 128;    // one packed 64-row frame-tile
   static constexpr uint32_t kQSub = NQ * 128;        // Q sub-tile stride (NQ rows x 128 B)
   static constexpr uint32_t kQBytes = (D / 64) * kQSub;
@@ -108,11 +113,12 @@ struct AttnCfg {
   static constexpr uint32_t kOffV = kOffK + kNK * kKVBytes;
   static constexpr uint32_t kOffP = kOffV + kNV * kKVBytes;
   static constexpr uint32_t kOffS = kOffP + kNP * kPBytes;  // scratch
-  static constexpr uint32_t kScratch = 5120;
+  static constexpr uint32_t kScratch = 10240;
   static constexpr uint32_t kBytes = kOffS + kScratch + 1024;  // + alignment slack
-  static constexpr uint32_t kTmemCols = 512;         // S x NS + O x 2
-  static_assert(kNS * NQ + 2 * NQ <= 512, "TMEM budget");
+  static constexpr uint32_t kTmemCols = 512;         // S x NS + O x groups x OB
+  static_assert(kNS * NQ + kGroups * kOB * NQ <= 512, "TMEM budget");
   static_assert(kBytes <= 232448, "shared memory budget");
+  static_assert(kNP * NQ * 256 >= NQ * D * 2, "O staging fits the P buffers");
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -133,12 +139,13 @@ __device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t n, bool v) {
   return r != 0;
 }
 
-// Butterfly reduce-scatter of N (16 or 32) per-thread column values across a warp: step s
-// keeps the half selected by lane bit (4-s); with N=16 a final xor-1 combine merges lane
-// pairs.  On return v[0] is the warp-wide reduction of column (N == 32 ? lane : lane >> 1).
+// Butterfly reduce-scatter of N (16, 32 or 64) per-thread column values across a warp:
+// step s keeps the half selected by lane bit (4-s); with N=16 a final xor-1 combine merges
+// lane pairs.  On return v[i], i < max(1, N/32), is the warp-wide reduction of column
+// col(i) = N == 64 ? 2*lane + i : (N == 32 ? lane : lane >> 1).
 template <int N, bool kMax>
-__device__ __forceinline__ void warp_colreduce(float (&v)[N], int lane) {
-  constexpr int kSteps = N == 32 ? 5 : 4;
+__device__ __forceinline__ void warp_colreduce(float* v, int lane) {
+  constexpr int kSteps = N >= 32 ? 5 : 4;
 #pragma unroll
   for (int step = 0; step < kSteps; ++step) {
     const int half = (N / 2) >> step;
@@ -157,6 +164,9 @@ __device__ __forceinline__ void warp_colreduce(float (&v)[N], int lane) {
     v[0] = kMax ? fmaxf(v[0], recv) : v[0] + recv;
   }
 }
+__device__ __forceinline__ int colreduce_col(int n, int lane, int i) {
+  return n == 64 ? 2 * lane + i : (n == 32 ? lane : lane >> 1);
+}
 
 template <int N>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t* r);
@@ -171,6 +181,11 @@ __device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, uint32_t* r) {
 template <>
 __device__ __forceinline__ void tmem_ld<32>(uint32_t taddr, uint32_t* r) {
   tmem_ld32(taddr, r);
+}
+template <>
+__device__ __forceinline__ void tmem_ld<64>(uint32_t taddr, uint32_t* r) {
+  tmem_ld32(taddr, r);
+  tmem_ld32(taddr + 32, r + 32);
 }
 template <int N>
 __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t* r);
@@ -187,10 +202,15 @@ template <>
 __device__ __forceinline__ void tmem_st<32>(uint32_t taddr, const uint32_t* r) {
   tmem_st32(taddr, r);
 }
+template <>
+__device__ __forceinline__ void tmem_st<64>(uint32_t taddr, const uint32_t* r) {
+  tmem_st32(taddr, r);
+  tmem_st32(taddr + 32, r + 32);
+}
 
 // max of N values as a balanced tree (ILP instead of a serial chain)
 template <int N>
-__device__ __forceinline__ float tree_max(const float (&v)[N]) {
+__device__ __forceinline__ float tree_max(const float* v) {
   float t[N / 2];
 #pragma unroll
   for (int i = 0; i < N / 2; ++i) t[i] = fmaxf(v[2 * i], v[2 * i + 1]);
@@ -212,13 +232,13 @@ __device__ __forceinline__ uint32_t tile_info(const DevGeom& g, int kb) {
 
 // MK: token-mask kind (0 all-allowed, 1 locality window, 2 explicit bitmask), fixed at
 // compile time so the per-tile mask logic of the other kinds costs nothing.
-template <int D, int NQ, int SWARPS, int MK>
-__global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
+template <int D, int NQ, int MK>
+__global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     sparse_attn_kernel(const __grid_constant__ DevGeom g, const __grid_constant__ DevMask m,
                        const __grid_constant__ AttnParams p) {
-  using Cfg = AttnCfg<D, NQ, SWARPS>;
-  constexpr int SW = Cfg::kSW, kNS = Cfg::kNS, CPT = Cfg::kCPT;
-  constexpr int kNK = Cfg::kNK, kNV = Cfg::kNV, kNP = Cfg::kNP;
+  using Cfg = AttnCfg<D, NQ>;
+  constexpr int SW = Cfg::kSW, kNS = Cfg::kNS, CPT = Cfg::kCPT, kGroups = Cfg::kGroups, WG = Cfg::kWG;
+  constexpr int kNK = Cfg::kNK, kNV = Cfg::kNV, kNP = Cfg::kNP, kOB = Cfg::kOB;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for SWIZZLE_128B, by offset so the compiler keeps the shared space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -228,12 +248,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
   uint8_t* sP = smem + Cfg::kOffP;
   uint8_t* scratch = smem + Cfg::kOffS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(scratch);
-  // Barrier protocol (two waits and two commits per tile in the MMA warp):
+  // Barrier protocol (one wait and one commit per tile in each MMA issuer):
   //   qk_go[G % NS]   K(G) landed (producer expect_tx + TMA bytes) and S buffer free
-  //                   (softmax arrivals after reading S(G - NS); pre-arrived at start)
+  //                   (arrivals of the tile's softmax group after reading S(G - NS))
   //   s_full[G % NS]  QK(G) complete (commit); also frees K stage G % NK for the producer
   //   pv_go[G % 2]    V(G) landed (V producer expect_tx + TMA bytes) and P(G) written
   //   pv_done[G % 2]  PV(G) complete (commit); frees V stage and P buffer
+  //   o_full / o_empty  per unit: all PVs done / epilogue read O
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* qk_go = bars + 2;
@@ -243,11 +264,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
   uint64_t* o_full = pv_done + 2;
   uint64_t* o_empty = o_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
-  float* c_s = reinterpret_cast<float*>(scratch + 256);  // [NQ] column references
-  float* alpha_s = c_s + 128;                            // [NQ] rescale factors / denominators
-  float* red = alpha_s + 128;                            // [CG][4 quarter][CPT]
-  int* win = reinterpret_cast<int*>(red + 512);          // [4][8]: hlo, hhi, wlo, whi per q row/col
-  uint32_t* info = reinterpret_cast<uint32_t*>(win + 32);// [kInfoCap]
+  float* c_s = reinterpret_cast<float*>(scratch + 256);  // [2][128] column references per group
+  float* alpha_s = c_s + 256;                            // [2][128] rescale factors
+  float* l_s = alpha_s + 256;                            // [2][128] denominators
+  float* f_s = l_s + 256;                                // [2][128] merge factors (incl. 1/l)
+  float* red = f_s + 256;                                // [2][CGg][4][CPT] cross-quarter partials
+  int* win = reinterpret_cast<int*>(red + 2 * Cfg::kCGg * 4 * CPT);  // [4][8] locality windows
+  uint32_t* info = reinterpret_cast<uint32_t*>(win + 32);           // [kInfoCap]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long n_units = p.unit_end - p.unit_begin;
@@ -275,8 +298,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int i = 0; i < kNS; ++i) { mbar_init(qk_go + i, SW + 1); mbar_init(s_full + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(pv_go + i, SW + 1); mbar_init(pv_done + i, 1); }
+    for (int i = 0; i < kNS; ++i) { mbar_init(qk_go + i, WG + 1); mbar_init(s_full + i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(pv_go + i, WG + 1); mbar_init(pv_done + i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, SW); }
     fence_barrier_init();
   }
@@ -284,7 +307,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS0 = tmem, tO0 = tmem + kNS * NQ;  // S buffers at [0, NS*NQ), O buffers after
+  // TMEM columns: S buffers [0, NS*NQ), then O^T buffers [group][unit parity]
+  const uint32_t tS0 = tmem, tO0 = tmem + kNS * NQ;
 
   // Per-lane metadata of tile (base + lane) of a unit's selection, fetched warp-wide once per
   // 32 tiles and broadcast per tile with shuffles (no per-tile global round trip).
@@ -327,8 +351,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
 
   if (warp == Cfg::kProducerWarp) {
     // ================================ Q / K producer (warp-wide) =========================
-    int T = 0;  // global tile counter
-    int U = 0;        // units with work
+    int T = 0;  // tiles of this CTA so far
+    int U = 0;  // units with work
     for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
       int head, qtr, qtile, n;
       const int* sel;
@@ -352,7 +376,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
       for (int t = 0; t < n; ++t, ++T) {
         if ((t & 31) == 0) mine = fetch_meta(sel, n, t, head);
         const TileMeta mt = bcast_meta(mine, t & 31);
-        const int ks = (int)(T % kNK);
+        const int ks = T % kNK;
         // K stage ks is free once QK(T - NK) completed
         if (T >= kNK) mbar_wait(s_full + (T - kNK) % kNS, (uint32_t)((T - kNK) / kNS) & 1);
         if (elect_one()) {
@@ -378,7 +402,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
       for (int t = 0; t < n; ++t, ++T) {
         if ((t & 31) == 0) mine = fetch_meta(sel, n, t, head);
         const TileMeta mt = bcast_meta(mine, t & 31);
-        const int vs = (int)(T % kNV);
+        const int vs = T % kNV;
         // V stage vs is free once PV(T - NV) completed
         if (T >= kNV) mbar_wait(pv_done + (T - kNV) % 2, (uint32_t)((T - kNV) / 2) & 1);
         if (elect_one()) {
@@ -434,7 +458,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
     }
   } else if (warp == Cfg::kPvWarp) {
     // ================================ PV issuer (warp-wide, elected lane issues) ==========
-    // O^T += V(G)^T . P(G)^T once V(G) landed and the softmax wrote P(G) (pv_go).
+    // O^T[group(G)] += V(G)^T . P(G)^T once V(G) landed and the softmax wrote P(G) (pv_go).
     constexpr uint32_t idesc_pv = umma_idesc_bf16(128, NQ, 1, 1);
     const uint32_t aV0 = smem_u32(sV), aP0 = smem_u32(sP);
     int G = 0, U = 0, vs = 0, pb = 0, gb = 0;
@@ -445,7 +469,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
       decode(u, head, qtr, qtile, n, sel);
       if (n == 0) continue;
       const int ob = U & 1;
-      const uint32_t tO = tO0 + ob * NQ;
       if (U >= 2) mbar_wait(o_empty + ob, ((U >> 1) - 1) & 1);  // epilogue of unit U-2 done
       uint32_t fullmask = 0;  // bit i: tile (chunk base + i) is a 128-row block
       for (int t = 0; t < n; ++t, ++G) {
@@ -454,6 +477,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
           fullmask = __ballot_sync(0xffffffffu, tt < n && g.k_tr_count[sel_at(sel, tt) / g.n_tiles] == 2);
         }
         const bool full = ((fullmask >> (t & 31)) & 1u) != 0u;
+        const uint32_t tO = tO0 + ((G % kGroups) * kOB + ob) * NQ;
         if (lane == 0) trace_at(p, 16, G);
         mbar_wait(pv_go + gb, gph);
         if (lane == 0) trace_at(p, 17, G);
@@ -467,7 +491,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
             if (kk < 4 || full) {  // a 64-row key block has 4 valid K=16 steps
               const uint64_t da = umma_desc_sw128(aV + kk * 2048, D == 128 ? 16384u : 0u, 1024u);
               const uint64_t db = umma_desc_sw128(aP + kk * 2048, 16384u, 1024u);
-              tc_mma_f16(tO, da, db, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+              // the first tile of each group in the unit overwrites its O^T buffer
+              tc_mma_f16(tO, da, db, idesc_pv, (t >= kGroups || kk > 0) ? 1u : 0u);
             }
           }
           trace_at(p, 14, G);
@@ -484,15 +509,22 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
     }
   } else {
     // ===================================== softmax warps ================================
-    const int quarter = warp & 3, cg = warp >> 2;
+    // Group grp handles the tiles G with G % kGroups == grp (ping-pong: the two groups'
+    // latencies overlap) with its own running references and O^T accumulator.
+    const int grp = warp / WG, wl = warp % WG;
+    const int quarter = warp & 3, cg = wl >> 2;
     const int j = quarter * 32 + lane;  // key row == TMEM lane
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int col0 = cg * CPT;          // first of this thread's CPT query columns
-    const int bar_id = 1 + cg;          // named barrier of the column group (128 threads)
-    constexpr int kAllBar = 7;          // named barrier of all softmax warps
+    const int bar_id = 1 + grp * 4 + cg;  // named barrier of the column group (128 threads)
+    const int grp_bar = 9 + grp;          // named barrier of the group
+    constexpr int kAllBar = 11;           // named barrier of all softmax warps
+    float* cg_c = c_s + grp * 128;
+    float* cg_a = alpha_s + grp * 128;
+    float* cg_red = red + (grp * Cfg::kCGg + cg) * 4 * CPT;
     if (lane == 0)
-      for (int i = 0; i < kNS; ++i) mbar_arrive(qk_go + i);  // every S buffer starts free
-    long long T = 0;
+      for (int i = grp; i < kNS; i += kGroups) mbar_arrive(qk_go + i);  // S buffers start free
+    int T = 0;
     int U = 0;
     for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
       int head, qtr, qtile, n;
@@ -502,7 +534,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
       const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
       // per-unit tables: tile infos, locality windows of the 8 query rows / cols
       for (int i = threadIdx.x; i < min(n, kInfoCap); i += SW * 32) info[i] = tile_info(g, sel_at(sel, i));
-      if (threadIdx.x < 8) {
+      if (MK == 1 && threadIdx.x < 8) {
         int lo, hi;
         locality_range(m.mode, qh0 + threadIdx.x, m.extent_h, g.rows, lo, hi);
         win[threadIdx.x] = lo;
@@ -511,24 +543,30 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
         win[16 + threadIdx.x] = lo;
         win[24 + threadIdx.x] = hi;
       }
-      if (quarter == 0 && lane < CPT) c_s[col0 + lane] = -INFINITY;
+      if (threadIdx.x < 256) c_s[threadIdx.x] = -INFINITY;
       named_bar_sync(kAllBar, SW * 32);
-      // query columns of this thread that are real tokens
-      uint32_t qvalid = 0;
+      // query columns of this thread that are real tokens, as 32-column words
+      constexpr int kW = CPT / 32;
+      uint32_t qvalid[kW];
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const int qc = (col0 + i) & 63;
-        if (qh0 + (qc >> 3) < g.rows && qw0 + (qc & 7) < g.cols) qvalid |= 1u << i;
+      for (int w = 0; w < kW; ++w) {
+        qvalid[w] = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int qc = (col0 + 32 * w + i) & 63;
+          if (qh0 + (qc >> 3) < g.rows && qw0 + (qc & 7) < g.cols) qvalid[w] |= 1u << i;
+        }
       }
-      const uint32_t qfull = CPT == 32 ? 0xffffffffu : ((1u << CPT) - 1u);
       uint32_t my_pairs = 0;  // <= tiles * CPT per thread per unit
-      float c[CPT], lp[CPT];
+      float lp[CPT];
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) { c[i] = -INFINITY; lp[i] = 0.0f; }
+      for (int i = 0; i < CPT; ++i) lp[i] = 0.0f;
       const int ob = U & 1;
-      const uint32_t tO = tO0 + ob * NQ;
+      const uint32_t tO = tO0 + (grp * kOB + ob) * NQ;
+      const int t_first = (grp - (T % kGroups) + kGroups) % kGroups;
+      bool any = false;  // this group processed a tile of the unit (its O^T is defined)
 
-      for (int t = 0; t < n; ++t) {
+      for (int t = t_first; t < n; t += kGroups) {
         const int G = T + t;
         const int sb = G % kNS, pb = G % kNP;
         // ---- key row j: validity and allowed-query mask over this thread's columns ----
@@ -537,158 +575,221 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
         const int kh = (int)((inf >> 8) & 0xfff) + ((j & 63) >> 3);
         const int kw = (int)(inf >> 20) + (j & 7);
         const bool kvalid = (j < 64 || kcnt == 2) && kh < g.rows && kw < g.cols;
-        uint32_t mk = 0;
+        uint32_t mk[kW];  // bit i of word w: (key j, column col0 + 32w + i) allowed
+#pragma unroll
+        for (int w = 0; w < kW; ++w) mk[w] = 0;
         if (kvalid) {
           if (MK == 0) {
-            mk = qvalid;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) mk[w] = qvalid[w];
           } else if (MK == 1) {
-            uint32_t wb = 0, hb = 0;
+            uint32_t wb = 0, hb = 0;  // allowed query cols / rows of the 8x8 query tile
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               wb |= (kw >= win[16 + i] && kw < win[24 + i]) ? (1u << i) : 0u;
               hb |= (kh >= win[i] && kh < win[8 + i]) ? (1u << i) : 0u;
             }
 #pragma unroll
-            for (int i = 0; i < CPT; ++i) {
-              const int qc = (col0 + i) & 63;
-              if (((hb >> (qc >> 3)) & (wb >> (qc & 7)) & 1u) != 0u) mk |= 1u << i;
+            for (int w = 0; w < kW; ++w) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int qc = (col0 + 32 * w + i) & 63;
+                if (((hb >> (qc >> 3)) & (wb >> (qc & 7)) & 1u) != 0u) mk[w] |= 1u << i;
+              }
+              mk[w] &= qvalid[w];
             }
-            mk &= qvalid;
           } else {
             const long long tk = g.k_frame_tok0[kf0 + (j >> 6)] + (long long)kh * g.cols + kw;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) {
 #pragma unroll 4
-            for (int i = 0; i < CPT; ++i) {
-              if (!((qvalid >> i) & 1u)) continue;
-              const int col = col0 + i, qc = col & 63;
-              const long long tq =
-                  g.q_frame_tok0[qf0 + (col >> 6)] + (long long)(qh0 + (qc >> 3)) * g.cols + qw0 + (qc & 7);
-              if ((m.bits[tq * m.words_per_row + (tk >> 6)] >> (tk & 63)) & 1ull) mk |= 1u << i;
-            }
-          }
-        }
-        my_pairs += __popc(mk);
-
-        // ---- S^T row j, this thread's columns -> registers ------------------------------
-        mbar_wait(s_full + sb, (uint32_t)(G / kNS) & 1);
-        tc_fence_after();
-        uint32_t sr[CPT];
-        tmem_ld<CPT>(tS0 + sb * NQ + col0 + lane_off, sr);
-        tc_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(qk_go + sb);  // S buffer free for QK(G + NS)
-        if (threadIdx.x == 0) trace_at(p, 2, G);
-
-        uint32_t pk[CPT / 2];
-        if (kInstrument && (p.debug & 1)) {  // experiment: no softmax math
-#pragma unroll
-          for (int i = 0; i < CPT / 2; ++i) pk[i] = 0x3f803f80u;  // bf16 pair (1, 1)
-#pragma unroll
-          for (int i = 0; i < CPT; ++i) lp[i] += 1.0f;
-        } else {
-          // d = s*scale*log2(e) - c  (one FFMA); masked entries -> -inf (ex2 -> 0)
-          float d[CPT];
-          if (mk == qfull) {
-#pragma unroll
-            for (int i = 0; i < CPT; ++i) d[i] = fmaf(__uint_as_float(sr[i]), p.scale_log2, -c[i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < CPT; ++i)
-              d[i] = ((mk >> i) & 1u) ? fmaf(__uint_as_float(sr[i]), p.scale_log2, -c[i]) : -INFINITY;
-          }
-          const bool need = bar_red_or(bar_id, 128, tree_max<CPT>(d) > kRescaleThreshold);
-          if (threadIdx.x == 0) trace_at(p, 6, G);
-          if (need) {
-            // exact column max of this tile over the group's 128 key rows
-            float v[CPT];
-#pragma unroll
-            for (int i = 0; i < CPT; ++i) v[i] = ((mk >> i) & 1u) ? __uint_as_float(sr[i]) * p.scale_log2 : -INFINITY;
-            warp_colreduce<CPT, true>(v, lane);
-            const int rc = CPT == 32 ? lane : (lane >> 1);
-            if (CPT == 32 || (lane & 1) == 0) red[(cg * 4 + quarter) * CPT + rc] = v[0];
-            named_bar_sync(bar_id, 128);
-            if (quarter == 0 && lane < CPT) {
-              const float* r = red + cg * 4 * CPT + lane;
-              const float mx = fmaxf(fmaxf(r[0], r[CPT]), fmaxf(r[2 * CPT], r[3 * CPT]));
-              const float cold = c_s[col0 + lane];
-              const float nw = fmaxf(cold, mx);
-              c_s[col0 + lane] = nw;
-              alpha_s[col0 + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
-            }
-            named_bar_sync(bar_id, 128);
-#pragma unroll
-            for (int i = 0; i < CPT; ++i) {
-              const float cn = c_s[col0 + i];
-              lp[i] *= alpha_s[col0 + i];
-              d[i] = ((mk >> i) & 1u) ? fmaf(__uint_as_float(sr[i]), p.scale_log2, -cn) : -INFINITY;
-              c[i] = cn;
-            }
-            if (t > 0) {
-              // O^T holds PV of this unit's tiles 0..t-1: wait for PV(G-1), rescale columns
-              mbar_wait(pv_done + (G - 1) % 2, (uint32_t)((G - 1) / 2) & 1);
-              tc_fence_after();
-              if (j < D) {
-                uint32_t o[CPT];
-                tmem_ld<CPT>(tO + col0 + lane_off, o);
-                tc_wait_ld();
-#pragma unroll
-                for (int i = 0; i < CPT; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha_s[col0 + i]);
-                tmem_st<CPT>(tO + col0 + lane_off, o);
-                tc_wait_st();
+              for (int i = 0; i < 32; ++i) {
+                if (!((qvalid[w] >> i) & 1u)) continue;
+                const int col = col0 + 32 * w + i, qc = col & 63;
+                const long long tq =
+                    g.q_frame_tok0[qf0 + (col >> 6)] + (long long)(qh0 + (qc >> 3)) * g.cols + qw0 + (qc & 7);
+                if ((m.bits[tq * m.words_per_row + (tk >> 6)] >> (tk & 63)) & 1ull) mk[w] |= 1u << i;
               }
             }
           }
-          if (threadIdx.x == 0) trace_at(p, 7, G);
-          // ---- P^T row j (bf16) and partial denominators (fp32) -------------------------
-#pragma unroll
-          for (int i = 0; i < CPT / 2; ++i) {
-            const float p0 = ex2(d[2 * i]), p1 = ex2(d[2 * i + 1]);
-            lp[2 * i] += p0;
-            lp[2 * i + 1] += p1;
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-            pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
-          }
         }
-        if (threadIdx.x == 0) trace_at(p, 8, G);
-        if (G >= kNP) mbar_wait(pv_done + (G - kNP) % 2, (uint32_t)((G - kNP) / 2) & 1);
-        if (threadIdx.x == 0) trace_at(p, 9, G);
-        // MN-major B operand: [NQ/64 groups][128 key rows][128 B], 16-B chunks swizzled by row
-        uint8_t* prow = sP + pb * Cfg::kPBytes + (col0 >> 6) * 16384 + j * 128;
-        const int ch0 = (col0 & 63) >> 3;
 #pragma unroll
-        for (int c8 = 0; c8 < CPT / 8; ++c8)
-          *reinterpret_cast<uint4*>(prow + (((ch0 + c8) ^ (j & 7)) << 4)) =
-              make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+        for (int w = 0; w < kW; ++w) my_pairs += __popc(mk[w]);
+        any = true;
+
+        mbar_wait(s_full + sb, (uint32_t)(G / kNS) & 1);
+        tc_fence_after();
+        if (threadIdx.x == 0) trace_at(p, 2, G);
+        // MN-major B operand: [NQ/64 groups][128 key rows][128 B], 16-B chunks swizzled by row
+        uint8_t* prow = sP + pb * Cfg::kPBytes + j * 128;
+        const float sl2 = p.scale_log2;
+        // Columns in 32-wide words: each word is loaded, exponentiated and stored on its own
+        // (32 live scores per thread); its columns have their own references and vote.
+#pragma unroll
+        for (int w = 0; w < kW; ++w) {
+          const int cw = col0 + 32 * w;                // first column of the word
+          const uint32_t tS = tS0 + sb * NQ + cw + lane_off;
+          float d[32];  // scores -> exponents -> probabilities
+          tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+          tc_wait_ld();
+          if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
+          uint32_t pk[16];
+          if (kInstrument && (p.debug & 1)) {  // experiment: no softmax math
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = 0x3f803f80u;  // bf16 pair (1, 1)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) lp[32 * w + i] += 1.0f;
+          } else {
+            // d = s*scale*log2(e) - c (one FFMA; c = -inf before a column's first key gives
+            // +inf, which forces the exact path); masked entries -> -inf (ex2 -> 0).  The mask
+            // word is warp-uniform except on ragged edge tiles: all-allowed / none / mixed.
+            const uint32_t mw = mk[w];
+            if (mw == 0xffffffffu) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
+                d[i] = fmaf(d[i], sl2, -c4.x);
+                d[i + 1] = fmaf(d[i + 1], sl2, -c4.y);
+                d[i + 2] = fmaf(d[i + 2], sl2, -c4.z);
+                d[i + 3] = fmaf(d[i + 3], sl2, -c4.w);
+              }
+            } else if (mw == 0u) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) d[i] = -INFINITY;
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
+                d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
+                d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
+                d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
+                d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
+              }
+            }
+            const bool need = bar_red_or(bar_id, 128, mw != 0u && tree_max<32>(d) > kRescaleThreshold);
+            if (threadIdx.x == 0) trace_at(p, 21 + 4 * w, G);
+            if (need) {
+              // exact column max of this tile over the group's 128 key rows, from the raw scores
+              tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) d[i] = ((mk[w] >> i) & 1u) ? d[i] * sl2 : -INFINITY;
+              warp_colreduce<32, true>(d, lane);
+              cg_red[quarter * 32 + lane] = d[0];
+              named_bar_sync(bar_id, 128);
+              if (quarter == 0) {
+                const float mx = fmaxf(fmaxf(cg_red[lane], cg_red[32 + lane]), fmaxf(cg_red[64 + lane], cg_red[96 + lane]));
+                const float cold = cg_c[cw + lane];
+                const float nw = fmaxf(cold, mx);
+                cg_c[cw + lane] = nw;
+                cg_a[cw + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
+              }
+              named_bar_sync(bar_id, 128);
+              tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                lp[32 * w + i] *= cg_a[cw + i];
+                d[i] = ((mk[w] >> i) & 1u) ? fmaf(d[i], sl2, -cg_c[cw + i]) : -INFINITY;
+              }
+              if (t >= kGroups) {
+                // O^T holds this group's PVs of the unit: wait for its last one, rescale columns
+                const int Gp = G - kGroups;
+                mbar_wait(pv_done + Gp % 2, (uint32_t)(Gp / 2) & 1);
+                tc_fence_after();
+                if (j < D) {
+                  uint32_t o[32];
+                  tmem_ld<32>(tO + cw + lane_off, o);
+                  tc_wait_ld();
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * cg_a[cw + i]);
+                  tmem_st<32>(tO + cw + lane_off, o);
+                  tc_wait_st();
+                }
+              }
+            }
+            if (threadIdx.x == 0) trace_at(p, 7, G);
+            // ---- P^T row j (bf16) and partial denominators (fp32) -------------------------
+            if (mw == 0u) {  // key row j of this tile is padding / masked for every column
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk[i] = 0u;
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float p0 = ex2(d[2 * i]), p1 = ex2(d[2 * i + 1]);
+                lp[32 * w + 2 * i] += p0;
+                lp[32 * w + 2 * i + 1] += p1;
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
+              }
+            }
+            if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
+          }
+          if (w == 0) {
+            if (threadIdx.x == 0) trace_at(p, 8, G);
+            // P buffer pb was last read by PV(G - NP)
+            if (G >= kNP) mbar_wait(pv_done + (G - kNP) % 2, (uint32_t)((G - kNP) / 2) & 1);
+            if (threadIdx.x == 0) trace_at(p, 9, G);
+          }
+          uint8_t* pw = prow + (cw >> 6) * 16384;
+          const int ch0 = (cw & 63) >> 3;
+#pragma unroll
+          for (int c8 = 0; c8 < 4; ++c8)
+            *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
+                make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+          if (threadIdx.x == 0) trace_at(p, 23 + 4 * w, G);
+        }
+        // S buffer free for QK(G + NS); P(G) visible to the tensor core
+        tc_fence_before();
         if (threadIdx.x == 0) trace_at(p, 10, G);
         fence_proxy_async_smem();
         if (threadIdx.x == 0) trace_at(p, 11, G);
-        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(pv_go + G % 2);
+        if (lane == 0) {
+          mbar_arrive(qk_go + sb);
+          mbar_arrive(pv_go + G % 2);
+        }
         if (threadIdx.x == 0) trace_at(p, 3, G);
       }
 
-      // ---- epilogue: denominators, normalise, store ------------------------------------
+      // ---- epilogue: per-group denominators, merge the groups, normalise, store --------
       if (p.pairs) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
         if (lane == 0 && my_pairs) atomicAdd(p.pairs, (unsigned long long)my_pairs);
       }
       warp_colreduce<CPT, false>(lp, lane);
-      {
-        const int rc = CPT == 32 ? lane : (lane >> 1);
-        if (CPT == 32 || (lane & 1) == 0) red[(cg * 4 + quarter) * CPT + rc] = lp[0];
-      }
+#pragma unroll
+      for (int i = 0; i < CPT / 32; ++i) cg_red[quarter * CPT + colreduce_col(CPT, lane, i)] = lp[i];
       named_bar_sync(bar_id, 128);
-      float* lsum = alpha_s;
-      if (quarter == 0 && lane < CPT) {
-        const float* r = red + cg * 4 * CPT + lane;
-        const float l = (r[0] + r[CPT]) + (r[2 * CPT] + r[3 * CPT]);
-        const int col = col0 + lane, qc = col & 63;
-        lsum[col] = l;
+      if (quarter == 0) {
+#pragma unroll
+        for (int i = 0; i < CPT / 32; ++i) {
+          const int cc = lane + 32 * i;
+          l_s[grp * 128 + col0 + cc] =
+              any ? (cg_red[cc] + cg_red[CPT + cc]) + (cg_red[2 * CPT + cc] + cg_red[3 * CPT + cc]) : 0.0f;
+        }
+      }
+      named_bar_sync(kAllBar, SW * 32);
+      // merge factors per query column: f_g = 2^(c_g - c) / l, l = sum_g l_g 2^(c_g - c)
+      const int tid = threadIdx.x;
+      if (tid < NQ) {
+        float cmax = -INFINITY;
+#pragma unroll
+        for (int gi = 0; gi < kGroups; ++gi) cmax = fmaxf(cmax, c_s[gi * 128 + tid]);
+        float e[kGroups], l = 0.0f;
+#pragma unroll
+        for (int gi = 0; gi < kGroups; ++gi) {
+          const float lg = l_s[gi * 128 + tid];
+          e[gi] = lg > 0.0f ? ex2(c_s[gi * 128 + tid] - cmax) : 0.0f;
+          l += lg * e[gi];
+        }
+#pragma unroll
+        for (int gi = 0; gi < kGroups; ++gi) f_s[gi * 128 + tid] = l > 0.0f ? e[gi] / l : 0.0f;
+        const int qc = tid & 63;
         const int qh = qh0 + (qc >> 3), qw = qw0 + (qc & 7);
-        if (qh < g.rows && qw < g.cols) {
-          const long long tq = g.q_frame_tok0[qf0 + (col >> 6)] + (long long)qh * g.cols + qw;
+        if (n > 0 && qh < g.rows && qw < g.cols) {
+          const long long tq = g.q_frame_tok0[qf0 + (tid >> 6)] + (long long)qh * g.cols + qw;
           if (tq >= p.row_begin && tq < p.row_end && !(l > 0.0f)) atomicOr(p.err, kErrDegenerate);
         }
       }
@@ -698,25 +799,38 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
         mbar_wait(o_full + ob, (uint32_t)(U >> 1) & 1);
         tc_fence_after();
       }
-      named_bar_sync(kAllBar, SW * 32);  // lsum visible, staging buffer free
-      if (n > 0) {
-        if (j < D) {
-          uint32_t o[CPT];
-          tmem_ld<CPT>(tO + col0 + lane_off, o);
-          tc_wait_ld();
+      named_bar_sync(kAllBar, SW * 32);  // factors visible, staging buffer free
+      {
+        // warp w: TMEM lane quarter w % 4, query-column slice w / 4 of NQ / (SW / 4) columns
+        constexpr int kSl = NQ / (SW / 4);
+        const int c0 = (warp >> 2) * kSl;
+        if (n > 0) {
+          if (j < D) {
+            float acc[kSl];
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) {
-            const float l = lsum[col0 + i];
-            const float val = l > 0.0f ? __uint_as_float(o[i]) / l : 0.0f;
-            so[(col0 + i) * D + j] = __bfloat16_as_ushort(__float2bfloat16_rn(val));
+            for (int i = 0; i < kSl; ++i) acc[i] = 0.0f;
+#pragma unroll
+            for (int gi = 0; gi < kGroups; ++gi) {
+              if (!(f_s[gi * 128 + c0] >= 0.0f)) continue;  // (always true; keeps the loop uniform)
+              uint32_t o[kSl];
+              tmem_ld<kSl>(tO0 + (gi * kOB + ob) * NQ + c0 + lane_off, o);
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < kSl; ++i) {
+                const float f = f_s[gi * 128 + c0 + i];
+                if (f != 0.0f) acc[i] = fmaf(__uint_as_float(o[i]), f, acc[i]);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < kSl; ++i) so[(c0 + i) * D + j] = __bfloat16_as_ushort(__float2bfloat16_rn(acc[i]));
           }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(o_empty + ob);
-      } else if (j < D) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(o_empty + ob);
+        } else if (j < D) {
 #pragma unroll
-        for (int i = 0; i < CPT; ++i) so[(col0 + i) * D + j] = 0;
+          for (int i = 0; i < kSl; ++i) so[(c0 + i) * D + j] = 0;
+        }
       }
       named_bar_sync(kAllBar, SW * 32);
       constexpr int kChunks = D / 8;
@@ -751,6 +865,5 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ, SWARPS>::kThreads, 1)
   tc_fence_after();
   if (warp == Cfg::kQkWarp) tmem_dealloc(tmem, Cfg::kTmemCols);
 }
-
 
 }  // namespace fvsr
