@@ -331,10 +331,28 @@ def run_b200(args):
     d2h = (HEADS if world == 1 else HEADS) * N * D * 2
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     hq = [[x.cpu().pin_memory() for x in fr] for fr in pool_local]
-    ho = torch.empty((HEADS, N, D), dtype=torch.bfloat16).pin_memory()
+    # Streaming pipeline: consecutive layer-steps (different layers, independent rings) go to
+    # alternating (context, stream) pairs, so step s+1's H2D copy overlaps step s's kernels
+    # and step s-1's D2H read.  Every step still copies its own inputs in and its output out.
+    n_pipe = 2 if world == 1 else 1
+    ctxs = [ctx] + [fv.Context() for _ in range(n_pipe - 1)]
+    streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(n_pipe - 1)]
+    hos = [torch.empty((HEADS, N, D), dtype=torch.bfloat16).pin_memory() for _ in range(n_pipe)]
+    ho = hos[0]
+    if world == 1:  # size each context's staging buffers outside the timed region
+        for j in range(n_pipe):
+            s = state["s"]
+            state["s"] += 1
+            l, t = s % LAYERS, T0 + s // LAYERS
+            q, k, v = hq[(t + l) % POOL]
+            _abi.check(lib.fvsr_ring_step_host(ctxs[j].h, rings.h, l, t, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                               C.byref(md), TOPK, scale, hos[j].data_ptr(),
+                                               C.c_void_p(streams[j].cuda_stream)))
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    for st in streams[1:]:
+        st.wait_event(e0)
     for i in range(e2e_steps):
         s = state["s"]
         state["s"] += 1
@@ -342,8 +360,10 @@ def run_b200(args):
         t = T0 + s // LAYERS
         q, k, v = hq[(t + l) % POOL]
         if world == 1:
-            _abi.check(lib.fvsr_ring_step_host(ctx.h, rings.h, l, t, q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                               C.byref(md), TOPK, scale, ho.data_ptr(), C.c_void_p(sptr)))
+            j = i % n_pipe
+            _abi.check(lib.fvsr_ring_step_host(ctxs[j].h, rings.h, l, t, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                               C.byref(md), TOPK, scale, hos[j].data_ptr(),
+                                               C.c_void_p(streams[j].cuda_stream)))
         else:
             qd, kd, vd = (x.to(dev, non_blocking=True) for x in (q, k, v))
             rings.append(l, t, kd, vd)
@@ -354,6 +374,10 @@ def run_b200(args):
             full = gather.result()
             ho.view(-1)[: full.numel()].copy_(full.reshape(-1)[: ho.numel()], non_blocking=True)
             rings.evict(l)
+    for st in streams[1:]:
+        ev = torch.cuda.Event()
+        ev.record(st)
+        stream.wait_event(ev)
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
@@ -361,10 +385,12 @@ def run_b200(args):
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    ctx.check_errors()
+    for c_, st in zip(ctxs, streams):
+        c_.check_errors(st)
     e2e = {"value": N * e2e_steps / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
-           "path": "fvsr_ring_step_host (C-ABI, pinned host buffers)" if world == 1 else
+           "path": f"fvsr_ring_step_host (C-ABI, pinned host buffers), {n_pipe} contexts/streams pipelined"
+                   if world == 1 else
                    "python composition over the C-ABI + NCCL gather, pinned host buffers"}
 
     if rank != 0:
