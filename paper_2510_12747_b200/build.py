@@ -44,6 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", SRC]
     if os.environ.get("FVSR_ATTN_INSTRUMENT"):  # experiments: per-tile timelines, debug short-cuts
         cmd.insert(1, "-DFVSR_ATTN_INSTRUMENT=1")
+    if os.environ.get("FVSR_ATTN_EXP"):  # experiments: bottleneck ablations (not attention)
+        cmd.insert(1, "-DFVSR_ATTN_EXP=" + str(int(os.environ["FVSR_ATTN_EXP"])))
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

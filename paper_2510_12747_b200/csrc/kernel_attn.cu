@@ -70,6 +70,13 @@ constexpr int kTraceCtaSlots = 16;  // per CTA: [0] start, [1..7] unit ends (glo
 #define FVSR_ATTN_INSTRUMENT 0
 #endif
 constexpr bool kInstrument = FVSR_ATTN_INSTRUMENT != 0;
+// Bottleneck experiments (results are NOT attention): -DFVSR_ATTN_EXP=mask of
+//   1 exp2 replaced by a constant (no MUFU), 2 S^T not read from TMEM (constant scores),
+//   4 no cross-warp rescale vote (exact path only on a group's first tile).
+#ifndef FVSR_ATTN_EXP
+#define FVSR_ATTN_EXP 0
+#endif
+constexpr int kExp = FVSR_ATTN_EXP;
 __device__ __forceinline__ void trace_at(const AttnParams& p, int ev, int G) {
   if (kInstrument && p.trace && blockIdx.x == 0 && G < kTraceTiles) p.trace[ev * kTraceTiles + G] = clock64();
 }
@@ -99,8 +106,9 @@ struct AttnCfg {
   static constexpr int kPvWarp = kSW + 3;            // PV issuer (own program order: QK never waits on P)
   static constexpr int kThreads = kSW * 32 + 128;
   static constexpr int kNS = NQ == 64 ? 4 : 2;       // S^T buffers in TMEM
-  static constexpr int kNK = NQ == 64 ? 3 : 2;       // K stages
-  static constexpr int kNV = 2;                      // V stages
+  static constexpr int kNK = 2;                      // K stages (QK consumes them right away)
+  static constexpr int kNV = NQ == 64 ? 3 : 2;       // V stages (released only after PV: deeper)
+  static constexpr int kPB = 4;                      // pv_go / pv_done barrier ring (> kNV)
   static constexpr int kNP = NQ == 64 ? 2 : 1;       // P^T buffers (one per group for NQ=64)
   static constexpr int kOB = 2;                      // O^T buffers per group (double-buffered units)
   static constexpr uint32_t kTileBytes = D * 128;    // one packed 64-row frame-tile
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
                        const __grid_constant__ AttnParams p) {
   using Cfg = AttnCfg<D, NQ>;
   constexpr int SW = Cfg::kSW, kNS = Cfg::kNS, CPT = Cfg::kCPT, kGroups = Cfg::kGroups, WG = Cfg::kWG;
-  constexpr int kNK = Cfg::kNK, kNV = Cfg::kNV, kNP = Cfg::kNP, kOB = Cfg::kOB;
+  constexpr int kNK = Cfg::kNK, kNV = Cfg::kNV, kNP = Cfg::kNP, kOB = Cfg::kOB, kPB = Cfg::kPB;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for SWIZZLE_128B, by offset so the compiler keeps the shared space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -252,16 +260,16 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   //   qk_go[G % NS]   K(G) landed (producer expect_tx + TMA bytes) and S buffer free
   //                   (arrivals of the tile's softmax group after reading S(G - NS))
   //   s_full[G % NS]  QK(G) complete (commit); also frees K stage G % NK for the producer
-  //   pv_go[G % 2]    V(G) landed (V producer expect_tx + TMA bytes) and P(G) written
-  //   pv_done[G % 2]  PV(G) complete (commit); frees V stage and P buffer
+  //   pv_go[G % PB]   V(G) landed (V producer expect_tx + TMA bytes) and P(G) written
+  //   pv_done[G % PB] PV(G) complete (commit); frees V stage and P buffer
   //   o_full / o_empty  per unit: all PVs done / epilogue read O
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* qk_go = bars + 2;
   uint64_t* s_full = qk_go + kNS;
   uint64_t* pv_go = s_full + kNS;
-  uint64_t* pv_done = pv_go + 2;
-  uint64_t* o_full = pv_done + 2;
+  uint64_t* pv_done = pv_go + kPB;
+  uint64_t* o_full = pv_done + kPB;
   uint64_t* o_empty = o_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
   float* c_s = reinterpret_cast<float*>(scratch + 256);  // [2][128] column references per group
@@ -299,7 +307,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int i = 0; i < kNS; ++i) { mbar_init(qk_go + i, WG + 1); mbar_init(s_full + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(pv_go + i, WG + 1); mbar_init(pv_done + i, 1); }
+    for (int i = 0; i < kPB; ++i) { mbar_init(pv_go + i, WG + 1); mbar_init(pv_done + i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, SW); }
     fence_barrier_init();
   }
@@ -404,13 +412,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         const TileMeta mt = bcast_meta(mine, t & 31);
         const int vs = T % kNV;
         // V stage vs is free once PV(T - NV) completed
-        if (T >= kNV) mbar_wait(pv_done + (T - kNV) % 2, (uint32_t)((T - kNV) / 2) & 1);
+        if (T >= kNV) mbar_wait(pv_done + (T - kNV) % kPB, (uint32_t)((T - kNV) / kPB) & 1);
         if (elect_one()) {
           if ((kInstrument && (p.debug & 2)) && T >= kNV) {
-            mbar_arrive(pv_go + T % 2);
+            mbar_arrive(pv_go + T % kPB);
           } else {
             trace_at(p, 5, T);
-            load_kv(p.v, sV + vs * Cfg::kKVBytes, mt, pv_go + T % 2);
+            load_kv(p.v, sV + vs * Cfg::kKVBytes, mt, pv_go + T % kPB);
           }
         }
         __syncwarp();
@@ -501,7 +509,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           trace_at(p, 15, G);
         }
         __syncwarp();
-        if (++gb == 2) { gb = 0; gph ^= 1u; }
+        if (++gb == kPB) { gb = 0; gph ^= 1u; }
         if (++vs == kNV) vs = 0;
         if (++pb == kNP) pb = 0;
       }
@@ -543,7 +551,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         win[16 + threadIdx.x] = lo;
         win[24 + threadIdx.x] = hi;
       }
-      if (threadIdx.x < 256) c_s[threadIdx.x] = -INFINITY;
+      if (threadIdx.x < 256) c_s[threadIdx.x] = (kInstrument && (p.debug & 1)) ? 0.0f : -INFINITY;
       named_bar_sync(kAllBar, SW * 32);
       // query columns of this thread that are real tokens, as 32-column words
       constexpr int kW = CPT / 32;
@@ -630,8 +638,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           const int cw = col0 + 32 * w;                // first column of the word
           const uint32_t tS = tS0 + sb * NQ + cw + lane_off;
           float d[32];  // scores -> exponents -> probabilities
-          tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
-          tc_wait_ld();
+          if (kExp & 2) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
+          } else {
+            tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+            tc_wait_ld();
+          }
           if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
           uint32_t pk[16];
           if (kInstrument && (p.debug & 1)) {  // experiment: no softmax math
@@ -666,7 +679,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
                 d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
               }
             }
-            const bool need = bar_red_or(bar_id, 128, mw != 0u && tree_max<32>(d) > kRescaleThreshold);
+            const bool need = (kExp & 4) ? (t < kGroups)
+                                         : bar_red_or(bar_id, 128, mw != 0u && tree_max<32>(d) > kRescaleThreshold);
             if (threadIdx.x == 0) trace_at(p, 21 + 4 * w, G);
             if (need) {
               // exact column max of this tile over the group's 128 key rows, from the raw scores
@@ -695,7 +709,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
               if (t >= kGroups) {
                 // O^T holds this group's PVs of the unit: wait for its last one, rescale columns
                 const int Gp = G - kGroups;
-                mbar_wait(pv_done + Gp % 2, (uint32_t)(Gp / 2) & 1);
+                mbar_wait(pv_done + Gp % kPB, (uint32_t)(Gp / kPB) & 1);
                 tc_fence_after();
                 if (j < D) {
                   uint32_t o[32];
@@ -716,7 +730,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
             } else {
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const float p0 = ex2(d[2 * i]), p1 = ex2(d[2 * i + 1]);
+                const float p0 = (kExp & 1) ? 1.0f : ex2(d[2 * i]), p1 = (kExp & 1) ? 1.0f : ex2(d[2 * i + 1]);
                 lp[32 * w + 2 * i] += p0;
                 lp[32 * w + 2 * i + 1] += p1;
                 const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
@@ -728,7 +742,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           if (w == 0) {
             if (threadIdx.x == 0) trace_at(p, 8, G);
             // P buffer pb was last read by PV(G - NP)
-            if (G >= kNP) mbar_wait(pv_done + (G - kNP) % 2, (uint32_t)((G - kNP) / 2) & 1);
+            if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
             if (threadIdx.x == 0) trace_at(p, 9, G);
           }
           uint8_t* pw = prow + (cw >> 6) * 16384;
@@ -747,7 +761,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(qk_go + sb);
-          mbar_arrive(pv_go + G % 2);
+          mbar_arrive(pv_go + G % kPB);
         }
         if (threadIdx.x == 0) trace_at(p, 3, G);
       }
