@@ -96,6 +96,7 @@ struct fvsr_ring {
   uint8_t* v = nullptr;
   float* s0 = nullptr;
   float* s1 = nullptr;
+  float* kn2 = nullptr;  // max squared key-row norm per (layer, head, slot, tile)
   std::vector<std::vector<std::pair<int, int>>> ctx;  // per layer: (frame_id, slot), ascending
   std::vector<std::vector<char>> used;                // per layer: slot occupancy
   long long kv_head_stride() const { return (long long)slots * n_tiles * (long long)tile_bytes; }
@@ -104,6 +105,8 @@ struct fvsr_ring {
   uint8_t* v_layer(int l) const { return v + (long long)l * heads * kv_head_stride(); }
   float* s0_layer(int l) const { return s0 + (long long)l * heads * part_head_stride(); }
   float* s1_layer(int l) const { return s1 + (long long)l * heads * part_head_stride(); }
+  long long kn2_head_stride() const { return (long long)slots * n_tiles; }
+  float* kn2_layer(int l) const { return kn2 + (long long)l * heads * kn2_head_stride(); }
 };
 
 namespace {
@@ -764,8 +767,10 @@ int32_t fvsr_ring_create(fvsr_ctx* ctx, int32_t layers, int32_t heads, int32_t d
   r->tile_bytes = (size_t)d * 128;
   const size_t kvb = (size_t)layers * heads * r->kv_head_stride();
   const size_t pb = (size_t)layers * heads * r->part_head_stride() * sizeof(float);
+  const size_t nb = (size_t)layers * heads * r->kn2_head_stride() * sizeof(float);
   if (cudaMalloc(&r->k, kvb) != cudaSuccess || cudaMalloc(&r->v, kvb) != cudaSuccess ||
-      cudaMalloc(&r->s0, pb) != cudaSuccess || cudaMalloc(&r->s1, pb) != cudaSuccess) {
+      cudaMalloc(&r->s0, pb) != cudaSuccess || cudaMalloc(&r->s1, pb) != cudaSuccess ||
+      cudaMalloc(&r->kn2, nb) != cudaSuccess) {
     fvsr_ring_destroy(r);
     return fail(FVSR_E_NOMEM, "ring allocation of %zu bytes failed", 2 * kvb + 2 * pb);
   }
@@ -781,6 +786,7 @@ void fvsr_ring_destroy(fvsr_ring* ring) {
   cudaFree(ring->v);
   cudaFree(ring->s0);
   cudaFree(ring->s1);
+  cudaFree(ring->kn2);
   delete ring;
 }
 
@@ -823,6 +829,8 @@ int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t fra
   a.s1 = r->s1_layer(layer);
   a.part_head_stride = r->part_head_stride();
   a.ext_s0 = r->s0_layer(layer);
+  a.norm2 = r->kn2_layer(layer);
+  a.norm2_head_stride = r->kn2_head_stride();
   a.rows = r->rows;
   a.cols = r->cols;
   a.tiles_w = r->tiles_w;
@@ -893,7 +901,8 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   const size_t qpart = (size_t)r->heads * g.nqf * g.n_tiles * d;
   const size_t nsel = (size_t)r->heads * g.bnq;
   int st;
-  void* ws = ws_get(ctx, Carve::need({qbytes, qpart * 4, qpart * 4, nsel * cap * 4, nsel * 4}), &st);
+  const size_t qn = (size_t)r->heads * g.nqf * g.n_tiles;
+  void* ws = ws_get(ctx, Carve::need({qbytes, qpart * 4, qpart * 4, nsel * cap * 4, nsel * 4, qn * 4}), &st);
   if (!ws) return st;
   Carve cv(ws);
   uint8_t* qp = cv.take<uint8_t>(qbytes);
@@ -901,6 +910,7 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   float* qs1 = cv.take<float>(qpart);
   int* wsel = cv.take<int>(nsel * cap);
   int* wcnt = cv.take<int>(nsel);
+  float* qn2 = cv.take<float>(qn);
   int* use_sel = sel ? sel : wsel;
   int* use_cnt = sel_count ? sel_count : wcnt;
 
@@ -915,6 +925,8 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
     a.s0 = qs0;
     a.s1 = qs1;
     a.part_head_stride = (long long)g.nqf * g.n_tiles * d;
+    a.norm2 = qn2;
+    a.norm2_head_stride = (long long)g.nqf * g.n_tiles;
     a.rows = g.rows;
     a.cols = g.cols;
     a.tiles_w = g.tiles_w;
@@ -958,6 +970,10 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   p.out_tile_major = out_layout == FVSR_OUT_TILE_MAJOR ? 1 : 0;
   p.err = ctx->d_err;
   p.pairs = ctx->d_pairs;
+  p.kn2 = r->kn2_layer(layer);
+  p.kn2_head_stride = r->kn2_head_stride();
+  p.qn2 = qn2;
+  p.qn2_head_stride = (long long)g.nqf * g.n_tiles;
   FVSR_TRY(launch_attention(ctx, g, dm, p, r->heads, unit_begin, unit_end, s));
   return after_launch(ctx, s, 4);
 }

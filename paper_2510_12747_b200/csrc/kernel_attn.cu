@@ -56,7 +56,15 @@ struct AttnParams {
   unsigned long long* pairs; // += executed (mask-allowed, selected-block) token pairs
   int debug;                 // experiments only (FVSR_ATTN_DEBUG): 1 skip softmax math, 2 skip K/V loads
   long long* trace;          // experiments only (FVSR_ATTN_TRACE): per-tile clock64 stamps of CTA 0
+  // Optional score bounds (null = always vote): max squared key-row norm per (slot, tile) and
+  // query-row norm per (q frame, tile).  |s| <= |q||k| lets a column group skip the rescale
+  // vote when no score of a tile can exceed the word's references by more than kBoundSlack.
+  const float* kn2;
+  long long kn2_head_stride;  // elements
+  const float* qn2;
+  long long qn2_head_stride;  // elements
 };
+constexpr float kBoundSlack = 64.0f;  // log2 units: p <= 2^64 keeps O, l and bf16 P finite
 
 // trace slots [event][tile]: 0 K issued, 1 QK issued, 2 S ready (softmax warp 0), 3 P done
 // (warp 0), 4 PV issued, 5 V issued, 6-11 S ready / P done of softmax warps 3/4/7, 12/13 QK
@@ -77,6 +85,10 @@ constexpr bool kInstrument = FVSR_ATTN_INSTRUMENT != 0;
 #define FVSR_ATTN_EXP 0
 #endif
 constexpr int kExp = FVSR_ATTN_EXP;
+#ifndef FVSR_POLY_EXP
+#define FVSR_POLY_EXP 0
+#endif
+constexpr bool kPolyExp = FVSR_POLY_EXP != 0;
 __device__ __forceinline__ void trace_at(const AttnParams& p, int ev, int G) {
   if (kInstrument && p.trace && blockIdx.x == 0 && G < kTraceTiles) p.trace[ev * kTraceTiles + G] = clock64();
 }
@@ -121,7 +133,7 @@ struct AttnCfg {
   static constexpr uint32_t kOffV = kOffK + kNK * kKVBytes;
   static constexpr uint32_t kOffP = kOffV + kNV * kKVBytes;
   static constexpr uint32_t kOffS = kOffP + kNP * kPBytes;  // scratch
-  static constexpr uint32_t kScratch = 10240;
+  static constexpr uint32_t kScratch = 11264;
   static constexpr uint32_t kBytes = kOffS + kScratch + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = 512;         // S x NS + O x groups x OB
   static_assert(kNS * NQ + kGroups * kOB * NQ <= 512, "TMEM budget");
@@ -133,6 +145,20 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA/ALU pipes only (no MUFU, no conversion unit): round-to-nearest via the
+// 1.5*2^23 magic constant, q(f) ~ 2^f on [-0.5, 0.5] (degree-3 fit, max rel. error 1.6e-4,
+// far below the bf16 rounding of P), exponent added as an integer.  Valid for finite x; x is
+// clamped at -127 (result then ~1e-38, negligible), so it is only used on unmasked words.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -127.0f);
+  const float j = xc + 12582912.0f;      // low mantissa bits = round(xc)
+  const float f = xc - (j - 12582912.0f);  // in [-0.5, 0.5]
+  float q = fmaf(0.0536014065f, f, 0.2423731536f);
+  q = fmaf(q, f, 0.6935025454f);
+  q = fmaf(q, f, 0.9999481440f);
+  return __int_as_float(__float_as_int(q) + (__float_as_int(j) << 23));
 }
 
 // Barrier over `n` threads that also ORs a predicate across them.
@@ -279,6 +305,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   float* red = f_s + 256;                                // [2][CGg][4][CPT] cross-quarter partials
   int* win = reinterpret_cast<int*>(red + 2 * Cfg::kCGg * 4 * CPT);  // [4][8] locality windows
   uint32_t* info = reinterpret_cast<uint32_t*>(win + 32);           // [kInfoCap]
+  float* kn2_s = reinterpret_cast<float*>(info + kInfoCap);        // [kInfoCap] key-norm bound per tile
+  float* cmin_s = kn2_s + kInfoCap;                                 // [2][CGg][CPT/32] min reference
+  float* qn2_s = cmin_s + 16;                                       // [1] query-norm bound of the unit
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long n_units = p.unit_end - p.unit_begin;
@@ -541,7 +570,28 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       const int qf0 = g.q_tr_first[qtr];
       const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
       // per-unit tables: tile infos, locality windows of the 8 query rows / cols
-      for (int i = threadIdx.x; i < min(n, kInfoCap); i += SW * 32) info[i] = tile_info(g, sel_at(sel, i));
+      for (int i = threadIdx.x; i < min(n, kInfoCap); i += SW * 32) {
+        const int kb = sel_at(sel, i);
+        info[i] = tile_info(g, kb);
+        float kn = INFINITY;
+        if (p.kn2) {
+          const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles, kf = g.k_tr_first[ktr];
+          const float* kh = p.kn2 + head * p.kn2_head_stride + ktile;
+          kn = kh[(long long)g.k_slot[kf] * g.n_tiles];
+          if (g.k_tr_count[ktr] == 2) kn = fmaxf(kn, kh[(long long)g.k_slot[kf + 1] * g.n_tiles]);
+        }
+        kn2_s[i] = kn;
+      }
+      if (threadIdx.x < 16) cmin_s[threadIdx.x] = -INFINITY;
+      if (threadIdx.x == 0) {
+        float qn = INFINITY;
+        if (p.qn2) {
+          qn = 0.0f;
+          for (int f = 0; f < g.q_tr_count[qtr]; ++f)
+            qn = fmaxf(qn, p.qn2[head * p.qn2_head_stride + (long long)(qf0 + f) * g.n_tiles + qtile]);
+        }
+        qn2_s[0] = qn;
+      }
       if (MK == 1 && threadIdx.x < 8) {
         int lo, hi;
         locality_range(m.mode, qh0 + threadIdx.x, m.extent_h, g.rows, lo, hi);
@@ -631,127 +681,198 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         // MN-major B operand: [NQ/64 groups][128 key rows][128 B], 16-B chunks swizzled by row
         uint8_t* prow = sP + pb * Cfg::kPBytes + j * 128;
         const float sl2 = p.scale_log2;
-        // Columns in 32-wide words: each word is loaded, exponentiated and stored on its own
-        // (32 live scores per thread); its columns have their own references and vote.
+        // Fast path: |q||k| bounds every score of the tile within kBoundSlack of each word's
+        // smallest reference, so no reference can need to move — no vote, no barrier, no
+        // memory-clobbering asm between the words, so their loads and math interleave.  The
+        // decision uses only shared inputs: all 4 warps of a column group take the same path.
+        bool fast = !(kExp & 4) && !(kInstrument && (p.debug & 1)) && t < kInfoCap;
+        if (fast) {
+          const float b2 = qn2_s[0] * kn2_s[t] * (sl2 * sl2) * 1.0002f;
 #pragma unroll
-        for (int w = 0; w < kW; ++w) {
-          const int cw = col0 + 32 * w;                // first column of the word
-          const uint32_t tS = tS0 + sb * NQ + cw + lane_off;
-          float d[32];  // scores -> exponents -> probabilities
-          if (kExp & 2) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
-          } else {
-            tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
-            tc_wait_ld();
+          for (int w = 0; w < kW; ++w) {
+            const float lim = kBoundSlack + cmin_s[(grp * Cfg::kCGg + cg) * kW + w];
+            fast = fast && lim > 0.0f && b2 <= lim * lim;
           }
-          if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
-          uint32_t pk[16];
-          if (kInstrument && (p.debug & 1)) {  // experiment: no softmax math
+        }
+        if (fast) {
+          uint32_t pk[CPT / 2];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = 0x3f803f80u;  // bf16 pair (1, 1)
-#pragma unroll
-            for (int i = 0; i < 32; ++i) lp[32 * w + i] += 1.0f;
-          } else {
-            // d = s*scale*log2(e) - c (one FFMA; c = -inf before a column's first key gives
-            // +inf, which forces the exact path); masked entries -> -inf (ex2 -> 0).  The mask
-            // word is warp-uniform except on ragged edge tiles: all-allowed / none / mixed.
+          for (int w = 0; w < kW; ++w) {
             const uint32_t mw = mk[w];
-            if (mw == 0xffffffffu) {
+            const float* cw = cg_c + col0 + 32 * w;
+            float d[32];
+            if (kExp & 2) {
 #pragma unroll
-              for (int i = 0; i < 32; i += 4) {
-                const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
-                d[i] = fmaf(d[i], sl2, -c4.x);
-                d[i + 1] = fmaf(d[i + 1], sl2, -c4.y);
-                d[i + 2] = fmaf(d[i + 2], sl2, -c4.z);
-                d[i + 3] = fmaf(d[i + 3], sl2, -c4.w);
-              }
-            } else if (mw == 0u) {
+              for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
+            } else {
+              tmem_ld<32>(tS0 + sb * NQ + col0 + 32 * w + lane_off, reinterpret_cast<uint32_t*>(d));
+              tc_wait_ld();
+            }
+            if (mw == 0u) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) d[i] = -INFINITY;
+              for (int i = 0; i < 16; ++i) pk[16 * w + i] = 0u;
             } else {
 #pragma unroll
               for (int i = 0; i < 32; i += 4) {
-                const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
+                const float4 c4 = *reinterpret_cast<const float4*>(cw + i);
                 d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
                 d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
                 d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
                 d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
               }
-            }
-            const bool need = (kExp & 4) ? (t < kGroups)
-                                         : bar_red_or(bar_id, 128, mw != 0u && tree_max<32>(d) > kRescaleThreshold);
-            if (threadIdx.x == 0) trace_at(p, 21 + 4 * w, G);
-            if (need) {
-              // exact column max of this tile over the group's 128 key rows, from the raw scores
-              tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
-              tc_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) d[i] = ((mk[w] >> i) & 1u) ? d[i] * sl2 : -INFINITY;
-              warp_colreduce<32, true>(d, lane);
-              cg_red[quarter * 32 + lane] = d[0];
-              named_bar_sync(bar_id, 128);
-              if (quarter == 0) {
-                const float mx = fmaxf(fmaxf(cg_red[lane], cg_red[32 + lane]), fmaxf(cg_red[64 + lane], cg_red[96 + lane]));
-                const float cold = cg_c[cw + lane];
-                const float nw = fmaxf(cold, mx);
-                cg_c[cw + lane] = nw;
-                cg_a[cw + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
-              }
-              named_bar_sync(bar_id, 128);
-              tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
-              tc_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                lp[32 * w + i] *= cg_a[cw + i];
-                d[i] = ((mk[w] >> i) & 1u) ? fmaf(d[i], sl2, -cg_c[cw + i]) : -INFINITY;
-              }
-              if (t >= kGroups) {
-                // O^T holds this group's PVs of the unit: wait for its last one, rescale columns
-                const int Gp = G - kGroups;
-                mbar_wait(pv_done + Gp % kPB, (uint32_t)(Gp / kPB) & 1);
-                tc_fence_after();
-                if (j < D) {
-                  uint32_t o[32];
-                  tmem_ld<32>(tO + cw + lane_off, o);
-                  tc_wait_ld();
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * cg_a[cw + i]);
-                  tmem_st<32>(tO + cw + lane_off, o);
-                  tc_wait_st();
-                }
-              }
-            }
-            if (threadIdx.x == 0) trace_at(p, 7, G);
-            // ---- P^T row j (bf16) and partial denominators (fp32) -------------------------
-            if (mw == 0u) {  // key row j of this tile is padding / masked for every column
-#pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = 0u;
-            } else {
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 const float p0 = (kExp & 1) ? 1.0f : ex2(d[2 * i]), p1 = (kExp & 1) ? 1.0f : ex2(d[2 * i + 1]);
                 lp[32 * w + 2 * i] += p0;
                 lp[32 * w + 2 * i + 1] += p1;
                 const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
+                pk[16 * w + i] = *reinterpret_cast<const uint32_t*>(&h2);
               }
             }
-            if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
           }
-          if (w == 0) {
-            if (threadIdx.x == 0) trace_at(p, 8, G);
-            // P buffer pb was last read by PV(G - NP)
-            if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
-            if (threadIdx.x == 0) trace_at(p, 9, G);
-          }
-          uint8_t* pw = prow + (cw >> 6) * 16384;
-          const int ch0 = (cw & 63) >> 3;
+          // P buffer pb was last read by PV(G - NP)
+          if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
 #pragma unroll
-          for (int c8 = 0; c8 < 4; ++c8)
-            *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
-                make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
-          if (threadIdx.x == 0) trace_at(p, 23 + 4 * w, G);
+          for (int w = 0; w < kW; ++w) {
+            const int cwi = col0 + 32 * w;
+            uint8_t* pw = prow + (cwi >> 6) * 16384;
+            const int ch0 = (cwi & 63) >> 3;
+#pragma unroll
+            for (int c8 = 0; c8 < 4; ++c8)
+              *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
+                  make_uint4(pk[16 * w + 4 * c8], pk[16 * w + 4 * c8 + 1], pk[16 * w + 4 * c8 + 2],
+                             pk[16 * w + 4 * c8 + 3]);
+          }
+        } else {
+          // Columns in 32-wide words: each word is loaded, exponentiated and stored on its own
+          // (32 live scores per thread); its columns have their own references and vote.
+  #pragma unroll
+          for (int w = 0; w < kW; ++w) {
+            const int cw = col0 + 32 * w;                // first column of the word
+            const uint32_t tS = tS0 + sb * NQ + cw + lane_off;
+            float d[32];  // scores -> exponents -> probabilities
+            if (kExp & 2) {
+  #pragma unroll
+              for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
+            } else {
+              tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+              tc_wait_ld();
+            }
+            if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
+            uint32_t pk[16];
+            if (kInstrument && (p.debug & 1)) {  // experiment: no softmax math
+  #pragma unroll
+              for (int i = 0; i < 16; ++i) pk[i] = 0x3f803f80u;  // bf16 pair (1, 1)
+  #pragma unroll
+              for (int i = 0; i < 32; ++i) lp[32 * w + i] += 1.0f;
+            } else {
+              // d = s*scale*log2(e) - c (one FFMA; c = -inf before a column's first key gives
+              // +inf, which forces the exact path); masked entries -> -inf (ex2 -> 0).  The mask
+              // word is warp-uniform except on ragged edge tiles: all-allowed / none / mixed.
+              const uint32_t mw = mk[w];
+              if (mw == 0xffffffffu) {
+  #pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
+                  d[i] = fmaf(d[i], sl2, -c4.x);
+                  d[i + 1] = fmaf(d[i + 1], sl2, -c4.y);
+                  d[i + 2] = fmaf(d[i + 2], sl2, -c4.z);
+                  d[i + 3] = fmaf(d[i + 3], sl2, -c4.w);
+                }
+              } else if (mw == 0u) {
+  #pragma unroll
+                for (int i = 0; i < 32; ++i) d[i] = -INFINITY;
+              } else {
+  #pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
+                  d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
+                  d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
+                  d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
+                  d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
+                }
+              }
+              const bool need = (kExp & 4) ? (t < kGroups)
+                                           : bar_red_or(bar_id, 128, mw != 0u && tree_max<32>(d) > kRescaleThreshold);
+              if (threadIdx.x == 0) trace_at(p, 21 + 4 * w, G);
+              if (need) {
+                // exact column max of this tile over the group's 128 key rows, from the raw scores
+                tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+                tc_wait_ld();
+  #pragma unroll
+                for (int i = 0; i < 32; ++i) d[i] = ((mk[w] >> i) & 1u) ? d[i] * sl2 : -INFINITY;
+                warp_colreduce<32, true>(d, lane);
+                cg_red[quarter * 32 + lane] = d[0];
+                named_bar_sync(bar_id, 128);
+                if (quarter == 0) {
+                  const float mx = fmaxf(fmaxf(cg_red[lane], cg_red[32 + lane]), fmaxf(cg_red[64 + lane], cg_red[96 + lane]));
+                  const float cold = cg_c[cw + lane];
+                  const float nw = fmaxf(cold, mx);
+                  cg_c[cw + lane] = nw;
+                  cg_a[cw + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
+                  float mn = nw;
+  #pragma unroll
+                  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                  if (lane == 0) cmin_s[(grp * Cfg::kCGg + cg) * kW + w] = mn;
+                }
+                named_bar_sync(bar_id, 128);
+                tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+                tc_wait_ld();
+  #pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  lp[32 * w + i] *= cg_a[cw + i];
+                  d[i] = ((mk[w] >> i) & 1u) ? fmaf(d[i], sl2, -cg_c[cw + i]) : -INFINITY;
+                }
+                if (t >= kGroups) {
+                  // O^T holds this group's PVs of the unit: wait for its last one, rescale columns
+                  const int Gp = G - kGroups;
+                  mbar_wait(pv_done + Gp % kPB, (uint32_t)(Gp / kPB) & 1);
+                  tc_fence_after();
+                  if (j < D) {
+                    uint32_t o[32];
+                    tmem_ld<32>(tO + cw + lane_off, o);
+                    tc_wait_ld();
+  #pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * cg_a[cw + i]);
+                    tmem_st<32>(tO + cw + lane_off, o);
+                    tc_wait_st();
+                  }
+                }
+              }
+              if (threadIdx.x == 0) trace_at(p, 7, G);
+              // ---- P^T row j (bf16) and partial denominators (fp32) -------------------------
+              if (mw == 0u) {  // key row j of this tile is padding / masked for every column
+  #pragma unroll
+                for (int i = 0; i < 16; ++i) pk[i] = 0u;
+              } else {
+  #pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  // every 4th pair of an unmasked word on the FMA pipe (balances MUFU and issue)
+                  const bool poly = kPolyExp && (i & 3) == 3 && mw == 0xffffffffu;
+                  const float p0 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i]) : ex2(d[2 * i]));
+                  const float p1 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i + 1]) : ex2(d[2 * i + 1]));
+                  lp[32 * w + 2 * i] += p0;
+                  lp[32 * w + 2 * i + 1] += p1;
+                  const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                  pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
+                }
+              }
+              if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
+            }
+            if (w == 0) {
+              if (threadIdx.x == 0) trace_at(p, 8, G);
+              // P buffer pb was last read by PV(G - NP)
+              if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
+              if (threadIdx.x == 0) trace_at(p, 9, G);
+            }
+            uint8_t* pw = prow + (cw >> 6) * 16384;
+            const int ch0 = (cw & 63) >> 3;
+  #pragma unroll
+            for (int c8 = 0; c8 < 4; ++c8)
+              *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
+                  make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+            if (threadIdx.x == 0) trace_at(p, 23 + 4 * w, G);
+          }
         }
         // S buffer free for QK(G + NS); P(G) visible to the tensor core
         tc_fence_before();

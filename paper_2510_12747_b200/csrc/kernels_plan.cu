@@ -148,6 +148,8 @@ struct PackPoolArgs {
   float* s1;
   long long part_head_stride;  // elements
   const float* ext_s0;         // partner S0 for single-frame groups (ring appends), may be null
+  float* norm2;                // optional: max squared row norm of src per frame-tile [slot][tile]
+  long long norm2_head_stride; // elements
   int rows, cols, tiles_w, n_tiles, d;
 };
 
@@ -249,11 +251,47 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
     for (int t = 0; t < nt; ++t) {
       const uint8_t* st = stage(fi, t);
       uint8_t* dst = (t == 0 ? a.dst : a.dst2) + to;
-      for (int i = tid; i < chunks; i += kPPThreads) {
+      // Thread tid touches rows tid/8 + 16*(k%4) (8 channels per chunk); with norm2 it also
+      // accumulates those rows' sums of squares (bounds every score |q.k| <= |q||k| for the
+      // attention kernel's rescale-vote skip).
+      float rowacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int i = tid, k = 0; i < chunks; i += kPPThreads, ++k) {
         const int panel = i >> 9, r = (i >> 3) & 63, j = i & 7;
         const int c = panel * 64 + ((j ^ (r & 7)) << 3);
         const uint4 v = *reinterpret_cast<const uint4*>(st + (r * d + c) * 2);
         *reinterpret_cast<uint4*>(dst + (size_t)i * 16) = v;
+        if (t == 0 && a.norm2) {
+          const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+          float acc = rowacc[k & 3];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float x = __uint_as_float(w4[e] << 16), y = __uint_as_float(w4[e] & 0xffff0000u);
+            acc = fmaf(x, x, fmaf(y, y, acc));
+          }
+          rowacc[k & 3] = acc;
+        }
+      }
+      if (t == 0 && a.norm2) {
+        __shared__ float wmax[kPPThreads / 32];
+        float mx = 0.0f;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          float rs = rowacc[kk];  // full row sum over the 8 lanes sharing tid / 8
+          rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+          rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+          rs += __shfl_xor_sync(0xffffffffu, rs, 4);
+          mx = fmaxf(mx, rs);
+        }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        if ((tid & 31) == 0) wmax[tid >> 5] = mx;
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+          for (int w = 1; w < kPPThreads / 32; ++w) mx = fmaxf(mx, wmax[w]);
+          a.norm2[head * a.norm2_head_stride + (long long)slot * a.n_tiles + tile] = mx;
+        }
+        __syncthreads();
       }
     }
   }
