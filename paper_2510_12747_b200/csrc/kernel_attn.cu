@@ -80,7 +80,8 @@ constexpr int kTraceCtaSlots = 16;  // per CTA: [0] start, [1..7] unit ends (glo
 constexpr bool kInstrument = FVSR_ATTN_INSTRUMENT != 0;
 // Bottleneck experiments (results are NOT attention): -DFVSR_ATTN_EXP=mask of
 //   1 exp2 replaced by a constant (no MUFU), 2 S^T not read from TMEM (constant scores),
-//   4 no cross-warp rescale vote (exact path only on a group's first tile).
+//   4 no cross-warp rescale vote (exact path only on a group's first tile),
+//   16 no K/V traffic after the first stages (producers arrive without loading).
 #ifndef FVSR_ATTN_EXP
 #define FVSR_ATTN_EXP 0
 #endif
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         // K stage ks is free once QK(T - NK) completed
         if (T >= kNK) mbar_wait(s_full + (T - kNK) % kNS, (uint32_t)((T - kNK) / kNS) & 1);
         if (elect_one()) {
-          if ((kInstrument && (p.debug & 2)) && T >= kNK) {  // experiment: no K traffic after the first stages
+          if (((kInstrument && (p.debug & 2)) || (kExp & 16)) && T >= kNK) {  // experiment: no K traffic after the first stages
             mbar_arrive(qk_go + T % kNS);
           } else {
             trace_at(p, 0, T);
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         // V stage vs is free once PV(T - NV) completed
         if (T >= kNV) mbar_wait(pv_done + (T - kNV) % kPB, (uint32_t)((T - kNV) / kPB) & 1);
         if (elect_one()) {
-          if ((kInstrument && (p.debug & 2)) && T >= kNV) {
+          if (((kInstrument && (p.debug & 2)) || (kExp & 16)) && T >= kNV) {
             mbar_arrive(pv_go + T % kPB);
           } else {
             trace_at(p, 5, T);
