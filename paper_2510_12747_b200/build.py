@@ -44,6 +44,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", SRC]
     if os.environ.get("FVSR_ATTN_INSTRUMENT"):  # experiments: per-tile timelines, debug short-cuts
         cmd.insert(1, "-DFVSR_ATTN_INSTRUMENT=1")
+    if os.environ.get("FVSR_FIXED_REF"):  # experiments: 0 = always start from -inf references
+        cmd.insert(1, "-DFVSR_FIXED_REF=" + str(int(os.environ["FVSR_FIXED_REF"])))
+    if os.environ.get("FVSR_BALANCE_TAIL"):  # experiments: 0 = plain round-robin units
+        cmd.insert(1, "-DFVSR_BALANCE_TAIL=" + str(int(os.environ["FVSR_BALANCE_TAIL"])))
     if os.environ.get("FVSR_ATTN_EXP"):  # experiments: bottleneck ablations (not attention)
         cmd.insert(1, "-DFVSR_ATTN_EXP=" + str(int(os.environ["FVSR_ATTN_EXP"])))
     if verbose:

@@ -65,6 +65,10 @@ struct AttnParams {
   long long qn2_head_stride;  // elements
 };
 constexpr float kBoundSlack = 64.0f;  // log2 units: p <= 2^64 keeps O, l and bf16 P finite
+constexpr float kFixedBound = 60.0f;  // |s*scale*log2e| <= 60 for the unit: fixed reference 0
+#ifndef FVSR_FIXED_REF
+#define FVSR_FIXED_REF 1
+#endif
 
 // trace slots [event][tile]: 0 K issued, 1 QK issued, 2 S ready (softmax warp 0), 3 P done
 // (warp 0), 4 PV issued, 5 V issued, 6-11 S ready / P done of softmax warps 3/4/7, 12/13 QK
@@ -583,7 +587,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         }
         kn2_s[i] = kn;
       }
-      if (threadIdx.x < 16) cmin_s[threadIdx.x] = -INFINITY;
       if (threadIdx.x == 0) {
         float qn = INFINITY;
         if (p.qn2) {
@@ -602,7 +605,22 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         win[16 + threadIdx.x] = lo;
         win[24 + threadIdx.x] = hi;
       }
-      if (threadIdx.x < 256) c_s[threadIdx.x] = (kInstrument && (p.debug & 1)) ? 0.0f : -INFINITY;
+      named_bar_sync(kAllBar, SW * 32);
+      // Fixed-reference mode: when |q||k| bounds every score of the unit by kFixedBound (log2
+      // units), the references start at 0 and never move: p = 2^(s*scale*log2e) stays within
+      // [2^-kFixedBound, 2^kFixedBound] (no overflow, no underflow), every tile takes the
+      // barrier-free fast path and the first tiles need no exact column max.  Otherwise the
+      // references start at -inf (exact lazy-rescale path).
+      {
+        float kmax = 0.0f;
+        const int nt = min(n, kInfoCap);
+        for (int i = 0; i < nt; ++i) kmax = fmaxf(kmax, kn2_s[i]);
+        const float b2 = qn2_s[0] * kmax * (p.scale_log2 * p.scale_log2) * 1.0002f;
+        const bool fixed = FVSR_FIXED_REF && n <= kInfoCap && b2 <= kFixedBound * kFixedBound;
+        const float c0v = ((kInstrument && (p.debug & 1)) || fixed) ? 0.0f : -INFINITY;
+        if (threadIdx.x < 256) c_s[threadIdx.x] = c0v;
+        if (threadIdx.x < 16) cmin_s[threadIdx.x] = c0v;
+      }
       named_bar_sync(kAllBar, SW * 32);
       // query columns of this thread that are real tokens, as 32-column words
       constexpr int kW = CPT / 32;

@@ -20,8 +20,12 @@ def frame_data(seed, heads, n, d):
     return a[:, 0], a[:, 1], a[:, 2]
 
 
-@pytest.mark.parametrize("window,start,mask", [(4, 0, None), (3, 5, ("loc", 9, 13, True)), (2, 1, ("loc", 7, 7, False))])
-def test_streaming_ring_matches_oracle(window, start, mask):
+# qscale > 1 makes |q||k| exceed the fixed-reference bound, so the kernel runs the exact
+# lazy-rescale path (references start at -inf and move with the running column max)
+@pytest.mark.parametrize("window,start,mask,qscale", [(4, 0, None, 1.0), (3, 5, ("loc", 9, 13, True), 1.0),
+                                                      (2, 1, ("loc", 7, 7, False), 1.0), (4, 0, None, 6.0),
+                                                      (3, 2, ("loc", 9, 13, True), 6.0)])
+def test_streaming_ring_matches_oracle(window, start, mask, qscale):
     heads, rows, cols, d, topk, layers = 2, 20, 36, 128, 4, 2
     n = rows * cols
     fmask = fv.Mask.all_allowed() if mask is None else fv.Mask.locality(mask[1], mask[2], mask[3])
@@ -30,6 +34,7 @@ def test_streaming_ring_matches_oracle(window, start, mask):
     ctx_k, ctx_v, ids = [], [], []
     for t in range(start, start + 9):
         q, k, v = frame_data(t + 17, heads, n, d)
+        q = oracle.bf16_round(q * np.float32(qscale))
         layer = t % layers  # exercise per-layer bookkeeping
         ring.append(layer, t, to_dev(k), to_dev(v))
         if layer == 0:
