@@ -138,7 +138,7 @@ struct AttnCfg {
   static constexpr uint32_t kOffV = kOffK + kNK * kKVBytes;
   static constexpr uint32_t kOffP = kOffV + kNV * kKVBytes;
   static constexpr uint32_t kOffS = kOffP + kNP * kPBytes;  // scratch
-  static constexpr uint32_t kScratch = 11264;
+  static constexpr uint32_t kScratch = 13312;
   static constexpr uint32_t kBytes = kOffS + kScratch + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = 512;         // S x NS + O x groups x OB
   static_assert(kNS * NQ + kGroups * kOB * NQ <= 512, "TMEM budget");
@@ -302,17 +302,23 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   uint64_t* pv_done = pv_go + kPB;
   uint64_t* o_full = pv_done + kPB;
   uint64_t* o_empty = o_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* tab_full = o_empty + 2;   // per-unit tables built (producer)
+  uint64_t* tab_empty = tab_full + 2; // per-unit tables released (softmax epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tab_empty + 2);
   float* c_s = reinterpret_cast<float*>(scratch + 256);  // [2][128] column references per group
   float* alpha_s = c_s + 256;                            // [2][128] rescale factors
   float* l_s = alpha_s + 256;                            // [2][128] denominators
   float* f_s = l_s + 256;                                // [2][128] merge factors (incl. 1/l)
   float* red = f_s + 256;                                // [2][CGg][4][CPT] cross-quarter partials
-  int* win = reinterpret_cast<int*>(red + 2 * Cfg::kCGg * 4 * CPT);  // [4][8] locality windows
-  uint32_t* info = reinterpret_cast<uint32_t*>(win + 32);           // [kInfoCap]
-  float* kn2_s = reinterpret_cast<float*>(info + kInfoCap);        // [kInfoCap] key-norm bound per tile
-  float* cmin_s = kn2_s + kInfoCap;                                 // [2][CGg][CPT/32] min reference
-  float* qn2_s = cmin_s + 16;                                       // [1] query-norm bound of the unit
+  // Per-unit tables, double-buffered by unit parity and built ahead by the Q/K producer:
+  // locality windows [2][32], tile infos [2][kInfoCap], key-norm bounds [2][kInfoCap],
+  // query-norm bound [2], initial reference [2]
+  int* win2 = reinterpret_cast<int*>(red + 2 * Cfg::kCGg * 4 * CPT);
+  uint32_t* info2 = reinterpret_cast<uint32_t*>(win2 + 64);
+  float* kn2_2 = reinterpret_cast<float*>(info2 + 2 * kInfoCap);
+  float* qn2_2 = kn2_2 + 2 * kInfoCap;
+  float* c0_2 = qn2_2 + 2;
+  float* cmin_s = c0_2 + 2;                                         // [2][CGg][CPT/32] min reference
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long n_units = p.unit_end - p.unit_begin;
@@ -343,6 +349,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     for (int i = 0; i < kNS; ++i) { mbar_init(qk_go + i, WG + 1); mbar_init(s_full + i, 1); }
     for (int i = 0; i < kPB; ++i) { mbar_init(pv_go + i, WG + 1); mbar_init(pv_done + i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, SW); }
+    for (int i = 0; i < 2; ++i) { mbar_init(tab_full + i, 1); mbar_init(tab_empty + i, SW); }
     fence_barrier_init();
   }
   tc_fence_before();
@@ -400,6 +407,58 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       const int* sel;
       decode(u, head, qtr, qtile, n, sel);
       if (n == 0) continue;
+      // ---- per-unit tables for the softmax warps (slot U & 1) --------------------------
+      {
+        if (U >= 2) mbar_wait(tab_empty + (U & 1), ((U >> 1) - 1) & 1);
+        const int sl = U & 1;
+        uint32_t* info = info2 + sl * kInfoCap;
+        float* kn2_s = kn2_2 + sl * kInfoCap;
+        float kmax = 0.0f;
+        for (int i = lane; i < min(n, kInfoCap); i += 32) {
+          const int kb = sel_at(sel, i);
+          info[i] = tile_info(g, kb);
+          float kn = INFINITY;
+          if (p.kn2) {
+            const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles, kf = g.k_tr_first[ktr];
+            const float* kh = p.kn2 + head * p.kn2_head_stride + ktile;
+            kn = kh[(long long)g.k_slot[kf] * g.n_tiles];
+            if (g.k_tr_count[ktr] == 2) kn = fmaxf(kn, kh[(long long)g.k_slot[kf + 1] * g.n_tiles]);
+          }
+          kn2_s[i] = kn;
+          kmax = fmaxf(kmax, kn);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        float qn = INFINITY;
+        if (p.qn2) {
+          qn = 0.0f;
+          for (int f = 0; f < g.q_tr_count[qtr]; ++f)
+            qn = fmaxf(qn, p.qn2[head * p.qn2_head_stride + (long long)(g.q_tr_first[qtr] + f) * g.n_tiles + qtile]);
+        }
+        // Fixed-reference mode: when |q||k| bounds every score of the unit by kFixedBound (log2
+        // units), the references start at 0 and never move: p = 2^(s*scale*log2e) stays in
+        // [2^-kFixedBound, 2^kFixedBound] (no overflow, no underflow), every tile takes the
+        // barrier-free fast path and no first tile needs an exact column max.  Otherwise the
+        // references start at -inf (exact lazy-rescale path).
+        const float b2 = qn * kmax * (p.scale_log2 * p.scale_log2) * 1.0002f;
+        const bool fixed = FVSR_FIXED_REF && n <= kInfoCap && b2 <= kFixedBound * kFixedBound;
+        if (lane == 0) {
+          qn2_2[sl] = qn;
+          c0_2[sl] = ((kInstrument && (p.debug & 1)) || fixed) ? 0.0f : -INFINITY;
+        }
+        if (MK == 1 && lane < 8) {
+          const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
+          int lo, hi;
+          locality_range(m.mode, qh0 + lane, m.extent_h, g.rows, lo, hi);
+          win2[sl * 32 + lane] = lo;
+          win2[sl * 32 + 8 + lane] = hi;
+          locality_range(m.mode, qw0 + lane, m.extent_w, g.cols, lo, hi);
+          win2[sl * 32 + 16 + lane] = lo;
+          win2[sl * 32 + 24 + lane] = hi;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tab_full + sl);
+      }
       if (U >= 1) mbar_wait(q_empty, (U - 1) & 1);
       if (elect_one()) {
         mbar_arrive_expect_tx(q_full, Cfg::kQBytes);
@@ -561,6 +620,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     const int bar_id = 1 + grp * 4 + cg;  // named barrier of the column group (128 threads)
     const int grp_bar = 9 + grp;          // named barrier of the group
     constexpr int kAllBar = 11;           // named barrier of all softmax warps
+    constexpr int kW = CPT / 32;
     float* cg_c = c_s + grp * 128;
     float* cg_a = alpha_s + grp * 128;
     float* cg_red = red + (grp * Cfg::kCGg + cg) * 4 * CPT;
@@ -574,56 +634,21 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       decode(u, head, qtr, qtile, n, sel);
       const int qf0 = g.q_tr_first[qtr];
       const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
-      // per-unit tables: tile infos, locality windows of the 8 query rows / cols
-      for (int i = threadIdx.x; i < min(n, kInfoCap); i += SW * 32) {
-        const int kb = sel_at(sel, i);
-        info[i] = tile_info(g, kb);
-        float kn = INFINITY;
-        if (p.kn2) {
-          const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles, kf = g.k_tr_first[ktr];
-          const float* kh = p.kn2 + head * p.kn2_head_stride + ktile;
-          kn = kh[(long long)g.k_slot[kf] * g.n_tiles];
-          if (g.k_tr_count[ktr] == 2) kn = fmaxf(kn, kh[(long long)g.k_slot[kf + 1] * g.n_tiles]);
-        }
-        kn2_s[i] = kn;
+      // per-unit tables (slot U & 1), built ahead by the Q/K producer
+      const int tsl = U & 1;
+      const uint32_t* info = info2 + tsl * kInfoCap;
+      const float* kn2_s = kn2_2 + tsl * kInfoCap;
+      const float* qn2_s = qn2_2 + tsl;
+      const int* win = win2 + tsl * 32;
+      if (n > 0) {
+        mbar_wait(tab_full + tsl, (uint32_t)(U >> 1) & 1);
+        // this group's references (and their word minima) start at the unit's initial value
+        const float c0v = c0_2[tsl];
+        for (int i = wl * 32 + lane; i < NQ; i += WG * 32) cg_c[i] = c0v;
+        if (wl == 0 && lane < Cfg::kCGg * kW) cmin_s[grp * Cfg::kCGg * kW + lane] = c0v;
+        named_bar_sync(grp_bar, WG * 32);
       }
-      if (threadIdx.x == 0) {
-        float qn = INFINITY;
-        if (p.qn2) {
-          qn = 0.0f;
-          for (int f = 0; f < g.q_tr_count[qtr]; ++f)
-            qn = fmaxf(qn, p.qn2[head * p.qn2_head_stride + (long long)(qf0 + f) * g.n_tiles + qtile]);
-        }
-        qn2_s[0] = qn;
-      }
-      if (MK == 1 && threadIdx.x < 8) {
-        int lo, hi;
-        locality_range(m.mode, qh0 + threadIdx.x, m.extent_h, g.rows, lo, hi);
-        win[threadIdx.x] = lo;
-        win[8 + threadIdx.x] = hi;
-        locality_range(m.mode, qw0 + threadIdx.x, m.extent_w, g.cols, lo, hi);
-        win[16 + threadIdx.x] = lo;
-        win[24 + threadIdx.x] = hi;
-      }
-      named_bar_sync(kAllBar, SW * 32);
-      // Fixed-reference mode: when |q||k| bounds every score of the unit by kFixedBound (log2
-      // units), the references start at 0 and never move: p = 2^(s*scale*log2e) stays within
-      // [2^-kFixedBound, 2^kFixedBound] (no overflow, no underflow), every tile takes the
-      // barrier-free fast path and the first tiles need no exact column max.  Otherwise the
-      // references start at -inf (exact lazy-rescale path).
-      {
-        float kmax = 0.0f;
-        const int nt = min(n, kInfoCap);
-        for (int i = 0; i < nt; ++i) kmax = fmaxf(kmax, kn2_s[i]);
-        const float b2 = qn2_s[0] * kmax * (p.scale_log2 * p.scale_log2) * 1.0002f;
-        const bool fixed = FVSR_FIXED_REF && n <= kInfoCap && b2 <= kFixedBound * kFixedBound;
-        const float c0v = ((kInstrument && (p.debug & 1)) || fixed) ? 0.0f : -INFINITY;
-        if (threadIdx.x < 256) c_s[threadIdx.x] = c0v;
-        if (threadIdx.x < 16) cmin_s[threadIdx.x] = c0v;
-      }
-      named_bar_sync(kAllBar, SW * 32);
       // query columns of this thread that are real tokens, as 32-column words
-      constexpr int kW = CPT / 32;
       uint32_t qvalid[kW];
 #pragma unroll
       for (int w = 0; w < kW; ++w) {
@@ -1006,6 +1031,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         }
       }
       named_bar_sync(kAllBar, SW * 32);  // staging buffer and per-unit tables reusable
+      if (n > 0 && lane == 0) mbar_arrive(tab_empty + tsl);
       if (threadIdx.x == 0) trace_cta(p, 1 + U);
       if (n > 0) {
         T += n;
