@@ -191,6 +191,10 @@ FVSR_API int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer,
                          const uint16_t* k, const uint16_t* v, fvsr_stream_t stream);
 /* KVCache::evict with the sliding_window strategy (P/src/kv_cache.cpp:100-106). */
 FVSR_API int32_t fvsr_ring_evict_sliding(fvsr_ring* ring, int32_t layer);
+/* Sliding eviction down to `keep` frames (oldest first).  Chunked streaming of Tq frames per
+ * step (the paper's 2-latent chunks) creates the ring with window_frames = W + Tq - 1 and
+ * calls this with keep = W before appending each chunk. */
+FVSR_API int32_t fvsr_ring_evict_keep(fvsr_ring* ring, int32_t layer, int32_t keep);
 /* KVCache::frame_ids (identical for every head under sliding eviction). */
 FVSR_API int32_t fvsr_ring_frame_ids(const fvsr_ring* ring, int32_t layer, int32_t* ids, int32_t cap,
                             int32_t* n);

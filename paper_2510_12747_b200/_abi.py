@@ -98,6 +98,7 @@ SIGNATURES = {
     "fvsr_ring_destroy": (None, [P]),
     "fvsr_ring_append": (I32, [P, P, I32, I32, P, P, P]),
     "fvsr_ring_evict_sliding": (I32, [P, I32]),
+    "fvsr_ring_evict_keep": (I32, [P, I32, I32]),
     "fvsr_ring_frame_ids": (I32, [P, I32, C.POINTER(I32), I32, C.POINTER(I32)]),
     "fvsr_ring_attention": (I32, [P, P, I32, P, C.POINTER(I32), I32, MP, I64, F32, I64, I64, P, I32, I32, P, P,
                                   P]),

@@ -859,6 +859,18 @@ int32_t fvsr_ring_evict_sliding(fvsr_ring* r, int32_t layer) {
   return FVSR_OK;
 }
 
+int32_t fvsr_ring_evict_keep(fvsr_ring* r, int32_t layer, int32_t keep) {
+  if (!r) return fail(FVSR_E_CONFIG, "null ring");
+  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
+  if (keep < 0) return fail(FVSR_E_CONFIG, "ring_evict_keep: keep must be >= 0");
+  auto& c = r->ctx[layer];
+  while ((int)c.size() > keep) {  // sliding: oldest first (kv_cache.cpp:100-106)
+    r->used[layer][c.front().second] = 0;
+    c.erase(c.begin());
+  }
+  return FVSR_OK;
+}
+
 int32_t fvsr_ring_frame_ids(const fvsr_ring* r, int32_t layer, int32_t* ids, int32_t cap, int32_t* n) {
   if (!r) return fail(FVSR_E_CONFIG, "null ring");
   if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");

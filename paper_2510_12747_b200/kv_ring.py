@@ -56,8 +56,12 @@ class KVRing:
         check(self.ctx.lib.fvsr_ring_append(self.ctx.h, self.h, layer, int(frame_id), k3.data_ptr(), v3.data_ptr(),
                                             _stream()))
 
-    def evict(self, layer: int) -> None:
-        check(self.ctx.lib.fvsr_ring_evict_sliding(self.h, layer))
+    def evict(self, layer: int, keep: Optional[int] = None) -> None:
+        """KVCache::evict(sliding): down to the window, or to `keep` frames (chunked streaming)."""
+        if keep is None:
+            check(self.ctx.lib.fvsr_ring_evict_sliding(self.h, layer))
+        else:
+            check(self.ctx.lib.fvsr_ring_evict_keep(self.h, layer, int(keep)))
 
     def frame_ids(self, layer: int):
         buf = (C.c_int32 * 64)()
