@@ -294,6 +294,7 @@ def run_b200(args):
     ev0.record(stream)
     for _ in range(args.steps):
         step()
+    w_enq = time.time()
     if gather:
         gather.drain()
     ev1.record(stream)
@@ -454,6 +455,7 @@ def run_b200(args):
         "e2e": e2e,
         "clocks": clocks.summary(),
         "gpu_launches": launches,
+        "host_enqueue_us_per_step": (w_enq - w0) * 1e6 / args.steps,
         "executed_pairs_per_step": pairs_total / args.steps,
     }
     print(json.dumps(line), flush=True)
