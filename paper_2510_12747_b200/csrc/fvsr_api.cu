@@ -496,7 +496,8 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
     const char* names[kTraceEvents] = {"K",    "QK",   "S0",  "P0",  "PV",    "V",     "vote",  "rare",
                                        "exps", "pbuf", "sts", "fence", "QKmma", "QKcmt", "PVmma", "PVcmt",
                                        "wV",   "wP",   "wK",  "wS",    "ld0",   "vt0",   "ex0",   "st0",
-                                       "ld1",  "vt1",  "ex1", "st1"};
+                                       "ld1",  "vt1",  "ex1", "st1",
+                                       "Ebeg", "El",   "Eof", "Eo",    "Est",   "Unx",   "Utab",  "Qiss"};
     const long long base = h[0];
     std::fprintf(stderr, "trace (cycles from first K issue), tiles 0..60\n  G");
     for (int e = 0; e < kTraceEvents; ++e) std::fprintf(stderr, "%9s", names[e]);
@@ -504,6 +505,13 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
     for (int G = 0; G < 60; ++G) {
       std::fprintf(stderr, "%3d", G);
       for (int e = 0; e < kTraceEvents; ++e) std::fprintf(stderr, "%9lld", h[e * kTraceTiles + G] ? h[e * kTraceTiles + G] - base : -1);
+      std::fprintf(stderr, "\n");
+    }
+    std::fprintf(stderr, "per-unit (cycles from first K issue):\n");
+    for (int U = 0; U < 8; ++U) {
+      std::fprintf(stderr, "U%d", U);
+      for (int e = 28; e < kTraceEvents; ++e)
+        std::fprintf(stderr, " %s=%lld", names[e], h[e * kTraceTiles + U] ? h[e * kTraceTiles + U] - base : -1);
       std::fprintf(stderr, "\n");
     }
     // per-CTA unit timeline (globaltimer ns)

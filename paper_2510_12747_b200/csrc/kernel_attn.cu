@@ -74,7 +74,7 @@ constexpr float kFixedBound = 60.0f;  // |s*scale*log2e| <= 60 for the unit: fix
 // (warp 0), 4 PV issued, 5 V issued, 6-11 S ready / P done of softmax warps 3/4/7, 12/13 QK
 // MMAs / commits issued, 14/15 PV MMAs / commits issued.
 constexpr int kTraceTiles = 512;
-constexpr int kTraceEvents = 28;
+constexpr int kTraceEvents = 36;  // 28-35: per-unit epilogue stamps (indexed by unit)
 constexpr int kTraceCtaSlots = 16;  // per CTA: [0] start, [1..7] unit ends (globaltimer ns); +8: clock64
 // Instrumentation (per-tile timeline, debug short-cuts) only exists in builds with
 // -DFVSR_ATTN_INSTRUMENT=1; the production kernel carries none of it.
@@ -85,7 +85,9 @@ constexpr bool kInstrument = FVSR_ATTN_INSTRUMENT != 0;
 // Bottleneck experiments (results are NOT attention): -DFVSR_ATTN_EXP=mask of
 //   1 exp2 replaced by a constant (no MUFU), 2 S^T not read from TMEM (constant scores),
 //   4 no cross-warp rescale vote (exact path only on a group's first tile),
-//   16 no K/V traffic after the first stages (producers arrive without loading).
+//   16 no K/V traffic after the first stages (producers arrive without loading),
+//   32 no epilogue (O is never read or stored), 64 epilogue without TMEM loads, 128 epilogue
+//   without the output stores.
 #ifndef FVSR_ATTN_EXP
 #define FVSR_ATTN_EXP 0
 #endif
@@ -111,7 +113,7 @@ __device__ __forceinline__ void trace_cta(const AttnParams& p, int slot) {
 
 template <int D, int NQ>
 struct AttnCfg {
-  static constexpr int kSW = 8;                      // softmax warps (12 warps total: 168 registers)
+  static constexpr int kSW = 8;                      // softmax warps (two warpgroups, 168 registers)
   static constexpr int kGroups = NQ == 64 ? 2 : 1;   // ping-pong softmax groups (tile parity)
   static constexpr int kWG = kSW / kGroups;          // warps per group
   static constexpr int kCGg = kWG / 4;               // column groups per group (4 lane quarters each)
@@ -121,12 +123,21 @@ struct AttnCfg {
   static constexpr int kQkWarp = kSW + 1;            // QK^T issuer (+ TMEM allocator)
   static constexpr int kVProducerWarp = kSW + 2;     // V tiles (decoupled so K runs ahead)
   static constexpr int kPvWarp = kSW + 3;            // PV issuer (own program order: QK never waits on P)
-  static constexpr int kThreads = kSW * 32 + 128;
+  static constexpr int kEpiWarp = kSW + 4;           // epilogue warpgroup (merge, normalise, store)
+  static constexpr int kThreads = kSW * 32 + 256;    // 16 warps
+  static constexpr int kRegSoftmax = 168;            // setmaxnreg: 256 x 168 + 256 x 88 = 64K
+  static constexpr int kRegOther = 88;
   static constexpr int kNS = NQ == 64 ? 4 : 2;       // S^T buffers in TMEM
   static constexpr int kNK = 2;                      // K stages (QK consumes them right away)
-  static constexpr int kNV = NQ == 64 ? 3 : 2;       // V stages (released only after PV: deeper)
+#ifndef FVSR_NV64
+#define FVSR_NV64 2
+#endif
+#ifndef FVSR_NP64
+#define FVSR_NP64 4
+#endif
+  static constexpr int kNV = NQ == 64 ? FVSR_NV64 : 2;  // V stages (released only after PV: deeper)
   static constexpr int kPB = 4;                      // pv_go / pv_done barrier ring (> kNV)
-  static constexpr int kNP = NQ == 64 ? 2 : 1;       // P^T buffers (one per group for NQ=64)
+  static constexpr int kNP = NQ == 64 ? FVSR_NP64 : 1;  // P^T buffers (per group: kNP / 2 for NQ=64)
   static constexpr int kOB = 2;                      // O^T buffers per group (double-buffered units)
   static constexpr uint32_t kTileBytes = D * 128;    // one packed 64-row frame-tile
   static constexpr uint32_t kQSub = NQ * 128;        // Q sub-tile stride (NQ rows x 128 B)
@@ -138,12 +149,21 @@ struct AttnCfg {
   static constexpr uint32_t kOffV = kOffK + kNK * kKVBytes;
   static constexpr uint32_t kOffP = kOffV + kNV * kKVBytes;
   static constexpr uint32_t kOffS = kOffP + kNP * kPBytes;  // scratch
-  static constexpr uint32_t kScratch = 13312;
-  static constexpr uint32_t kBytes = kOffS + kScratch + 1024;  // + alignment slack
+  static constexpr uint32_t kScratch = NQ == 64 ? 13312 : 16384;
+  // scratch layout (bytes): barriers 256 | c [2][2][128] f32 | alpha [2][128] | l [2][2][128] |
+  // f [2][128] | red [2][CGg][4][CPT] | win [2][32] i32 | info [2][cap] | kn2 [2][cap] | qn2 [2] |
+  // c0 [2] | cmin [2][CGg][CPT/32] | unit [2][4] i32
+  static constexpr uint32_t kScratchUsed =
+      256 + 4 * (512 + 256 + 512 + 256) + 4 * (2 * kCGg * 4 * kCPT) + 4 * 64 + 8 * 2 * 256 + 16 +
+      4 * (2 * kCGg * (kCPT / 32)) + 32;
+  static_assert(kScratchUsed <= kScratch, "scratch budget");
+  static constexpr uint32_t kOffE = kOffS + kScratch;         // epilogue staging chunk
+  static constexpr uint32_t kEpiBytes = 4096;
+  static constexpr int kEpiCols = kEpiBytes / (2 * D);        // query columns per staged chunk
+  static constexpr uint32_t kBytes = kOffE + kEpiBytes + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = 512;         // S x NS + O x groups x OB
   static_assert(kNS * NQ + kGroups * kOB * NQ <= 512, "TMEM budget");
   static_assert(kBytes <= 232448, "shared memory budget");
-  static_assert(kNP * NQ * 256 >= NQ * D * 2, "O staging fits the P buffers");
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -164,6 +184,24 @@ __device__ __forceinline__ float ex2_poly(float x) {
   q = fmaf(q, f, 0.6935025454f);
   q = fmaf(q, f, 0.9999481440f);
   return __int_as_float(__float_as_int(q) + (__float_as_int(j) << 23));
+}
+
+// Packed fp32 pairs (FMUL2 / FADD2 on sm_100): a * s and a += b on two lanes of a pair.
+__device__ __forceinline__ void fmul2(float& a0, float& a1, float s) {
+  unsigned long long x;
+  asm("{\n\t.reg .b64 s2;\n\tmov.b64 s2, {%3, %3};\n\tmov.b64 %0, {%1, %2};\n\t"
+      "mul.rn.f32x2 %0, %0, s2;\n\t}"
+      : "=l"(x)
+      : "f"(a0), "f"(a1), "f"(s));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(x));
+}
+__device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) {
+  unsigned long long x;
+  asm("{\n\t.reg .b64 b2;\n\tmov.b64 b2, {%3, %4};\n\tmov.b64 %0, {%1, %2};\n\t"
+      "add.rn.f32x2 %0, %0, b2;\n\t}"
+      : "=l"(x)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(x));
 }
 
 // Barrier over `n` threads that also ORs a predicate across them.
@@ -294,6 +332,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   //   pv_go[G % PB]   V(G) landed (V producer expect_tx + TMA bytes) and P(G) written
   //   pv_done[G % PB] PV(G) complete (commit); frees V stage and P buffer
   //   o_full / o_empty  per unit: all PVs done / epilogue read O
+  //   tab_full / tab_empty  per-unit tables built (producer) / released (epilogue)
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* qk_go = bars + 2;
@@ -303,12 +342,12 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   uint64_t* o_full = pv_done + kPB;
   uint64_t* o_empty = o_full + 2;
   uint64_t* tab_full = o_empty + 2;   // per-unit tables built (producer)
-  uint64_t* tab_empty = tab_full + 2; // per-unit tables released (softmax epilogue)
+  uint64_t* tab_empty = tab_full + 2; // per-unit tables released (epilogue)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tab_empty + 2);
-  float* c_s = reinterpret_cast<float*>(scratch + 256);  // [2][128] column references per group
-  float* alpha_s = c_s + 256;                            // [2][128] rescale factors
-  float* l_s = alpha_s + 256;                            // [2][128] denominators
-  float* f_s = l_s + 256;                                // [2][128] merge factors (incl. 1/l)
+  float* c_s = reinterpret_cast<float*>(scratch + 256);  // [unit parity][group][128] column references
+  float* alpha_s = c_s + 512;                            // [group][128] rescale factors
+  float* l_s = alpha_s + 256;                            // [unit parity][group][128] denominators
+  float* f_s = l_s + 512;                                // [group][128] merge factors (incl. 1/l)
   float* red = f_s + 256;                                // [2][CGg][4][CPT] cross-quarter partials
   // Per-unit tables, double-buffered by unit parity and built ahead by the Q/K producer:
   // locality windows [2][32], tile infos [2][kInfoCap], key-norm bounds [2][kInfoCap],
@@ -319,8 +358,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   float* qn2_2 = kn2_2 + 2 * kInfoCap;
   float* c0_2 = qn2_2 + 2;
   float* cmin_s = c0_2 + 2;                                         // [2][CGg][CPT/32] min reference
+  int* utab = reinterpret_cast<int*>(cmin_s + 2 * Cfg::kCGg * (CPT / 32));  // [2][4] n head qtr qtile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // named barriers: 1.. softmax column groups, 9/10 softmax groups, 12 epilogue warpgroup,
+  // 13/14 (by unit parity) softmax end of unit -> epilogue
+  constexpr int kStatBar0 = 13;
+  constexpr int kStatCount = 128 + 32 * kGroups * Cfg::kCGg;
   const long long n_units = p.unit_end - p.unit_begin;
   const int units_per_head = p.n_trows * g.n_tiles;
 
@@ -348,8 +392,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     mbar_init(q_empty, 1);
     for (int i = 0; i < kNS; ++i) { mbar_init(qk_go + i, WG + 1); mbar_init(s_full + i, 1); }
     for (int i = 0; i < kPB; ++i) { mbar_init(pv_go + i, WG + 1); mbar_init(pv_done + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, SW); }
-    for (int i = 0; i < 2; ++i) { mbar_init(tab_full + i, 1); mbar_init(tab_empty + i, SW); }
+    for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(tab_full + i, 1); mbar_init(tab_empty + i, 4); }
+
     fence_barrier_init();
   }
   tc_fence_before();
@@ -398,6 +443,138 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     }
   };
 
+  // ================================ epilogue warpgroup ====================================
+  // Per unit (same order as every role): wait for both groups' references and denominators
+  // (named barrier 13 | 14) and all PVs (o_full), merge the groups' O^T accumulators,
+  // O = sum_g 2^(c_g - c) O_g / sum_g 2^(c_g - c) l_g, and store bf16 rows straight from
+  // registers (lane pairs swap one value so each lane writes a 2-channel word).  Runs beside
+  // the softmax warps, which move on to the next unit at once.
+  auto epilogue_warps = [&]() {
+    const int q4 = warp & 3;                   // TMEM lane quarter = channel rows 32*q4..
+    const int et = threadIdx.x - Cfg::kEpiWarp * 32;
+    const int dj = q4 * 32 + lane;             // output channel of this lane
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    constexpr int kEpiBar = 12;
+    constexpr int kEC = Cfg::kEpiCols;
+    uint16_t* stage = reinterpret_cast<uint16_t*>(smem + Cfg::kOffE);  // [kEC][D] bf16
+    int U = 0;
+    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int head, qtr, qtile, n;
+      const int* sel;
+      decode(u, head, qtr, qtile, n, sel);
+      const int qf0 = g.q_tr_first[qtr];
+      const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
+      const int cv = min(8, g.cols - qw0);   // real tokens per tile row
+      // first token of tile row r (0-7) of q frame f (0-1) of this unit
+      auto row_tok = [&](int f, int r) { return g.q_frame_tok0[qf0 + f] + (long long)(qh0 + r) * g.cols + qw0; };
+      if (n == 0) {  // no selected block: the unit's real rows are zero
+        constexpr int kChunks = D / 8;
+        for (int idx = et; idx < NQ * kChunks; idx += 128) {
+          const int col = idx / kChunks, ch = idx % kChunks, qc = col & 63;
+          if (qh0 + (qc >> 3) >= g.rows || (qc & 7) >= cv) continue;
+          uint16_t* row = p.out_tile_major ? p.out + (u * NQ + col) * D
+                                           : p.out + head * p.out_head_stride + (row_tok(col >> 6, qc >> 3) + (qc & 7)) * D;
+          *reinterpret_cast<uint4*>(row + ch * 8) = make_uint4(0, 0, 0, 0);
+        }
+        continue;
+      }
+      const int par = U & 1;
+      // hardware barrier, not an mbarrier: the epilogue waits most of a unit here and a parked
+      // warp costs no issue slots (ids alternate by unit parity: the softmax cannot run two
+      // units ahead, it needs the tables this epilogue releases)
+      named_bar_sync(kStatBar0 + par, kStatCount);
+      if (et == 0) trace_at(p, 30, U);
+      // merge factors per query column: f_g = 2^(c_g - c) / l, l = sum_g l_g 2^(c_g - c);
+      // zero for columns outside [row_begin, row_end) (their rows are written as zeros)
+      if (et < NQ) {
+        float cmax = -INFINITY;
+#pragma unroll
+        for (int gi = 0; gi < kGroups; ++gi) cmax = fmaxf(cmax, c_s[(par * 2 + gi) * 128 + et]);
+        float e[kGroups], l = 0.0f;
+#pragma unroll
+        for (int gi = 0; gi < kGroups; ++gi) {
+          const float lg = l_s[(par * 2 + gi) * 128 + et];
+          e[gi] = lg > 0.0f ? ex2(c_s[(par * 2 + gi) * 128 + et] - cmax) : 0.0f;
+          l += lg * e[gi];
+        }
+        const int qc = et & 63;
+        bool inr = false;
+        if (qh0 + (qc >> 3) < g.rows && (qc & 7) < cv) {
+          const long long tq = row_tok(et >> 6, qc >> 3) + (qc & 7);
+          inr = tq >= p.row_begin && tq < p.row_end;
+          if (inr && !(l > 0.0f)) atomicOr(p.err, kErrDegenerate);
+        }
+#pragma unroll
+        for (int gi = 0; gi < kGroups; ++gi) f_s[gi * 128 + et] = (inr && l > 0.0f) ? e[gi] / l : 0.0f;
+      }
+      mbar_wait_sleep(o_full + par, (uint32_t)(U >> 1) & 1, 128);
+      tc_fence_after();
+      if (et == 0) trace_at(p, 31, U);
+      named_bar_sync(kEpiBar, 128);  // factors visible
+      // O in chunks of kEC query columns: TMEM -> merged bf16 -> staging -> bulk store
+#pragma unroll 1
+      for (int c0 = 0; c0 < ((kExp & 32) ? 0 : NQ); c0 += kEC) {
+        float acc[kEC];
+#pragma unroll
+        for (int i = 0; i < kEC; ++i) acc[i] = 0.0f;
+#pragma unroll
+        for (int gi = 0; gi < kGroups; ++gi) {
+          uint32_t o[kEC];
+          if (kExp & 64) {
+#pragma unroll
+            for (int i = 0; i < kEC; ++i) o[i] = 0x3f800000u;
+          } else {
+            tmem_ld<kEC>(tO0 + (gi * kOB + par) * NQ + c0 + lane_off, o);
+            tc_wait_ld();
+          }
+          const float* fg = f_s + gi * 128 + c0;
+#pragma unroll
+          for (int i = 0; i < kEC; i += 4) {
+            const float4 f4 = *reinterpret_cast<const float4*>(fg + i);
+            // a group without tiles in this unit has f = 0 and an undefined accumulator
+            if (f4.x != 0.0f) acc[i] = fmaf(__uint_as_float(o[i]), f4.x, acc[i]);
+            if (f4.y != 0.0f) acc[i + 1] = fmaf(__uint_as_float(o[i + 1]), f4.y, acc[i + 1]);
+            if (f4.z != 0.0f) acc[i + 2] = fmaf(__uint_as_float(o[i + 2]), f4.z, acc[i + 2]);
+            if (f4.w != 0.0f) acc[i + 3] = fmaf(__uint_as_float(o[i + 3]), f4.w, acc[i + 3]);
+          }
+        }
+        if (et == 0) bulk_wait_read();  // the previous chunk's stores have read the staging
+        if (!(kExp & 512)) named_bar_sync(kEpiBar, 128);
+        if (dj < D && !(kExp & 256)) {
+#pragma unroll
+          for (int i = 0; i < kEC; ++i) stage[i * D + dj] = __bfloat16_as_ushort(__float2bfloat16_rn(acc[i]));
+        }
+        if (!(kExp & 256)) fence_proxy_async_smem();
+        if (!(kExp & 512)) named_bar_sync(kEpiBar, 128);
+        if (et == 0 && !(kExp & 128)) {
+          if (p.out_tile_major) {
+            bulk_s2g(p.out + (u * NQ + c0) * D, stage, kEC * D * 2);
+          } else {
+            // the chunk's tile rows: cv consecutive tokens each
+#pragma unroll 1
+            for (int r0 = c0; r0 < c0 + kEC; r0 += 8) {
+              const int qc = r0 & 63;
+              if (qh0 + (qc >> 3) < g.rows)
+                bulk_s2g(p.out + head * p.out_head_stride + row_tok(r0 >> 6, qc >> 3) * D, stage + (r0 - c0) * D,
+                         cv * D * 2);
+            }
+          }
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_empty + par);   // O^T buffers of this parity free for unit U + 2
+      if (lane == 0) mbar_arrive(tab_empty + par); // tables and c / l slots reusable (f is ours)
+      if (et == 0) trace_at(p, 32, U);
+      if (et == 0) trace_cta(p, 1 + U);
+      ++U;
+    }
+    if (et == 0) bulk_wait_all();
+  };
+
+  if (warp >= SW) {
+  reg_dealloc<Cfg::kRegOther>();
   if (warp == Cfg::kProducerWarp) {
     // ================================ Q / K producer (warp-wide) =========================
     int T = 0;  // tiles of this CTA so far
@@ -443,6 +620,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         const float b2 = qn * kmax * (p.scale_log2 * p.scale_log2) * 1.0002f;
         const bool fixed = FVSR_FIXED_REF && n <= kInfoCap && b2 <= kFixedBound * kFixedBound;
         if (lane == 0) {
+          utab[sl * 4 + 0] = n;
+          utab[sl * 4 + 1] = head;
+          utab[sl * 4 + 2] = qtr;
+          utab[sl * 4 + 3] = qtile;
           qn2_2[sl] = qn;
           c0_2[sl] = ((kInstrument && (p.debug & 1)) || fixed) ? 0.0f : -INFINITY;
         }
@@ -459,8 +640,20 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(tab_full + sl);
       }
+      // the next unit's Q into L2 now: its load below waits for this unit's last QK and
+      // would otherwise pay the full HBM latency between units
+      if (lane < 2 && u + gridDim.x < n_units) {
+        int nh, ntr, ntile, nn;
+        const int* nsel;
+        decode(u + gridDim.x, nh, ntr, ntile, nn, nsel);
+        if (lane < g.q_tr_count[ntr])
+          bulk_prefetch_l2(p.q + nh * p.q_head_stride +
+                               ((long long)(g.q_tr_first[ntr] + lane) * g.n_tiles + ntile) * Cfg::kTileBytes,
+                           Cfg::kTileBytes);
+      }
       if (U >= 1) mbar_wait(q_empty, (U - 1) & 1);
       if (elect_one()) {
+        trace_at(p, 35, U);
         mbar_arrive_expect_tx(q_full, Cfg::kQBytes);
         const int f0 = g.q_tr_first[qtr];
         const uint8_t* qa = p.q + head * p.q_head_stride + ((long long)f0 * g.n_tiles + qtile) * Cfg::kTileBytes;
@@ -491,6 +684,12 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         __syncwarp();
       }
       ++U;
+    }
+    // end of the unit stream for the softmax warps
+    if (U >= 2) mbar_wait(tab_empty + (U & 1), ((U >> 1) - 1) & 1);
+    if (lane == 0) {
+      utab[(U & 1) * 4] = -1;
+      mbar_arrive(tab_full + (U & 1));
     }
   } else if (warp == Cfg::kVProducerWarp) {
     // ================================ V producer (warp-wide) =============================
@@ -609,6 +808,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       ++U;
     }
   } else {
+    epilogue_warps();
+  }
+  } else {
+    reg_alloc<Cfg::kRegSoftmax>();
     // ===================================== softmax warps ================================
     // Group grp handles the tiles G with G % kGroups == grp (ping-pong: the two groups'
     // latencies overlap) with its own running references and O^T accumulator.
@@ -619,45 +822,48 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     const int col0 = cg * CPT;          // first of this thread's CPT query columns
     const int bar_id = 1 + grp * 4 + cg;  // named barrier of the column group (128 threads)
     const int grp_bar = 9 + grp;          // named barrier of the group
-    constexpr int kAllBar = 11;           // named barrier of all softmax warps
     constexpr int kW = CPT / 32;
-    float* cg_c = c_s + grp * 128;
     float* cg_a = alpha_s + grp * 128;
     float* cg_red = red + (grp * Cfg::kCGg + cg) * 4 * CPT;
     if (lane == 0)
       for (int i = grp; i < kNS; i += kGroups) mbar_arrive(qk_go + i);  // S buffers start free
     int T = 0;
-    int U = 0;
-    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int head, qtr, qtile, n;
-      const int* sel;
-      decode(u, head, qtr, qtile, n, sel);
+    // Units with work, in the producer's order, from its per-unit tables (slot U & 1); an
+    // entry with n < 0 ends the stream.  Empty units are the epilogue warps' alone.
+    for (int U = 0;; ++U) {
+      const int tsl = U & 1;
+      if (threadIdx.x == 0) trace_at(p, 33, U);
+      mbar_wait(tab_full + tsl, (uint32_t)(U >> 1) & 1);
+      if (threadIdx.x == 0) trace_at(p, 34, U);
+      const int n = utab[tsl * 4];
+      if (n < 0) break;
+      const int head = utab[tsl * 4 + 1], qtr = utab[tsl * 4 + 2], qtile = utab[tsl * 4 + 3];
+      const int* sel = p.sel + ((long long)head * g.bnq + qtr * g.n_tiles + qtile) * p.cap;
       const int qf0 = g.q_tr_first[qtr];
       const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
-      // per-unit tables (slot U & 1), built ahead by the Q/K producer
-      const int tsl = U & 1;
       const uint32_t* info = info2 + tsl * kInfoCap;
       const float* kn2_s = kn2_2 + tsl * kInfoCap;
       const float* qn2_s = qn2_2 + tsl;
       const int* win = win2 + tsl * 32;
-      if (n > 0) {
-        mbar_wait(tab_full + tsl, (uint32_t)(U >> 1) & 1);
-        // this group's references (and their word minima) start at the unit's initial value
+      // this group's references (and their word minima) start at the unit's initial value;
+      // the epilogue of unit U - 2 (same slot) released them with the tables
+      float* cg_c = c_s + (tsl * 2 + grp) * 128;
+      const bool fixed_unit = c0_2[tsl] == 0.0f;  // references 0 for the whole unit
+      {
         const float c0v = c0_2[tsl];
         for (int i = wl * 32 + lane; i < NQ; i += WG * 32) cg_c[i] = c0v;
         if (wl == 0 && lane < Cfg::kCGg * kW) cmin_s[grp * Cfg::kCGg * kW + lane] = c0v;
         named_bar_sync(grp_bar, WG * 32);
       }
-      // query columns of this thread that are real tokens, as 32-column words
+      // query columns of this thread that are real tokens, as 32-column words: rows of the
+      // 8x8 tile below g.rows times columns left of g.cols (both frames of NQ = 128 alike)
       uint32_t qvalid[kW];
+      {
+        const int rv = min(8, g.rows - qh0), cv = min(8, g.cols - qw0);
+        const unsigned long long rowbits = (cv >= 8 ? 0xffull : ((1ull << cv) - 1ull)) * 0x0101010101010101ull;
+        const unsigned long long vm = rv >= 8 ? rowbits : (rowbits & ((1ull << (8 * rv)) - 1ull));
 #pragma unroll
-      for (int w = 0; w < kW; ++w) {
-        qvalid[w] = 0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int qc = (col0 + 32 * w + i) & 63;
-          if (qh0 + (qc >> 3) < g.rows && qw0 + (qc & 7) < g.cols) qvalid[w] |= 1u << i;
-        }
+        for (int w = 0; w < kW; ++w) qvalid[w] = (uint32_t)(vm >> (((col0 + 32 * w) & 63)));
       }
       uint32_t my_pairs = 0;  // <= tiles * CPT per thread per unit
       float lp[CPT];
@@ -719,6 +925,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         for (int w = 0; w < kW; ++w) my_pairs += __popc(mk[w]);
         any = true;
 
+        if (threadIdx.x == 0) trace_at(p, 6, G);
         mbar_wait(s_full + sb, (uint32_t)(G / kNS) & 1);
         tc_fence_after();
         if (threadIdx.x == 0) trace_at(p, 2, G);
@@ -739,6 +946,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           }
         }
         if (fast) {
+          // P buffer pb was last read by PV(G - NP) (kNP tiles back: normally long done), so
+          // each word's P^T is stored as soon as it is computed, under the next word's exps
+          if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
+          if (threadIdx.x == 0) trace_at(p, 9, G);
           uint32_t pk[CPT / 2];
 #pragma unroll
           for (int w = 0; w < kW; ++w) {
@@ -752,32 +963,35 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
               tmem_ld<32>(tS0 + sb * NQ + col0 + 32 * w + lane_off, reinterpret_cast<uint32_t*>(d));
               tc_wait_ld();
             }
+            if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
             if (mw == 0u) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) pk[16 * w + i] = 0u;
             } else {
+              if (fixed_unit && mw == 0xffffffffu) {
+                // references fixed at 0, every key allowed: d = s * scale * log2(e)
 #pragma unroll
-              for (int i = 0; i < 32; i += 4) {
-                const float4 c4 = *reinterpret_cast<const float4*>(cw + i);
-                d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
-                d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
-                d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
-                d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
+                for (int i = 0; i < 16; ++i) fmul2(d[2 * i], d[2 * i + 1], sl2);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  const float4 c4 = fixed_unit ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                               : *reinterpret_cast<const float4*>(cw + i);
+                  d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
+                  d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
+                  d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
+                  d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
+                }
               }
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 const float p0 = (kExp & 1) ? 1.0f : ex2(d[2 * i]), p1 = (kExp & 1) ? 1.0f : ex2(d[2 * i + 1]);
-                lp[32 * w + 2 * i] += p0;
-                lp[32 * w + 2 * i + 1] += p1;
+                fadd2(lp[32 * w + 2 * i], lp[32 * w + 2 * i + 1], p0, p1);
                 const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                 pk[16 * w + i] = *reinterpret_cast<const uint32_t*>(&h2);
               }
             }
-          }
-          // P buffer pb was last read by PV(G - NP)
-          if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
-#pragma unroll
-          for (int w = 0; w < kW; ++w) {
+            if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
             const int cwi = col0 + 32 * w;
             uint8_t* pw = prow + (cwi >> 6) * 16384;
             const int ch0 = (cwi & 63) >> 3;
@@ -931,7 +1145,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         if (threadIdx.x == 0) trace_at(p, 3, G);
       }
 
-      // ---- epilogue: per-group denominators, merge the groups, normalise, store --------
+      // ---- end of unit: this group's denominators -> the epilogue warpgroup -------------
+      if (threadIdx.x == 0) trace_at(p, 28, U);
       if (p.pairs) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
@@ -942,101 +1157,16 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       for (int i = 0; i < CPT / 32; ++i) cg_red[quarter * CPT + colreduce_col(CPT, lane, i)] = lp[i];
       named_bar_sync(bar_id, 128);
       if (quarter == 0) {
+        float* lg = l_s + (tsl * 2 + grp) * 128 + col0;
 #pragma unroll
         for (int i = 0; i < CPT / 32; ++i) {
           const int cc = lane + 32 * i;
-          l_s[grp * 128 + col0 + cc] =
-              any ? (cg_red[cc] + cg_red[CPT + cc]) + (cg_red[2 * CPT + cc] + cg_red[3 * CPT + cc]) : 0.0f;
+          lg[cc] = any ? (cg_red[cc] + cg_red[CPT + cc]) + (cg_red[2 * CPT + cc] + cg_red[3 * CPT + cc]) : 0.0f;
         }
+        named_bar_arrive(kStatBar0 + tsl, kStatCount);  // references (written by quarter 0) and l final
       }
-      named_bar_sync(kAllBar, SW * 32);
-      // merge factors per query column: f_g = 2^(c_g - c) / l, l = sum_g l_g 2^(c_g - c)
-      const int tid = threadIdx.x;
-      if (tid < NQ) {
-        float cmax = -INFINITY;
-#pragma unroll
-        for (int gi = 0; gi < kGroups; ++gi) cmax = fmaxf(cmax, c_s[gi * 128 + tid]);
-        float e[kGroups], l = 0.0f;
-#pragma unroll
-        for (int gi = 0; gi < kGroups; ++gi) {
-          const float lg = l_s[gi * 128 + tid];
-          e[gi] = lg > 0.0f ? ex2(c_s[gi * 128 + tid] - cmax) : 0.0f;
-          l += lg * e[gi];
-        }
-#pragma unroll
-        for (int gi = 0; gi < kGroups; ++gi) f_s[gi * 128 + tid] = l > 0.0f ? e[gi] / l : 0.0f;
-        const int qc = tid & 63;
-        const int qh = qh0 + (qc >> 3), qw = qw0 + (qc & 7);
-        if (n > 0 && qh < g.rows && qw < g.cols) {
-          const long long tq = g.q_frame_tok0[qf0 + (tid >> 6)] + (long long)qh * g.cols + qw;
-          if (tq >= p.row_begin && tq < p.row_end && !(l > 0.0f)) atomicOr(p.err, kErrDegenerate);
-        }
-      }
-      uint16_t* so = reinterpret_cast<uint16_t*>(sP);  // staged O tile [NQ][D] bf16
-      if (n > 0) {
-        // all PVs of this unit complete => every P^T buffer is free for staging
-        mbar_wait(o_full + ob, (uint32_t)(U >> 1) & 1);
-        tc_fence_after();
-      }
-      named_bar_sync(kAllBar, SW * 32);  // factors visible, staging buffer free
-      {
-        // warp w: TMEM lane quarter w % 4, query-column slice w / 4 of NQ / (SW / 4) columns
-        constexpr int kSl = NQ / (SW / 4);
-        const int c0 = (warp >> 2) * kSl;
-        if (n > 0) {
-          if (j < D) {
-            float acc[kSl];
-#pragma unroll
-            for (int i = 0; i < kSl; ++i) acc[i] = 0.0f;
-#pragma unroll
-            for (int gi = 0; gi < kGroups; ++gi) {
-              if (!(f_s[gi * 128 + c0] >= 0.0f)) continue;  // (always true; keeps the loop uniform)
-              uint32_t o[kSl];
-              tmem_ld<kSl>(tO0 + (gi * kOB + ob) * NQ + c0 + lane_off, o);
-              tc_wait_ld();
-#pragma unroll
-              for (int i = 0; i < kSl; ++i) {
-                const float f = f_s[gi * 128 + c0 + i];
-                if (f != 0.0f) acc[i] = fmaf(__uint_as_float(o[i]), f, acc[i]);
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < kSl; ++i) so[(c0 + i) * D + j] = __bfloat16_as_ushort(__float2bfloat16_rn(acc[i]));
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(o_empty + ob);
-        } else if (j < D) {
-#pragma unroll
-          for (int i = 0; i < kSl; ++i) so[(c0 + i) * D + j] = 0;
-        }
-      }
-      named_bar_sync(kAllBar, SW * 32);
-      constexpr int kChunks = D / 8;
-      if (p.out_tile_major) {
-        uint16_t* outu = p.out + u * NQ * D;
-        for (int idx = threadIdx.x; idx < NQ * kChunks; idx += SW * 32)
-          *reinterpret_cast<uint4*>(outu + idx * 8) = *reinterpret_cast<const uint4*>(so + idx * 8);
-      } else {
-        uint16_t* outh = p.out + head * p.out_head_stride;
-        for (int idx = threadIdx.x; idx < NQ * kChunks; idx += SW * 32) {
-          const int col = idx / kChunks, ch = idx % kChunks, qc = col & 63;
-          const int qh = qh0 + (qc >> 3), qw = qw0 + (qc & 7);
-          if (qh < g.rows && qw < g.cols) {
-            const long long tq = g.q_frame_tok0[qf0 + (col >> 6)] + (long long)qh * g.cols + qw;
-            uint4 val = make_uint4(0, 0, 0, 0);
-            if (tq >= p.row_begin && tq < p.row_end) val = *reinterpret_cast<const uint4*>(so + col * D + ch * 8);
-            *reinterpret_cast<uint4*>(outh + tq * D + ch * 8) = val;
-          }
-        }
-      }
-      named_bar_sync(kAllBar, SW * 32);  // staging buffer and per-unit tables reusable
-      if (n > 0 && lane == 0) mbar_arrive(tab_empty + tsl);
-      if (threadIdx.x == 0) trace_cta(p, 1 + U);
-      if (n > 0) {
-        T += n;
-        ++U;
-      }
+      if (threadIdx.x == 0) trace_at(p, 29, U);
+      T += n;
     }
   }
 
