@@ -463,7 +463,8 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
     if (const char* dbg = std::getenv("FVSR_ATTN_DEBUG")) p.debug = std::atoi(dbg);
   static long long* trace = nullptr;
   static int trace_calls = 0;
-  const bool tracing = kInstrument && std::getenv("FVSR_ATTN_TRACE") != nullptr && ++trace_calls == 20;
+  const bool tracing =
+      (kInstrument || kCtaTimeline) && std::getenv("FVSR_ATTN_TRACE") != nullptr && ++trace_calls == 20;
   if (tracing) {
     const size_t tn = kTraceEvents * kTraceTiles + 1024 * kTraceCtaSlots;
     if (!trace) cudaMalloc(&trace, tn * sizeof(long long));

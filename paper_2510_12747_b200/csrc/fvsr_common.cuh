@@ -201,6 +201,14 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
 __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* ptr) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(ptr)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_shared(uint32_t* ptr, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(ptr)), "r"(v) : "memory");
+}
 // Per-warpgroup register budget (all 4 warps of the warpgroup execute it).
 template <int N>
 __device__ __forceinline__ void reg_alloc() {

@@ -95,7 +95,12 @@ constexpr int kExp = FVSR_ATTN_EXP;
 #ifndef FVSR_POLY_EXP
 #define FVSR_POLY_EXP 0
 #endif
-constexpr bool kPolyExp = FVSR_POLY_EXP != 0;
+#ifndef FVSR_QK_LEAD
+#define FVSR_QK_LEAD 3
+#endif
+constexpr int kQkLead = FVSR_QK_LEAD;
+constexpr int kPolyN = FVSR_POLY_EXP;  // of every 8 exp pairs of an unmasked word, on the FMA pipe
+constexpr bool kPolyExp = kPolyN != 0;
 __device__ __forceinline__ void trace_at(const AttnParams& p, int ev, int G) {
   if (kInstrument && p.trace && blockIdx.x == 0 && G < kTraceTiles) p.trace[ev * kTraceTiles + G] = clock64();
 }
@@ -104,8 +109,12 @@ __device__ __forceinline__ long long globaltimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+#ifndef FVSR_CTA_TIMELINE
+#define FVSR_CTA_TIMELINE 0
+#endif
+constexpr bool kCtaTimeline = FVSR_CTA_TIMELINE != 0;  // per-CTA unit stamps only (cheap)
 __device__ __forceinline__ void trace_cta(const AttnParams& p, int slot) {
-  if (kInstrument && p.trace && slot < kTraceCtaSlots / 2) {
+  if ((kInstrument || kCtaTimeline) && p.trace && slot < kTraceCtaSlots / 2) {
     p.trace[kTraceEvents * kTraceTiles + blockIdx.x * kTraceCtaSlots + slot] = globaltimer();
     p.trace[kTraceEvents * kTraceTiles + blockIdx.x * kTraceCtaSlots + 8 + slot] = clock64();
   }
@@ -155,7 +164,7 @@ struct AttnCfg {
   // c0 [2] | cmin [2][CGg][CPT/32] | unit [2][4] i32
   static constexpr uint32_t kScratchUsed =
       256 + 4 * (512 + 256 + 512 + 256) + 4 * (2 * kCGg * 4 * kCPT) + 4 * 64 + 8 * 2 * 256 + 16 +
-      4 * (2 * kCGg * (kCPT / 32)) + 32;
+      4 * (2 * kCGg * (kCPT / 32)) + 32 + 8;
   static_assert(kScratchUsed <= kScratch, "scratch budget");
   static constexpr uint32_t kOffE = kOffS + kScratch;         // epilogue staging chunk
   static constexpr uint32_t kEpiBytes = 4096;
@@ -343,7 +352,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   uint64_t* o_empty = o_full + 2;
   uint64_t* tab_full = o_empty + 2;   // per-unit tables built (producer)
   uint64_t* tab_empty = tab_full + 2; // per-unit tables released (epilogue)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tab_empty + 2);
+  uint64_t* pv_iss = tab_empty + 2;   // [4] PV(G) issued (PV issuer), paces the QK issuer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_iss + 4);
   float* c_s = reinterpret_cast<float*>(scratch + 256);  // [unit parity][group][128] column references
   float* alpha_s = c_s + 512;                            // [group][128] rescale factors
   float* l_s = alpha_s + 256;                            // [unit parity][group][128] denominators
@@ -359,6 +369,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   float* c0_2 = qn2_2 + 2;
   float* cmin_s = c0_2 + 2;                                         // [2][CGg][CPT/32] min reference
   int* utab = reinterpret_cast<int*>(cmin_s + 2 * Cfg::kCGg * (CPT / 32));  // [2][4] n head qtr qtile
+  uint32_t* prog = reinterpret_cast<uint32_t*>(utab + 8);  // [0] QKs, [1] PVs known complete (count)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // named barriers: 1.. softmax column groups, 9/10 softmax groups, 12 epilogue warpgroup,
@@ -388,12 +399,15 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   if (threadIdx.x == 0) trace_cta(p, 0);
   if (warp == Cfg::kQkWarp) tmem_alloc(tmem_slot, Cfg::kTmemCols);
   if (threadIdx.x == 0) {
+    prog[0] = 0;
+    prog[1] = 0;
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int i = 0; i < kNS; ++i) { mbar_init(qk_go + i, WG + 1); mbar_init(s_full + i, 1); }
     for (int i = 0; i < kPB; ++i) { mbar_init(pv_go + i, WG + 1); mbar_init(pv_done + i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, 4); }
     for (int i = 0; i < 2; ++i) { mbar_init(tab_full + i, 1); mbar_init(tab_empty + i, 4); }
+    for (int i = 0; i < 4; ++i) mbar_init(pv_iss + i, 1);
 
     fence_barrier_init();
   }
@@ -672,7 +686,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         const TileMeta mt = bcast_meta(mine, t & 31);
         const int ks = T % kNK;
         // K stage ks is free once QK(T - NK) completed
-        if (T >= kNK) mbar_wait(s_full + (T - kNK) % kNS, (uint32_t)((T - kNK) / kNS) & 1);
+        if (T >= kNK) {
+          mbar_wait(s_full + (T - kNK) % kNS, (uint32_t)((T - kNK) / kNS) & 1);
+          if (lane == 0) st_release_shared(prog + 0, (uint32_t)(T - kNK + 1));  // QKs complete
+        }
         if (elect_one()) {
           if (((kInstrument && (p.debug & 2)) || (kExp & 16)) && T >= kNK) {  // experiment: no K traffic after the first stages
             mbar_arrive(qk_go + T % kNS);
@@ -704,7 +721,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         const TileMeta mt = bcast_meta(mine, t & 31);
         const int vs = T % kNV;
         // V stage vs is free once PV(T - NV) completed
-        if (T >= kNV) mbar_wait(pv_done + (T - kNV) % kPB, (uint32_t)((T - kNV) / kPB) & 1);
+        if (T >= kNV) {
+          mbar_wait(pv_done + (T - kNV) % kPB, (uint32_t)((T - kNV) / kPB) & 1);
+          if (lane == 0) st_release_shared(prog + 1, (uint32_t)(T - kNV + 1));  // PVs complete
+        }
         if (elect_one()) {
           if (((kInstrument && (p.debug & 2)) || (kExp & 16)) && T >= kNV) {
             mbar_arrive(pv_go + T % kPB);
@@ -733,6 +753,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       mbar_wait(q_full, U & 1);
       for (int t = 0; t < n; ++t, ++G) {
         if (lane == 0) trace_at(p, 18, G);
+        if (kQkLead > 0 && G >= kQkLead) mbar_wait(pv_iss + (G - kQkLead) % 4, (uint32_t)((G - kQkLead) / 4) & 1);
         mbar_wait(qk_go + sb, sph);
         if (lane == 0) trace_at(p, 19, G);
         tc_fence_after();
@@ -798,6 +819,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           trace_at(p, 14, G);
           tc_commit(pv_done + gb);
           if (t == n - 1) tc_commit(o_full + ob);
+          if (kQkLead > 0) mbar_arrive(pv_iss + G % 4);
           trace_at(p, 15, G);
         }
         __syncwarp();
@@ -874,11 +896,14 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       const int t_first = (grp - (T % kGroups) + kGroups) % kGroups;
       bool any = false;  // this group processed a tile of the unit (its O^T is defined)
 
+      auto info_at = [&](int tt) { return tt < kInfoCap ? info[tt] : tile_info(g, sel_at(sel, tt)); };
+      uint32_t inf_next = t_first < n ? info_at(t_first) : 0u;  // prefetched a tile ahead
       for (int t = t_first; t < n; t += kGroups) {
         const int G = T + t;
         const int sb = G % kNS, pb = G % kNP;
         // ---- key row j: validity and allowed-query mask over this thread's columns ----
-        const uint32_t inf = t < kInfoCap ? info[t] : tile_info(g, sel_at(sel, t));
+        const uint32_t inf = inf_next;
+        if (t + kGroups < n) inf_next = info_at(t + kGroups);
         const int kcnt = inf & 3, kf0 = (inf >> 2) & 63;
         const int kh = (int)((inf >> 8) & 0xfff) + ((j & 63) >> 3);
         const int kw = (int)(inf >> 20) + (j & 7);
@@ -925,10 +950,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         for (int w = 0; w < kW; ++w) my_pairs += __popc(mk[w]);
         any = true;
 
-        if (threadIdx.x == 0) trace_at(p, 6, G);
-        mbar_wait(s_full + sb, (uint32_t)(G / kNS) & 1);
-        tc_fence_after();
-        if (threadIdx.x == 0) trace_at(p, 2, G);
         // MN-major B operand: [NQ/64 groups][128 key rows][128 B], 16-B chunks swizzled by row
         uint8_t* prow = sP + pb * Cfg::kPBytes + j * 128;
         const float sl2 = p.scale_log2;
@@ -936,8 +957,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         // smallest reference, so no reference can need to move — no vote, no barrier, no
         // memory-clobbering asm between the words, so their loads and math interleave.  The
         // decision uses only shared inputs: all 4 warps of a column group take the same path.
+        // (Fixed-reference units: always.)
         bool fast = !(kExp & 4) && !(kInstrument && (p.debug & 1)) && t < kInfoCap;
-        if (fast) {
+        if (fast && !fixed_unit) {
           const float b2 = qn2_s[0] * kn2_s[t] * (sl2 * sl2) * 1.0002f;
 #pragma unroll
           for (int w = 0; w < kW; ++w) {
@@ -945,10 +967,18 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
             fast = fast && lim > 0.0f && b2 <= lim * lim;
           }
         }
+        // S(G) ready: the Q/K producer publishes the QKs it saw complete (it waits on them to
+        // recycle K stages, normally well before this tile), else wait on the barrier itself
+        if (threadIdx.x == 0) trace_at(p, 6, G);
+        if (ld_acquire_shared(prog + 0) <= (uint32_t)G) mbar_wait(s_full + sb, (uint32_t)(G / kNS) & 1);
+        tc_fence_after();
+        if (threadIdx.x == 0) trace_at(p, 2, G);
         if (fast) {
-          // P buffer pb was last read by PV(G - NP) (kNP tiles back: normally long done), so
-          // each word's P^T is stored as soon as it is computed, under the next word's exps
-          if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
+          // P buffer pb was last read by PV(G - NP) (kNP tiles back: normally long done, and
+          // published by the V producer, which waits on PVs to recycle V stages), so each
+          // word's P^T is stored as soon as it is computed, under the next word's exps
+          if (G >= kNP && ld_acquire_shared(prog + 1) <= (uint32_t)(G - kNP))
+            mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
           if (threadIdx.x == 0) trace_at(p, 9, G);
           uint32_t pk[CPT / 2];
 #pragma unroll
@@ -985,7 +1015,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
               }
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const float p0 = (kExp & 1) ? 1.0f : ex2(d[2 * i]), p1 = (kExp & 1) ? 1.0f : ex2(d[2 * i + 1]);
+                // kPolyN of every 8 pairs of an unmasked word on the FMA pipe (MUFU relief)
+                const bool poly = (i & 7) < kPolyN && mw == 0xffffffffu;
+                const float p0 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i]) : ex2(d[2 * i]));
+                const float p1 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i + 1]) : ex2(d[2 * i + 1]));
                 fadd2(lp[32 * w + 2 * i], lp[32 * w + 2 * i + 1], p0, p1);
                 const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                 pk[16 * w + i] = *reinterpret_cast<const uint32_t*>(&h2);
@@ -1106,7 +1139,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                   // every 4th pair of an unmasked word on the FMA pipe (balances MUFU and issue)
-                  const bool poly = kPolyExp && (i & 3) == 3 && mw == 0xffffffffu;
+                  const bool poly = (i & 7) < kPolyN && mw == 0xffffffffu;
                   const float p0 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i]) : ex2(d[2 * i]));
                   const float p1 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i + 1]) : ex2(d[2 * i + 1]));
                   lp[32 * w + 2 * i] += p0;

@@ -104,3 +104,28 @@ def test_ring_step_host_end_to_end():
         dev = ring2.attention(0, to_dev(q), [t], fv.Mask.all_allowed(), topk)
         ring2.evict(0)
         assert torch.equal(oh.cuda(), dev)
+
+
+# Shapes whose unit count leaves a partial last round of persistent CTAs on a 148-SM B200
+# (3 x 66 tiles = 198 units, 4 x 40 = 160), with fixed-reference and exact-path units.
+@pytest.mark.parametrize("heads,rows,cols,topk,qscale,mask", [
+    (3, 48, 88, 6, 1.0, None), (4, 40, 64, 5, 1.0, ("loc", 17, 25, True)), (4, 40, 64, 7, 4.0, None)])
+def test_partial_last_round_matches_oracle(heads, rows, cols, topk, qscale, mask):
+    d, window = 128, 3
+    n = rows * cols
+    fmask = fv.Mask.all_allowed() if mask is None else fv.Mask.locality(mask[1], mask[2], mask[3])
+    omask = oracle.Mask.all() if mask is None else oracle.Mask.locality(mask[1], mask[2], mask[3])
+    ring = fv.KVRing(1, heads, d, rows, cols, window)
+    ids, ctx_k, ctx_v = [], [], []
+    for t in range(window):
+        q, k, v = frame_data(300 + t, heads, n, d)
+        ring.append(0, t, to_dev(k), to_dev(v))
+        ids.append(t); ctx_k.append(k); ctx_v.append(v)
+    t = window - 1
+    q = oracle.bf16_round(frame_data(400, heads, n, d)[0] * np.float32(qscale))
+    out = ring.attention(0, to_dev(q), [t], fmask, topk).float().cpu().numpy()
+    K, V = np.concatenate(ctx_k, axis=1), np.concatenate(ctx_v, axis=1)
+    refs = oracle_plans(q, K, [t], ids, rows, cols, omask, topk)
+    ref = oracle_outs(q, K, V, [t], ids, rows, cols, omask, refs, oracle.head_scale(d))
+    assert rel_l2(out, ref) <= REL_L2_TOL, rel_l2(out, ref)
+    assert max_abs(out, ref) <= MAX_ABS_TOL, max_abs(out, ref)
