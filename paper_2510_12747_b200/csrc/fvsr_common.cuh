@@ -12,6 +12,7 @@
 // Row r of a frame-tile is spatial (8*th + r/8, 8*tw + r%8) of that frame.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>

@@ -870,7 +870,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       // this group's references (and their word minima) start at the unit's initial value;
       // the epilogue of unit U - 2 (same slot) released them with the tables
       float* cg_c = c_s + (tsl * 2 + grp) * 128;
-      const bool fixed_unit = c0_2[tsl] == 0.0f;  // references 0 for the whole unit
+      // references 0 for the whole unit (every tile of it then fits the bound: see the producer)
+      const bool fixed_unit = c0_2[tsl] == 0.0f && !(kInstrument && (p.debug & 1)) && !(kExp & 4);
       {
         const float c0v = c0_2[tsl];
         for (int i = wl * 32 + lane; i < NQ; i += WG * 32) cg_c[i] = c0v;
@@ -898,285 +899,292 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
 
       auto info_at = [&](int tt) { return tt < kInfoCap ? info[tt] : tile_info(g, sel_at(sel, tt)); };
       uint32_t inf_next = t_first < n ? info_at(t_first) : 0u;  // prefetched a tile ahead
-      for (int t = t_first; t < n; t += kGroups) {
-        const int G = T + t;
-        const int sb = G % kNS, pb = G % kNP;
-        // ---- key row j: validity and allowed-query mask over this thread's columns ----
-        const uint32_t inf = inf_next;
-        if (t + kGroups < n) inf_next = info_at(t + kGroups);
-        const int kcnt = inf & 3, kf0 = (inf >> 2) & 63;
-        const int kh = (int)((inf >> 8) & 0xfff) + ((j & 63) >> 3);
-        const int kw = (int)(inf >> 20) + (j & 7);
-        const bool kvalid = (j < 64 || kcnt == 2) && kh < g.rows && kw < g.cols;
-        uint32_t mk[kW];  // bit i of word w: (key j, column col0 + 32w + i) allowed
-#pragma unroll
-        for (int w = 0; w < kW; ++w) mk[w] = 0;
-        if (kvalid) {
-          if (MK == 0) {
-#pragma unroll
-            for (int w = 0; w < kW; ++w) mk[w] = qvalid[w];
-          } else if (MK == 1) {
-            uint32_t wb = 0, hb = 0;  // allowed query cols / rows of the 8x8 query tile
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              wb |= (kw >= win[16 + i] && kw < win[24 + i]) ? (1u << i) : 0u;
-              hb |= (kh >= win[i] && kh < win[8 + i]) ? (1u << i) : 0u;
-            }
-#pragma unroll
-            for (int w = 0; w < kW; ++w) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const int qc = (col0 + 32 * w + i) & 63;
-                if (((hb >> (qc >> 3)) & (wb >> (qc & 7)) & 1u) != 0u) mk[w] |= 1u << i;
+      // The tile loop, compiled twice: for fixed-reference units (references 0, every tile on
+      // the fast path: no vote, no rescale, no reference loads -- a compact hot loop) and for
+      // the general case.
+      auto tile_loop = [&](auto fixed_tag) {
+        constexpr bool kFixed = decltype(fixed_tag)::value;
+        for (int t = t_first; t < n; t += kGroups) {
+          const int G = T + t;
+          const int sb = G % kNS, pb = G % kNP;
+          // ---- key row j: validity and allowed-query mask over this thread's columns ----
+          const uint32_t inf = inf_next;
+          if (t + kGroups < n) inf_next = info_at(t + kGroups);
+          const int kcnt = inf & 3, kf0 = (inf >> 2) & 63;
+          const int kh = (int)((inf >> 8) & 0xfff) + ((j & 63) >> 3);
+          const int kw = (int)(inf >> 20) + (j & 7);
+          const bool kvalid = (j < 64 || kcnt == 2) && kh < g.rows && kw < g.cols;
+          uint32_t mk[kW];  // bit i of word w: (key j, column col0 + 32w + i) allowed
+  #pragma unroll
+          for (int w = 0; w < kW; ++w) mk[w] = 0;
+          if (kvalid) {
+            if (MK == 0) {
+  #pragma unroll
+              for (int w = 0; w < kW; ++w) mk[w] = qvalid[w];
+            } else if (MK == 1) {
+              uint32_t wb = 0, hb = 0;  // allowed query cols / rows of the 8x8 query tile
+  #pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                wb |= (kw >= win[16 + i] && kw < win[24 + i]) ? (1u << i) : 0u;
+                hb |= (kh >= win[i] && kh < win[8 + i]) ? (1u << i) : 0u;
               }
-              mk[w] &= qvalid[w];
-            }
-          } else {
-            const long long tk = g.k_frame_tok0[kf0 + (j >> 6)] + (long long)kh * g.cols + kw;
-#pragma unroll
-            for (int w = 0; w < kW; ++w) {
-#pragma unroll 4
-              for (int i = 0; i < 32; ++i) {
-                if (!((qvalid[w] >> i) & 1u)) continue;
-                const int col = col0 + 32 * w + i, qc = col & 63;
-                const long long tq =
-                    g.q_frame_tok0[qf0 + (col >> 6)] + (long long)(qh0 + (qc >> 3)) * g.cols + qw0 + (qc & 7);
-                if ((m.bits[tq * m.words_per_row + (tk >> 6)] >> (tk & 63)) & 1ull) mk[w] |= 1u << i;
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int w = 0; w < kW; ++w) my_pairs += __popc(mk[w]);
-        any = true;
-
-        // MN-major B operand: [NQ/64 groups][128 key rows][128 B], 16-B chunks swizzled by row
-        uint8_t* prow = sP + pb * Cfg::kPBytes + j * 128;
-        const float sl2 = p.scale_log2;
-        // Fast path: |q||k| bounds every score of the tile within kBoundSlack of each word's
-        // smallest reference, so no reference can need to move — no vote, no barrier, no
-        // memory-clobbering asm between the words, so their loads and math interleave.  The
-        // decision uses only shared inputs: all 4 warps of a column group take the same path.
-        // (Fixed-reference units: always.)
-        bool fast = !(kExp & 4) && !(kInstrument && (p.debug & 1)) && t < kInfoCap;
-        if (fast && !fixed_unit) {
-          const float b2 = qn2_s[0] * kn2_s[t] * (sl2 * sl2) * 1.0002f;
-#pragma unroll
-          for (int w = 0; w < kW; ++w) {
-            const float lim = kBoundSlack + cmin_s[(grp * Cfg::kCGg + cg) * kW + w];
-            fast = fast && lim > 0.0f && b2 <= lim * lim;
-          }
-        }
-        // S(G) ready: the Q/K producer publishes the QKs it saw complete (it waits on them to
-        // recycle K stages, normally well before this tile), else wait on the barrier itself
-        if (threadIdx.x == 0) trace_at(p, 6, G);
-        if (ld_acquire_shared(prog + 0) <= (uint32_t)G) mbar_wait(s_full + sb, (uint32_t)(G / kNS) & 1);
-        tc_fence_after();
-        if (threadIdx.x == 0) trace_at(p, 2, G);
-        if (fast) {
-          // P buffer pb was last read by PV(G - NP) (kNP tiles back: normally long done, and
-          // published by the V producer, which waits on PVs to recycle V stages), so each
-          // word's P^T is stored as soon as it is computed, under the next word's exps
-          if (G >= kNP && ld_acquire_shared(prog + 1) <= (uint32_t)(G - kNP))
-            mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
-          if (threadIdx.x == 0) trace_at(p, 9, G);
-          uint32_t pk[CPT / 2];
-#pragma unroll
-          for (int w = 0; w < kW; ++w) {
-            const uint32_t mw = mk[w];
-            const float* cw = cg_c + col0 + 32 * w;
-            float d[32];
-            if (kExp & 2) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
-            } else {
-              tmem_ld<32>(tS0 + sb * NQ + col0 + 32 * w + lane_off, reinterpret_cast<uint32_t*>(d));
-              tc_wait_ld();
-            }
-            if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
-            if (mw == 0u) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) pk[16 * w + i] = 0u;
-            } else {
-              if (fixed_unit && mw == 0xffffffffu) {
-                // references fixed at 0, every key allowed: d = s * scale * log2(e)
-#pragma unroll
-                for (int i = 0; i < 16; ++i) fmul2(d[2 * i], d[2 * i + 1], sl2);
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                  const float4 c4 = fixed_unit ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                               : *reinterpret_cast<const float4*>(cw + i);
-                  d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
-                  d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
-                  d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
-                  d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
-                }
-              }
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                // kPolyN of every 8 pairs of an unmasked word on the FMA pipe (MUFU relief)
-                const bool poly = (i & 7) < kPolyN && mw == 0xffffffffu;
-                const float p0 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i]) : ex2(d[2 * i]));
-                const float p1 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i + 1]) : ex2(d[2 * i + 1]));
-                fadd2(lp[32 * w + 2 * i], lp[32 * w + 2 * i + 1], p0, p1);
-                const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                pk[16 * w + i] = *reinterpret_cast<const uint32_t*>(&h2);
-              }
-            }
-            if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
-            const int cwi = col0 + 32 * w;
-            uint8_t* pw = prow + (cwi >> 6) * 16384;
-            const int ch0 = (cwi & 63) >> 3;
-#pragma unroll
-            for (int c8 = 0; c8 < 4; ++c8)
-              *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
-                  make_uint4(pk[16 * w + 4 * c8], pk[16 * w + 4 * c8 + 1], pk[16 * w + 4 * c8 + 2],
-                             pk[16 * w + 4 * c8 + 3]);
-          }
-        } else {
-          // Columns in 32-wide words: each word is loaded, exponentiated and stored on its own
-          // (32 live scores per thread); its columns have their own references and vote.
   #pragma unroll
-          for (int w = 0; w < kW; ++w) {
-            const int cw = col0 + 32 * w;                // first column of the word
-            const uint32_t tS = tS0 + sb * NQ + cw + lane_off;
-            float d[32];  // scores -> exponents -> probabilities
-            if (kExp & 2) {
-  #pragma unroll
-              for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
-            } else {
-              tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
-              tc_wait_ld();
-            }
-            if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
-            uint32_t pk[16];
-            if (kInstrument && (p.debug & 1)) {  // experiment: no softmax math
-  #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = 0x3f803f80u;  // bf16 pair (1, 1)
-  #pragma unroll
-              for (int i = 0; i < 32; ++i) lp[32 * w + i] += 1.0f;
-            } else {
-              // d = s*scale*log2(e) - c (one FFMA; c = -inf before a column's first key gives
-              // +inf, which forces the exact path); masked entries -> -inf (ex2 -> 0).  The mask
-              // word is warp-uniform except on ragged edge tiles: all-allowed / none / mixed.
-              const uint32_t mw = mk[w];
-              if (mw == 0xffffffffu) {
-  #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                  const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
-                  d[i] = fmaf(d[i], sl2, -c4.x);
-                  d[i + 1] = fmaf(d[i + 1], sl2, -c4.y);
-                  d[i + 2] = fmaf(d[i + 2], sl2, -c4.z);
-                  d[i + 3] = fmaf(d[i + 3], sl2, -c4.w);
-                }
-              } else if (mw == 0u) {
-  #pragma unroll
-                for (int i = 0; i < 32; ++i) d[i] = -INFINITY;
-              } else {
-  #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                  const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
-                  d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
-                  d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
-                  d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
-                  d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
-                }
-              }
-              const bool need = (kExp & 4) ? (t < kGroups)
-                                           : bar_red_or(bar_id, 128, mw != 0u && tree_max<32>(d) > kRescaleThreshold);
-              if (threadIdx.x == 0) trace_at(p, 21 + 4 * w, G);
-              if (need) {
-                // exact column max of this tile over the group's 128 key rows, from the raw scores
-                tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
-                tc_wait_ld();
-  #pragma unroll
-                for (int i = 0; i < 32; ++i) d[i] = ((mk[w] >> i) & 1u) ? d[i] * sl2 : -INFINITY;
-                warp_colreduce<32, true>(d, lane);
-                cg_red[quarter * 32 + lane] = d[0];
-                named_bar_sync(bar_id, 128);
-                if (quarter == 0) {
-                  const float mx = fmaxf(fmaxf(cg_red[lane], cg_red[32 + lane]), fmaxf(cg_red[64 + lane], cg_red[96 + lane]));
-                  const float cold = cg_c[cw + lane];
-                  const float nw = fmaxf(cold, mx);
-                  cg_c[cw + lane] = nw;
-                  cg_a[cw + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
-                  float mn = nw;
-  #pragma unroll
-                  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                  if (lane == 0) cmin_s[(grp * Cfg::kCGg + cg) * kW + w] = mn;
-                }
-                named_bar_sync(bar_id, 128);
-                tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
-                tc_wait_ld();
+              for (int w = 0; w < kW; ++w) {
   #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                  lp[32 * w + i] *= cg_a[cw + i];
-                  d[i] = ((mk[w] >> i) & 1u) ? fmaf(d[i], sl2, -cg_c[cw + i]) : -INFINITY;
+                  const int qc = (col0 + 32 * w + i) & 63;
+                  if (((hb >> (qc >> 3)) & (wb >> (qc & 7)) & 1u) != 0u) mk[w] |= 1u << i;
                 }
-                if (t >= kGroups) {
-                  // O^T holds this group's PVs of the unit: wait for its last one, rescale columns
-                  const int Gp = G - kGroups;
-                  mbar_wait(pv_done + Gp % kPB, (uint32_t)(Gp / kPB) & 1);
-                  tc_fence_after();
-                  if (j < D) {
-                    uint32_t o[32];
-                    tmem_ld<32>(tO + cw + lane_off, o);
-                    tc_wait_ld();
+                mk[w] &= qvalid[w];
+              }
+            } else {
+              const long long tk = g.k_frame_tok0[kf0 + (j >> 6)] + (long long)kh * g.cols + kw;
   #pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * cg_a[cw + i]);
-                    tmem_st<32>(tO + cw + lane_off, o);
-                    tc_wait_st();
-                  }
+              for (int w = 0; w < kW; ++w) {
+  #pragma unroll 4
+                for (int i = 0; i < 32; ++i) {
+                  if (!((qvalid[w] >> i) & 1u)) continue;
+                  const int col = col0 + 32 * w + i, qc = col & 63;
+                  const long long tq =
+                      g.q_frame_tok0[qf0 + (col >> 6)] + (long long)(qh0 + (qc >> 3)) * g.cols + qw0 + (qc & 7);
+                  if ((m.bits[tq * m.words_per_row + (tk >> 6)] >> (tk & 63)) & 1ull) mk[w] |= 1u << i;
                 }
               }
-              if (threadIdx.x == 0) trace_at(p, 7, G);
-              // ---- P^T row j (bf16) and partial denominators (fp32) -------------------------
-              if (mw == 0u) {  // key row j of this tile is padding / masked for every column
+            }
+          }
   #pragma unroll
-                for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          for (int w = 0; w < kW; ++w) my_pairs += __popc(mk[w]);
+          any = true;
+
+          // MN-major B operand: [NQ/64 groups][128 key rows][128 B], 16-B chunks swizzled by row
+          uint8_t* prow = sP + pb * Cfg::kPBytes + j * 128;
+          const float sl2 = p.scale_log2;
+          // Fast path: |q||k| bounds every score of the tile within kBoundSlack of each word's
+          // smallest reference, so no reference can need to move — no vote, no barrier, no
+          // memory-clobbering asm between the words, so their loads and math interleave.  The
+          // decision uses only shared inputs: all 4 warps of a column group take the same path.
+          // (Fixed-reference units: always.)
+          bool fast = kFixed || (!(kExp & 4) && !(kInstrument && (p.debug & 1)) && t < kInfoCap);
+          if (!kFixed && fast) {
+            const float b2 = qn2_s[0] * kn2_s[t] * (sl2 * sl2) * 1.0002f;
+  #pragma unroll
+            for (int w = 0; w < kW; ++w) {
+              const float lim = kBoundSlack + cmin_s[(grp * Cfg::kCGg + cg) * kW + w];
+              fast = fast && lim > 0.0f && b2 <= lim * lim;
+            }
+          }
+          // S(G) ready: the Q/K producer publishes the QKs it saw complete (it waits on them to
+          // recycle K stages, normally well before this tile), else wait on the barrier itself
+          if (threadIdx.x == 0) trace_at(p, 6, G);
+          if (ld_acquire_shared(prog + 0) <= (uint32_t)G) mbar_wait(s_full + sb, (uint32_t)(G / kNS) & 1);
+          tc_fence_after();
+          if (threadIdx.x == 0) trace_at(p, 2, G);
+          if (fast) {
+            // P buffer pb was last read by PV(G - NP) (kNP tiles back: normally long done, and
+            // published by the V producer, which waits on PVs to recycle V stages), so each
+            // word's P^T is stored as soon as it is computed, under the next word's exps
+            if (G >= kNP && ld_acquire_shared(prog + 1) <= (uint32_t)(G - kNP))
+              mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
+            if (threadIdx.x == 0) trace_at(p, 9, G);
+            uint32_t pk[CPT / 2];
+  #pragma unroll
+            for (int w = 0; w < kW; ++w) {
+              const uint32_t mw = mk[w];
+              const float* cw = cg_c + col0 + 32 * w;
+              float d[32];
+              if (kExp & 2) {
+  #pragma unroll
+                for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
               } else {
+                tmem_ld<32>(tS0 + sb * NQ + col0 + 32 * w + lane_off, reinterpret_cast<uint32_t*>(d));
+                tc_wait_ld();
+              }
+              if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
+              if (mw == 0u) {
+  #pragma unroll
+                for (int i = 0; i < 16; ++i) pk[16 * w + i] = 0u;
+              } else {
+                if (kFixed && mw == 0xffffffffu) {
+                  // references fixed at 0, every key allowed: d = s * scale * log2(e)
+  #pragma unroll
+                  for (int i = 0; i < 16; ++i) fmul2(d[2 * i], d[2 * i + 1], sl2);
+                } else {
+  #pragma unroll
+                  for (int i = 0; i < 32; i += 4) {
+                    const float4 c4 = kFixed ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                 : *reinterpret_cast<const float4*>(cw + i);
+                    d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
+                    d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
+                    d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
+                    d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
+                  }
+                }
   #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                  // every 4th pair of an unmasked word on the FMA pipe (balances MUFU and issue)
+                  // kPolyN of every 8 pairs of an unmasked word on the FMA pipe (MUFU relief)
                   const bool poly = (i & 7) < kPolyN && mw == 0xffffffffu;
                   const float p0 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i]) : ex2(d[2 * i]));
                   const float p1 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i + 1]) : ex2(d[2 * i + 1]));
-                  lp[32 * w + 2 * i] += p0;
-                  lp[32 * w + 2 * i + 1] += p1;
+                  fadd2(lp[32 * w + 2 * i], lp[32 * w + 2 * i + 1], p0, p1);
                   const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                  pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
+                  pk[16 * w + i] = *reinterpret_cast<const uint32_t*>(&h2);
                 }
               }
               if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
-            }
-            if (w == 0) {
-              if (threadIdx.x == 0) trace_at(p, 8, G);
-              // P buffer pb was last read by PV(G - NP)
-              if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
-              if (threadIdx.x == 0) trace_at(p, 9, G);
-            }
-            uint8_t* pw = prow + (cw >> 6) * 16384;
-            const int ch0 = (cw & 63) >> 3;
+              const int cwi = col0 + 32 * w;
+              uint8_t* pw = prow + (cwi >> 6) * 16384;
+              const int ch0 = (cwi & 63) >> 3;
   #pragma unroll
-            for (int c8 = 0; c8 < 4; ++c8)
-              *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
-                  make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
-            if (threadIdx.x == 0) trace_at(p, 23 + 4 * w, G);
+              for (int c8 = 0; c8 < 4; ++c8)
+                *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
+                    make_uint4(pk[16 * w + 4 * c8], pk[16 * w + 4 * c8 + 1], pk[16 * w + 4 * c8 + 2],
+                               pk[16 * w + 4 * c8 + 3]);
+            }
+          } else {
+            // Columns in 32-wide words: each word is loaded, exponentiated and stored on its own
+            // (32 live scores per thread); its columns have their own references and vote.
+    #pragma unroll
+            for (int w = 0; w < kW; ++w) {
+              const int cw = col0 + 32 * w;                // first column of the word
+              const uint32_t tS = tS0 + sb * NQ + cw + lane_off;
+              float d[32];  // scores -> exponents -> probabilities
+              if (kExp & 2) {
+    #pragma unroll
+                for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
+              } else {
+                tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+                tc_wait_ld();
+              }
+              if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
+              uint32_t pk[16];
+              if (kInstrument && (p.debug & 1)) {  // experiment: no softmax math
+    #pragma unroll
+                for (int i = 0; i < 16; ++i) pk[i] = 0x3f803f80u;  // bf16 pair (1, 1)
+    #pragma unroll
+                for (int i = 0; i < 32; ++i) lp[32 * w + i] += 1.0f;
+              } else {
+                // d = s*scale*log2(e) - c (one FFMA; c = -inf before a column's first key gives
+                // +inf, which forces the exact path); masked entries -> -inf (ex2 -> 0).  The mask
+                // word is warp-uniform except on ragged edge tiles: all-allowed / none / mixed.
+                const uint32_t mw = mk[w];
+                if (mw == 0xffffffffu) {
+    #pragma unroll
+                  for (int i = 0; i < 32; i += 4) {
+                    const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
+                    d[i] = fmaf(d[i], sl2, -c4.x);
+                    d[i + 1] = fmaf(d[i + 1], sl2, -c4.y);
+                    d[i + 2] = fmaf(d[i + 2], sl2, -c4.z);
+                    d[i + 3] = fmaf(d[i + 3], sl2, -c4.w);
+                  }
+                } else if (mw == 0u) {
+    #pragma unroll
+                  for (int i = 0; i < 32; ++i) d[i] = -INFINITY;
+                } else {
+    #pragma unroll
+                  for (int i = 0; i < 32; i += 4) {
+                    const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
+                    d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
+                    d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
+                    d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
+                    d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
+                  }
+                }
+                const bool need = (kExp & 4) ? (t < kGroups)
+                                             : bar_red_or(bar_id, 128, mw != 0u && tree_max<32>(d) > kRescaleThreshold);
+                if (threadIdx.x == 0) trace_at(p, 21 + 4 * w, G);
+                if (need) {
+                  // exact column max of this tile over the group's 128 key rows, from the raw scores
+                  tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+                  tc_wait_ld();
+    #pragma unroll
+                  for (int i = 0; i < 32; ++i) d[i] = ((mk[w] >> i) & 1u) ? d[i] * sl2 : -INFINITY;
+                  warp_colreduce<32, true>(d, lane);
+                  cg_red[quarter * 32 + lane] = d[0];
+                  named_bar_sync(bar_id, 128);
+                  if (quarter == 0) {
+                    const float mx = fmaxf(fmaxf(cg_red[lane], cg_red[32 + lane]), fmaxf(cg_red[64 + lane], cg_red[96 + lane]));
+                    const float cold = cg_c[cw + lane];
+                    const float nw = fmaxf(cold, mx);
+                    cg_c[cw + lane] = nw;
+                    cg_a[cw + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
+                    float mn = nw;
+    #pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    if (lane == 0) cmin_s[(grp * Cfg::kCGg + cg) * kW + w] = mn;
+                  }
+                  named_bar_sync(bar_id, 128);
+                  tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+                  tc_wait_ld();
+    #pragma unroll
+                  for (int i = 0; i < 32; ++i) {
+                    lp[32 * w + i] *= cg_a[cw + i];
+                    d[i] = ((mk[w] >> i) & 1u) ? fmaf(d[i], sl2, -cg_c[cw + i]) : -INFINITY;
+                  }
+                  if (t >= kGroups) {
+                    // O^T holds this group's PVs of the unit: wait for its last one, rescale columns
+                    const int Gp = G - kGroups;
+                    mbar_wait(pv_done + Gp % kPB, (uint32_t)(Gp / kPB) & 1);
+                    tc_fence_after();
+                    if (j < D) {
+                      uint32_t o[32];
+                      tmem_ld<32>(tO + cw + lane_off, o);
+                      tc_wait_ld();
+    #pragma unroll
+                      for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * cg_a[cw + i]);
+                      tmem_st<32>(tO + cw + lane_off, o);
+                      tc_wait_st();
+                    }
+                  }
+                }
+                if (threadIdx.x == 0) trace_at(p, 7, G);
+                // ---- P^T row j (bf16) and partial denominators (fp32) -------------------------
+                if (mw == 0u) {  // key row j of this tile is padding / masked for every column
+    #pragma unroll
+                  for (int i = 0; i < 16; ++i) pk[i] = 0u;
+                } else {
+    #pragma unroll
+                  for (int i = 0; i < 16; ++i) {
+                    // every 4th pair of an unmasked word on the FMA pipe (balances MUFU and issue)
+                    const bool poly = (i & 7) < kPolyN && mw == 0xffffffffu;
+                    const float p0 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i]) : ex2(d[2 * i]));
+                    const float p1 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i + 1]) : ex2(d[2 * i + 1]));
+                    lp[32 * w + 2 * i] += p0;
+                    lp[32 * w + 2 * i + 1] += p1;
+                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                    pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
+                  }
+                }
+                if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
+              }
+              if (w == 0) {
+                if (threadIdx.x == 0) trace_at(p, 8, G);
+                // P buffer pb was last read by PV(G - NP)
+                if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
+                if (threadIdx.x == 0) trace_at(p, 9, G);
+              }
+              uint8_t* pw = prow + (cw >> 6) * 16384;
+              const int ch0 = (cw & 63) >> 3;
+    #pragma unroll
+              for (int c8 = 0; c8 < 4; ++c8)
+                *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
+                    make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+              if (threadIdx.x == 0) trace_at(p, 23 + 4 * w, G);
+            }
           }
+          // S buffer free for QK(G + NS); P(G) visible to the tensor core
+          tc_fence_before();
+          if (threadIdx.x == 0) trace_at(p, 10, G);
+          fence_proxy_async_smem();
+          if (threadIdx.x == 0) trace_at(p, 11, G);
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(qk_go + sb);
+            mbar_arrive(pv_go + G % kPB);
+          }
+          if (threadIdx.x == 0) trace_at(p, 3, G);
         }
-        // S buffer free for QK(G + NS); P(G) visible to the tensor core
-        tc_fence_before();
-        if (threadIdx.x == 0) trace_at(p, 10, G);
-        fence_proxy_async_smem();
-        if (threadIdx.x == 0) trace_at(p, 11, G);
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(qk_go + sb);
-          mbar_arrive(pv_go + G % kPB);
-        }
-        if (threadIdx.x == 0) trace_at(p, 3, G);
-      }
+      };
+      if (fixed_unit) tile_loop(std::true_type{}); else tile_loop(std::false_type{});
 
       // ---- end of unit: this group's denominators -> the epilogue warpgroup -------------
       if (threadIdx.x == 0) trace_at(p, 28, U);
