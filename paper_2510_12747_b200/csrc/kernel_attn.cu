@@ -164,7 +164,7 @@ struct AttnCfg {
   // c0 [2] | cmin [2][CGg][CPT/32] | unit [2][4] i32
   static constexpr uint32_t kScratchUsed =
       256 + 4 * (512 + 256 + 512 + 256) + 4 * (2 * kCGg * 4 * kCPT) + 4 * 64 + 8 * 2 * 256 + 16 +
-      4 * (2 * kCGg * (kCPT / 32)) + 32 + 8;
+      4 * (2 * kCGg * (kCPT / 32)) + 32 + 8 + 16;
   static_assert(kScratchUsed <= kScratch, "scratch budget");
   static constexpr uint32_t kOffE = kOffS + kScratch;         // epilogue staging chunk
   static constexpr uint32_t kEpiBytes = 4096;
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   //   pv_go[G % PB]   V(G) landed (V producer expect_tx + TMA bytes) and P(G) written
   //   pv_done[G % PB] PV(G) complete (commit); frees V stage and P buffer
   //   o_full / o_empty  per unit: all PVs done / epilogue read O
-  //   tab_full / tab_empty  per-unit tables built (producer) / released (epilogue)
+  //   tab_full[U & 1]  per-unit tables built (epilogue warpgroup, a unit ahead)
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* qk_go = bars + 2;
@@ -351,15 +351,14 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   uint64_t* o_full = pv_done + kPB;
   uint64_t* o_empty = o_full + 2;
   uint64_t* tab_full = o_empty + 2;   // per-unit tables built (producer)
-  uint64_t* tab_empty = tab_full + 2; // per-unit tables released (epilogue)
-  uint64_t* pv_iss = tab_empty + 2;   // [4] PV(G) issued (PV issuer), paces the QK issuer
+  uint64_t* pv_iss = tab_full + 2;    // [4] PV(G) issued (PV issuer), paces the QK issuer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_iss + 4);
   float* c_s = reinterpret_cast<float*>(scratch + 256);  // [unit parity][group][128] column references
   float* alpha_s = c_s + 512;                            // [group][128] rescale factors
   float* l_s = alpha_s + 256;                            // [unit parity][group][128] denominators
   float* f_s = l_s + 512;                                // [group][128] merge factors (incl. 1/l)
   float* red = f_s + 256;                                // [2][CGg][4][CPT] cross-quarter partials
-  // Per-unit tables, double-buffered by unit parity and built ahead by the Q/K producer:
+  // Per-unit tables, double-buffered by unit parity and built a unit ahead by the epilogue warpgroup:
   // locality windows [2][32], tile infos [2][kInfoCap], key-norm bounds [2][kInfoCap],
   // query-norm bound [2], initial reference [2]
   int* win2 = reinterpret_cast<int*>(red + 2 * Cfg::kCGg * 4 * CPT);
@@ -370,6 +369,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   float* cmin_s = c0_2 + 2;                                         // [2][CGg][CPT/32] min reference
   int* utab = reinterpret_cast<int*>(cmin_s + 2 * Cfg::kCGg * (CPT / 32));  // [2][4] n head qtr qtile
   uint32_t* prog = reinterpret_cast<uint32_t*>(utab + 8);  // [0] QKs, [1] PVs known complete (count)
+  float* kmx = reinterpret_cast<float*>(prog + 2);          // [4] table builder's warp maxima
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // named barriers: 1.. softmax column groups, 9/10 softmax groups, 12 epilogue warpgroup,
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     for (int i = 0; i < kNS; ++i) { mbar_init(qk_go + i, WG + 1); mbar_init(s_full + i, 1); }
     for (int i = 0; i < kPB; ++i) { mbar_init(pv_go + i, WG + 1); mbar_init(pv_done + i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, 4); }
-    for (int i = 0; i < 2; ++i) { mbar_init(tab_full + i, 1); mbar_init(tab_empty + i, 4); }
+    for (int i = 0; i < 2; ++i) mbar_init(tab_full + i, 1);
     for (int i = 0; i < 4; ++i) mbar_init(pv_iss + i, 1);
 
     fence_barrier_init();
@@ -463,6 +463,90 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   // O = sum_g 2^(c_g - c) O_g / sum_g 2^(c_g - c) l_g, and store bf16 rows straight from
   // registers (lane pairs swap one value so each lane writes a 2-channel word).  Runs beside
   // the softmax warps, which move on to the next unit at once.
+  // Per-unit tables for the softmax warps (slot U & 1), built by the epilogue warpgroup a
+  // whole unit ahead: tile geometry, key-norm bounds, query-norm bound, initial reference,
+  // locality windows, and the unit descriptor (n < 0 ends the stream).
+  auto build_tables = [&](int sl, long long u, int n, int head, int qtr, int qtile, const int* sel) {
+    const int et = threadIdx.x - Cfg::kEpiWarp * 32;
+    constexpr int kEpiBar = 12;
+    uint32_t* info = info2 + sl * kInfoCap;
+    float* kn2_s = kn2_2 + sl * kInfoCap;
+    float kmax = 0.0f;
+    for (int i = et; i < min(n, kInfoCap); i += 128) {
+      const int kb = sel_at(sel, i);
+      info[i] = tile_info(g, kb);
+      float kn = INFINITY;
+      if (p.kn2) {
+        const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles, kf = g.k_tr_first[ktr];
+        const float* kh = p.kn2 + head * p.kn2_head_stride + ktile;
+        kn = kh[(long long)g.k_slot[kf] * g.n_tiles];
+        if (g.k_tr_count[ktr] == 2) kn = fmaxf(kn, kh[(long long)g.k_slot[kf + 1] * g.n_tiles]);
+      }
+      kn2_s[i] = kn;
+      kmax = fmaxf(kmax, kn);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    if (lane == 0) kmx[warp & 3] = kmax;
+    if (MK == 1 && et < 8) {
+      const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
+      int lo, hi;
+      locality_range(m.mode, qh0 + et, m.extent_h, g.rows, lo, hi);
+      win2[sl * 32 + et] = lo;
+      win2[sl * 32 + 8 + et] = hi;
+      locality_range(m.mode, qw0 + et, m.extent_w, g.cols, lo, hi);
+      win2[sl * 32 + 16 + et] = lo;
+      win2[sl * 32 + 24 + et] = hi;
+    }
+    named_bar_sync(kEpiBar, 128);
+    if (et == 0) {
+      kmax = fmaxf(fmaxf(kmx[0], kmx[1]), fmaxf(kmx[2], kmx[3]));
+      float qn = INFINITY;
+      if (p.qn2) {
+        qn = 0.0f;
+        for (int f = 0; f < g.q_tr_count[qtr]; ++f)
+          qn = fmaxf(qn, p.qn2[head * p.qn2_head_stride + (long long)(g.q_tr_first[qtr] + f) * g.n_tiles + qtile]);
+      }
+      // Fixed-reference mode: when |q||k| bounds every score of the unit by kFixedBound (log2
+      // units), the references start at 0 and never move: p = 2^(s*scale*log2e) stays in
+      // [2^-kFixedBound, 2^kFixedBound] (no overflow, no underflow), every tile takes the
+      // barrier-free fast path and no first tile needs an exact column max.  Otherwise the
+      // references start at -inf (exact lazy-rescale path).
+      const float b2 = qn * kmax * (p.scale_log2 * p.scale_log2) * 1.0002f;
+      const bool fixed = FVSR_FIXED_REF && n <= kInfoCap && b2 <= kFixedBound * kFixedBound;
+      utab[sl * 4 + 0] = n;
+      utab[sl * 4 + 1] = head;
+      utab[sl * 4 + 2] = qtr;
+      utab[sl * 4 + 3] = qtile;
+      qn2_2[sl] = qn;
+      c0_2[sl] = ((kInstrument && (p.debug & 1)) || fixed) ? 0.0f : -INFINITY;
+      mbar_arrive(tab_full + sl);
+    }
+  };
+  // next unit with work at or after item index k (returns the item index, or -1)
+  auto next_work = [&](int k, long long& u, int& head, int& qtr, int& qtile, int& n, const int*& sel) -> int {
+    for (;; ++k) {
+      if ((long long)blockIdx.x + (long long)k * gridDim.x >= n_units) return -1;
+      u = blockIdx.x + (long long)k * gridDim.x;
+      decode(u, head, qtr, qtile, n, sel);
+      if (n > 0) return k;
+    }
+  };
+  // tables of the work unit after item k into slot sl (or the end-of-stream entry)
+  auto build_next = [&](int sl, int& k) {
+    long long u;
+    int head, qtr, qtile, n;
+    const int* sel;
+    k = k < 0 ? -1 : next_work(k, u, head, qtr, qtile, n, sel);
+    if (k >= 0) {
+      build_tables(sl, u, n, head, qtr, qtile, sel);
+      ++k;
+    } else if (threadIdx.x == Cfg::kEpiWarp * 32) {
+      utab[sl * 4] = -1;
+      mbar_arrive(tab_full + sl);
+    }
+  };
+
   auto epilogue_warps = [&]() {
     const int q4 = warp & 3;                   // TMEM lane quarter = channel rows 32*q4..
     const int et = threadIdx.x - Cfg::kEpiWarp * 32;
@@ -471,6 +555,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     constexpr int kEpiBar = 12;
     constexpr int kEC = Cfg::kEpiCols;
     uint16_t* stage = reinterpret_cast<uint16_t*>(smem + Cfg::kOffE);  // [kEC][D] bf16
+    int kb = 0;  // item index from which the next table is searched (-1: stream ended)
+    build_next(0, kb);
+    build_next(1, kb);
     int U = 0;
     for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
       int head, qtr, qtile, n;
@@ -579,7 +666,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty + par);   // O^T buffers of this parity free for unit U + 2
-      if (lane == 0) mbar_arrive(tab_empty + par); // tables and c / l slots reusable (f is ours)
+      // slot par (tables, c, l) is free: the softmax finished unit U; build unit U + 2's tables
+      named_bar_sync(kEpiBar, 128);
+      build_next(par, kb);
       if (et == 0) trace_at(p, 32, U);
       if (et == 0) trace_cta(p, 1 + U);
       ++U;
@@ -598,62 +687,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       const int* sel;
       decode(u, head, qtr, qtile, n, sel);
       if (n == 0) continue;
-      // ---- per-unit tables for the softmax warps (slot U & 1) --------------------------
-      {
-        if (U >= 2) mbar_wait(tab_empty + (U & 1), ((U >> 1) - 1) & 1);
-        const int sl = U & 1;
-        uint32_t* info = info2 + sl * kInfoCap;
-        float* kn2_s = kn2_2 + sl * kInfoCap;
-        float kmax = 0.0f;
-        for (int i = lane; i < min(n, kInfoCap); i += 32) {
-          const int kb = sel_at(sel, i);
-          info[i] = tile_info(g, kb);
-          float kn = INFINITY;
-          if (p.kn2) {
-            const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles, kf = g.k_tr_first[ktr];
-            const float* kh = p.kn2 + head * p.kn2_head_stride + ktile;
-            kn = kh[(long long)g.k_slot[kf] * g.n_tiles];
-            if (g.k_tr_count[ktr] == 2) kn = fmaxf(kn, kh[(long long)g.k_slot[kf + 1] * g.n_tiles]);
-          }
-          kn2_s[i] = kn;
-          kmax = fmaxf(kmax, kn);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-        float qn = INFINITY;
-        if (p.qn2) {
-          qn = 0.0f;
-          for (int f = 0; f < g.q_tr_count[qtr]; ++f)
-            qn = fmaxf(qn, p.qn2[head * p.qn2_head_stride + (long long)(g.q_tr_first[qtr] + f) * g.n_tiles + qtile]);
-        }
-        // Fixed-reference mode: when |q||k| bounds every score of the unit by kFixedBound (log2
-        // units), the references start at 0 and never move: p = 2^(s*scale*log2e) stays in
-        // [2^-kFixedBound, 2^kFixedBound] (no overflow, no underflow), every tile takes the
-        // barrier-free fast path and no first tile needs an exact column max.  Otherwise the
-        // references start at -inf (exact lazy-rescale path).
-        const float b2 = qn * kmax * (p.scale_log2 * p.scale_log2) * 1.0002f;
-        const bool fixed = FVSR_FIXED_REF && n <= kInfoCap && b2 <= kFixedBound * kFixedBound;
-        if (lane == 0) {
-          utab[sl * 4 + 0] = n;
-          utab[sl * 4 + 1] = head;
-          utab[sl * 4 + 2] = qtr;
-          utab[sl * 4 + 3] = qtile;
-          qn2_2[sl] = qn;
-          c0_2[sl] = ((kInstrument && (p.debug & 1)) || fixed) ? 0.0f : -INFINITY;
-        }
-        if (MK == 1 && lane < 8) {
-          const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
-          int lo, hi;
-          locality_range(m.mode, qh0 + lane, m.extent_h, g.rows, lo, hi);
-          win2[sl * 32 + lane] = lo;
-          win2[sl * 32 + 8 + lane] = hi;
-          locality_range(m.mode, qw0 + lane, m.extent_w, g.cols, lo, hi);
-          win2[sl * 32 + 16 + lane] = lo;
-          win2[sl * 32 + 24 + lane] = hi;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tab_full + sl);
-      }
       // the next unit's Q into L2 now: its load below waits for this unit's last QK and
       // would otherwise pay the full HBM latency between units
       if (lane < 2 && u + gridDim.x < n_units) {
@@ -702,12 +735,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       }
       ++U;
     }
-    // end of the unit stream for the softmax warps
-    if (U >= 2) mbar_wait(tab_empty + (U & 1), ((U >> 1) - 1) & 1);
-    if (lane == 0) {
-      utab[(U & 1) * 4] = -1;
-      mbar_arrive(tab_full + (U & 1));
-    }
   } else if (warp == Cfg::kVProducerWarp) {
     // ================================ V producer (warp-wide) =============================
     int T = 0;
@@ -754,6 +781,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       for (int t = 0; t < n; ++t, ++G) {
         if (lane == 0) trace_at(p, 18, G);
         if (kQkLead > 0 && G >= kQkLead) mbar_wait(pv_iss + (G - kQkLead) % 4, (uint32_t)((G - kQkLead) / 4) & 1);
+        if (lane == 0) trace_at(p, 7, G);
         mbar_wait(qk_go + sb, sph);
         if (lane == 0) trace_at(p, 19, G);
         tc_fence_after();
