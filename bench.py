@@ -286,7 +286,6 @@ def run_b200(args):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    ctx.timing(True)
     launches0 = ctx.launch_count()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -303,11 +302,22 @@ def run_b200(args):
     clocks.window = (w0, w1)
     time.sleep(0.15)
     clocks.stop()
-    ctx.timing(False)
     elapsed_ms = ev0.elapsed_time(ev1)
     launches = ctx.launch_count() - launches0
     ctx.check_errors()
     pairs = ctx.read_pairs()
+    # per-kernel-class CUDA-event spans, in a separate pass after the timed region (events
+    # between the kernels would serialise their programmatic-dependent-launch overlap)
+    span_steps = min(args.steps, 200)
+    ctx.timing(True)
+    for _ in range(span_steps):
+        step()
+    if gather:
+        gather.drain()
+    barrier()
+    ctx.timing(False)
+    ctx.check_errors()
+    pairs_span = ctx.read_pairs()
     attn_ms, attn_n = ctx.timing_read(_abi.TIME_ATTENTION)
     mb_ms, mb_n = ctx.timing_read(_abi.TIME_MASK_BUILDER)
     ap_ms, ap_n = ctx.timing_read(_abi.TIME_APPEND, clear=True)
@@ -402,7 +412,7 @@ def run_b200(args):
 
     # ---- roofline of the dominant kernel ---------------------------------------------------
     attn_avg_ms = attn_ms / max(1, attn_n)
-    pairs_per_launch = pairs / max(1, attn_n)
+    pairs_per_launch = pairs_span / max(1, attn_n)
     achieved = 4.0 * D * pairs_per_launch / (attn_avg_ms / 1e3) / 1e12
     traffic = None
     prof = os.path.join(HERE, "profiles", "ncu_attention_summary.json")

@@ -254,6 +254,39 @@ int after_launch(fvsr_ctx* ctx, cudaStream_t s, int nlaunch) {
   return FVSR_OK;
 }
 
+// Kernel launch with programmatic stream serialization (PDL): the grid may be scheduled while
+// the previous kernel of the stream drains; every kernel of this library calls pdl_wait()
+// before touching global state, so the overlap covers launch latency and prologues only.
+// FVSR_PDL=0 disables it (plain stream order).
+// Only the attention kernel (one persistent CTA per SM, long prologue) is launched this way:
+// small many-CTA kernels launched early pile onto the first SMs that free up.
+inline int pdl_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("FVSR_PDL");
+    return e ? std::atoi(e) : 1;  // 0 off, 1 attention only, 2 every kernel
+  }();
+  return mode;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kp(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                      Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl_mode() == 2 || (pdl && pdl_mode() == 1)) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  return launch_kp(false, kern, grid, block, smem, s, std::forward<Args>(args)...);
+}
+
 int launch_pack_pool(const PackPoolArgs& a, const PoolGroups& pg, const SlotList& sl, dim3 grid, int max_cnt,
                      cudaStream_t s) {
   if (a.d % 8 != 0) return fail(FVSR_E_CONFIG, "pack_pool: head_dim must be a multiple of 8 (got %d)", a.d);
@@ -265,7 +298,7 @@ int launch_pack_pool(const PackPoolArgs& a, const PoolGroups& pg, const SlotList
     FVSR_CUDA(cudaFuncSetAttribute(pack_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  pack_pool_kernel<<<grid, kPPThreads, smem, s>>>(a, pg, sl);
+  FVSR_CUDA(launch_k(pack_pool_kernel, dim3(grid), dim3(kPPThreads), smem, s, a, pg, sl));
   return FVSR_OK;
 }
 
@@ -321,8 +354,8 @@ void launch_pack(const uint16_t* src, long long src_head_stride, int heads, int 
   SlotList sl{};
   for (int i = 0; i < nframes; ++i) sl.s[i] = slots ? slots[i] : i;
   dim3 grid(g.n_tiles, nframes, heads);
-  pack_frames_kernel<<<grid, 256, 0, s>>>(src, src_head_stride, g.rows, g.cols, g.tiles_w, g.n_tiles, g.d, dst,
-                                          dst_head_stride, sl);
+  (void)launch_k(pack_frames_kernel, grid, dim3(256), 0, s, src, src_head_stride, g.rows, g.cols, g.tiles_w,
+                 g.n_tiles, g.d, dst, dst_head_stride, sl);
 }
 
 // Pooled partials for the t_rows of a frame list.
@@ -341,8 +374,8 @@ void launch_pool_trows(const uint16_t* src, long long src_head_stride, int heads
   for (int i = 0; i < nf; ++i) sl.s[i] = slots ? slots[i] : i;
   dim3 grid(g.n_tiles, ntr, heads);
   const int threads = std::min(256, ((g.d + 31) / 32) * 32);
-  pool_partials_kernel<<<grid, threads, 0, s>>>(src, src_head_stride, g.rows, g.cols, g.tiles_w, g.n_tiles, g.d, pg,
-                                                sl, s0, s1, part_head_stride, nullptr);
+  (void)launch_k(pool_partials_kernel, grid, dim3(threads), 0, s, src, src_head_stride, g.rows, g.cols, g.tiles_w,
+                 g.n_tiles, g.d, pg, sl, s0, s1, part_head_stride, nullptr);
 }
 
 int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads, const float* q_s0,
@@ -384,14 +417,14 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
         FVSR_CUDA(cudaFuncSetAttribute(score_topk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
         conf8 = smem_f;
       }
-      score_topk_kernel<8><<<gf, kFThreads, smem_f, s>>>(g, dm, p);
+      FVSR_CUDA(launch_k(score_topk_kernel<8>, dim3(gf), dim3(kFThreads), smem_f, s, g, dm, p));
     } else {
       static size_t conf16 = 48 * 1024;
       if (smem_f > conf16) {
         FVSR_CUDA(cudaFuncSetAttribute(score_topk_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
         conf16 = smem_f;
       }
-      score_topk_kernel<16><<<gf, kFThreads, smem_f, s>>>(g, dm, p);
+      FVSR_CUDA(launch_k(score_topk_kernel<16>, dim3(gf), dim3(kFThreads), smem_f, s, g, dm, p));
     }
     return FVSR_OK;
   }
@@ -408,14 +441,14 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
   if (smem_sc > 48 * 1024)
     FVSR_CUDA(cudaFuncSetAttribute(coarse_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sc));
   dim3 gs((g.bnk + kScK - 1) / kScK, (g.bnq + kScQ - 1) / kScQ, heads);
-  coarse_score_kernel<<<gs, kScThreads, smem_sc, s>>>(g, dm, p, scores);
+  FVSR_CUDA(launch_k(coarse_score_kernel, dim3(gs), dim3(kScThreads), smem_sc, s, g, dm, p, scores));
   dim3 gt((g.bnq + kTopkWarps - 1) / kTopkWarps, heads);
   if (g.bnk <= 32 * 8)
-    topk_select_kernel<8><<<gt, kTopkWarps * 32, 0, s>>>(g, dm, p, scores);
+    FVSR_CUDA(launch_k(topk_select_kernel<8>, dim3(gt), dim3(kTopkWarps * 32), 0, s, g, dm, p, scores));
   else if (g.bnk <= 32 * 32)
-    topk_select_kernel<32><<<gt, kTopkWarps * 32, 0, s>>>(g, dm, p, scores);
+    FVSR_CUDA(launch_k(topk_select_kernel<32>, dim3(gt), dim3(kTopkWarps * 32), 0, s, g, dm, p, scores));
   else if (g.bnk <= 32 * 128)
-    topk_select_kernel<128><<<gt, kTopkWarps * 32, 0, s>>>(g, dm, p, scores);
+    FVSR_CUDA(launch_k(topk_select_kernel<128>, dim3(gt), dim3(kTopkWarps * 32), 0, s, g, dm, p, scores));
   else
     return fail(FVSR_E_CONFIG, "too many key blocks (%d > 4096) for the selector", g.bnk);
   return FVSR_OK;
@@ -433,7 +466,7 @@ int launch_attn_dqm(const DevGeom& g, const DevMask& dm, const AttnParams& p, in
   const long long units = p.unit_end - p.unit_begin;
   if (units <= 0) return FVSR_OK;
   const unsigned grid = (unsigned)std::min<long long>(units, sms);  // persistent CTAs
-  sparse_attn_kernel<D, NQ, MK><<<grid, Cfg::kThreads, Cfg::kBytes, s>>>(g, dm, p);
+  FVSR_CUDA(launch_kp(true, sparse_attn_kernel<D, NQ, MK>, dim3(grid), dim3(Cfg::kThreads), Cfg::kBytes, s, g, dm, p));
   return FVSR_OK;
 }
 
@@ -771,11 +804,11 @@ int32_t fvsr_sparsity_report(fvsr_ctx* ctx, int32_t heads, const fvsr_grid* grid
   for (uint64_t* o : {executed_pairs, dense_pairs, selected_blocks, allowed_blocks})
     FVSR_CUDA(cudaMemsetAsync(o, 0, sizeof(uint64_t) * heads, s));
   dim3 grid(g.bnq, heads);
-  sparsity_count_kernel<<<grid, 128, 0, s>>>(g, dm, sel, sel_count, cap,
+  FVSR_CUDA(launch_k(sparsity_count_kernel, dim3(grid), dim3(128), 0, s, g, dm, sel, sel_count, cap,
                                              reinterpret_cast<unsigned long long*>(executed_pairs),
                                              reinterpret_cast<unsigned long long*>(dense_pairs),
                                              reinterpret_cast<unsigned long long*>(selected_blocks),
-                                             reinterpret_cast<unsigned long long*>(allowed_blocks));
+                                             reinterpret_cast<unsigned long long*>(allowed_blocks)));
   return after_launch(ctx, s, 1);
 }
 

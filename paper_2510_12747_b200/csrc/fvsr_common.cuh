@@ -210,6 +210,11 @@ __device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* ptr) {
 __device__ __forceinline__ void st_release_shared(uint32_t* ptr, uint32_t v) {
   asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(ptr)), "r"(v) : "memory");
 }
+// Programmatic dependent launch: a kernel launched with programmatic stream serialization
+// may start while its predecessor drains; it must wait (griddepcontrol.wait) before touching
+// anything the predecessor writes or reads.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // Per-warpgroup register budget (all 4 warps of the warpgroup execute it).
 template <int N>
 __device__ __forceinline__ void reg_alloc() {

@@ -414,6 +414,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // setup above overlaps the predecessor (top-k) under programmatic dependent launch
+  pdl_trigger();
+  pdl_wait();
   const uint32_t tmem = *tmem_slot;
   // TMEM columns: S buffers [0, NS*NQ), then O^T buffers [group][unit parity]
   const uint32_t tS0 = tmem, tO0 = tmem + kNS * NQ;

@@ -39,6 +39,8 @@ __global__ void __launch_bounds__(256) pack_frames_kernel(const uint16_t* __rest
                                                           int d, uint8_t* __restrict__ dst,
                                                           long long dst_head_stride,  // bytes
                                                           SlotList slots) {
+  pdl_wait();
+  pdl_trigger();
   const int tile = blockIdx.x, f = blockIdx.y, head = blockIdx.z;
   const int th = tile / tiles_w, tw = tile % tiles_w;
   const int chunks_per_row = d >> 3;  // 16-byte chunks
@@ -76,6 +78,8 @@ __global__ void __launch_bounds__(256) pool_partials_kernel(const uint16_t* __re
                                                             float* __restrict__ s1,
                                                             long long part_head_stride,  // elements
                                                             const float* __restrict__ ext_s0) {
+  pdl_wait();
+  pdl_trigger();
   const int tile = blockIdx.x, grp = blockIdx.y, head = blockIdx.z;
   const int th = tile / tiles_w, tw = tile % tiles_w;
   const int hc = min(8, rows - 8 * th), wc = min(8, cols - 8 * tw);
@@ -163,6 +167,8 @@ inline size_t pack_pool_smem(int d, int max_cnt, bool two) {
 __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_constant__ PackPoolArgs a,
                                                                const __grid_constant__ PoolGroups groups,
                                                                const __grid_constant__ SlotList slots) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t sm_pp[];
   const int tile = blockIdx.x, grp = blockIdx.y, head = blockIdx.z;
   const int tid = threadIdx.x;
@@ -440,6 +446,8 @@ __device__ inline void chain4(float& acc, const float4& a, const float4& b) {
 
 __global__ void __launch_bounds__(kScThreads) coarse_score_kernel(DevGeom g, DevMask m, SelectParams p,
                                                                  float* __restrict__ scores) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) float smf[];
   const int d = g.d, ld = d + 4, d4 = d >> 2;
   float* pq = smf;              // [kScQ][d+4]
@@ -646,6 +654,8 @@ __global__ void __launch_bounds__(kTopkWarps * 32) topk_select_kernel(const __gr
                                                                      const __grid_constant__ DevMask m,
                                                                      const __grid_constant__ SelectParams p,
                                                                      const float* __restrict__ scores) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const int qb = blockIdx.x * kTopkWarps + warp;
   if (qb >= g.bnq) return;
@@ -669,6 +679,8 @@ template <int NPER>
 __global__ void __launch_bounds__(kFThreads) score_topk_kernel(const __grid_constant__ DevGeom g,
                                                               const __grid_constant__ DevMask m,
                                                               const __grid_constant__ SelectParams p) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) float smf[];
   const int d = g.d, ld = d + 4, d4 = d >> 2, bnk = g.bnk;
   const int rows = bnk + kFQB;                      // pooled keys, then pooled queries
@@ -776,6 +788,8 @@ __global__ void __launch_bounds__(128) sparsity_count_kernel(DevGeom g, DevMask 
                                                              unsigned long long* dense,
                                                              unsigned long long* nselected,
                                                              unsigned long long* nallowed) {
+  pdl_wait();
+  pdl_trigger();
   const int qb = blockIdx.x, head = blockIdx.y;
   const int qtr = qb / g.n_tiles, qtile = qb % g.n_tiles;
   unsigned long long ex = 0, dn = 0, na = 0;
