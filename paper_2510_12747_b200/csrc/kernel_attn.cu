@@ -1014,9 +1014,14 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
             // P buffer pb was last read by PV(G - NP) (kNP tiles back: normally long done, and
             // published by the V producer, which waits on PVs to recycle V stages), so each
             // word's P^T is stored as soon as it is computed, under the next word's exps
-            if (G >= kNP && ld_acquire_shared(prog + 1) <= (uint32_t)(G - kNP))
-              mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
-            if (threadIdx.x == 0) trace_at(p, 9, G);
+            // (one P buffer per group, NQ = 128: PV(G - 1) is the previous tile's, so the
+            // wait moves behind the exps and the stores follow all words)
+            constexpr bool kEarlyP = kNP > kGroups;
+            if constexpr (kEarlyP) {
+              if (G >= kNP && ld_acquire_shared(prog + 1) <= (uint32_t)(G - kNP))
+                mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
+              if (threadIdx.x == 0) trace_at(p, 9, G);
+            }
             uint32_t pk[CPT / 2];
   #pragma unroll
             for (int w = 0; w < kW; ++w) {
@@ -1062,14 +1067,32 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
                 }
               }
               if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
-              const int cwi = col0 + 32 * w;
-              uint8_t* pw = prow + (cwi >> 6) * 16384;
-              const int ch0 = (cwi & 63) >> 3;
-  #pragma unroll
-              for (int c8 = 0; c8 < 4; ++c8)
-                *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
-                    make_uint4(pk[16 * w + 4 * c8], pk[16 * w + 4 * c8 + 1], pk[16 * w + 4 * c8 + 2],
-                               pk[16 * w + 4 * c8 + 3]);
+              if constexpr (kEarlyP) {
+                const int cwi = col0 + 32 * w;
+                uint8_t* pw = prow + (cwi >> 6) * 16384;
+                const int ch0 = (cwi & 63) >> 3;
+#pragma unroll
+                for (int c8 = 0; c8 < 4; ++c8)
+                  *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
+                      make_uint4(pk[16 * w + 4 * c8], pk[16 * w + 4 * c8 + 1], pk[16 * w + 4 * c8 + 2],
+                                 pk[16 * w + 4 * c8 + 3]);
+              }
+            }
+            if constexpr (!kEarlyP) {
+              if (G >= kNP && ld_acquire_shared(prog + 1) <= (uint32_t)(G - kNP))
+                mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
+              if (threadIdx.x == 0) trace_at(p, 9, G);
+#pragma unroll
+              for (int w = 0; w < kW; ++w) {
+                const int cwi = col0 + 32 * w;
+                uint8_t* pw = prow + (cwi >> 6) * 16384;
+                const int ch0 = (cwi & 63) >> 3;
+#pragma unroll
+                for (int c8 = 0; c8 < 4; ++c8)
+                  *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
+                      make_uint4(pk[16 * w + 4 * c8], pk[16 * w + 4 * c8 + 1], pk[16 * w + 4 * c8 + 2],
+                                 pk[16 * w + 4 * c8 + 3]);
+              }
             }
           } else {
             // Columns in 32-wide words: each word is loaded, exponentiated and stored on its own
