@@ -99,6 +99,7 @@ constexpr int kExp = FVSR_ATTN_EXP;
 #define FVSR_QK_LEAD 3
 #endif
 constexpr int kQkLead = FVSR_QK_LEAD;
+static_assert(kQkLead >= 0 && kQkLead <= 4, "the pv_iss ring has 4 barriers");
 constexpr int kPolyN = FVSR_POLY_EXP;  // of every 8 exp pairs of an unmasked word, on the FMA pipe
 constexpr bool kPolyExp = kPolyN != 0;
 __device__ __forceinline__ void trace_at(const AttnParams& p, int ev, int G) {
