@@ -98,6 +98,8 @@ constexpr int kExp = FVSR_ATTN_EXP;
 #ifndef FVSR_QK_LEAD
 #define FVSR_QK_LEAD 3
 #endif
+// QK(G) is issued only once PV(G - kQkLead) was issued (0: only the S buffers bound the
+// run-ahead), so PVs do not queue behind several tiles of QK MMAs in the in-order tensor pipe
 constexpr int kQkLead = FVSR_QK_LEAD;
 static_assert(kQkLead >= 0 && kQkLead <= 4, "the pv_iss ring has 4 barriers");
 constexpr int kPolyN = FVSR_POLY_EXP;  // of every 8 exp pairs of an unmasked word, on the FMA pipe
