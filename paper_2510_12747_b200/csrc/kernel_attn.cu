@@ -137,8 +137,11 @@ struct AttnCfg {
   static constexpr int kPvWarp = kSW + 3;            // PV issuer (own program order: QK never waits on P)
   static constexpr int kEpiWarp = kSW + 4;           // epilogue warpgroup (merge, normalise, store)
   static constexpr int kThreads = kSW * 32 + 256;    // 16 warps
-  static constexpr int kRegSoftmax = 168;            // setmaxnreg: 256 x 168 + 256 x 88 = 64K
-  static constexpr int kRegOther = 88;
+#ifndef FVSR_REG_SOFTMAX
+#define FVSR_REG_SOFTMAX 184
+#endif
+  static constexpr int kRegSoftmax = FVSR_REG_SOFTMAX;  // setmaxnreg: 256 x 184 + 256 x 72 = 64K
+  static constexpr int kRegOther = 256 - kRegSoftmax;
   static constexpr int kNS = NQ == 64 ? 4 : 2;       // S^T buffers in TMEM
   static constexpr int kNK = 2;                      // K stages (QK consumes them right away)
 #ifndef FVSR_NV64
