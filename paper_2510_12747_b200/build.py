@@ -46,14 +46,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd.insert(1, "-DFVSR_ATTN_INSTRUMENT=1")
     if os.environ.get("FVSR_FIXED_REF"):  # experiments: 0 = always start from -inf references
         cmd.insert(1, "-DFVSR_FIXED_REF=" + str(int(os.environ["FVSR_FIXED_REF"])))
-    if os.environ.get("FVSR_BALANCE_TAIL"):  # experiments: 0 = plain round-robin units
-        cmd.insert(1, "-DFVSR_BALANCE_TAIL=" + str(int(os.environ["FVSR_BALANCE_TAIL"])))
     if os.environ.get("FVSR_ATTN_EXP"):  # experiments: bottleneck ablations (not attention)
         cmd.insert(1, "-DFVSR_ATTN_EXP=" + str(int(os.environ["FVSR_ATTN_EXP"])))
     # experiments: V stages / P buffers at NQ=64, test_wait-first barriers, polynomial exp2,
     # QK pacing lead, per-CTA timeline stamps, softmax register budget
     for k in ("FVSR_NV64", "FVSR_NP64", "FVSR_MBAR_TEST_FIRST", "FVSR_POLY_EXP", "FVSR_QK_LEAD",
-              "FVSR_CTA_TIMELINE", "FVSR_REG_SOFTMAX"):  # experiments: V stages / P buffers at NQ=64
+              "FVSR_CTA_TIMELINE", "FVSR_REG_SOFTMAX"):
         if os.environ.get(k):
             cmd.insert(1, "-D%s=%d" % (k, int(os.environ[k])))
     if verbose:
