@@ -107,6 +107,9 @@ enum {
                                included): each rank's shard is contiguous for the NCCL all-gather */
 };
 
+/* Eviction strategies == vsr::EvictStrategy (P/include/vsr/kv_cache.hpp:12). */
+enum { FVSR_EVICT_SLIDING = 0, FVSR_EVICT_UNIFORM = 1, FVSR_EVICT_HEAD_WISE = 2 };
+
 /* Kernel classes timed by fvsr_ctx_timing_enable. */
 enum { FVSR_TIME_APPEND = 0, FVSR_TIME_MASK_BUILDER = 1, FVSR_TIME_ATTENTION = 2 };
 
@@ -210,6 +213,30 @@ FVSR_API int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* ring, int32_t lay
                             int64_t topk, float scale, int64_t unit_begin, int64_t unit_end,
                             uint16_t* out, int32_t out_layout, int32_t sel_cap, int32_t* sel,
                             int32_t* sel_count, fvsr_stream_t stream);
+
+/* ---- scored eviction ------------------------------------------------- */
+/* frame_attention_mass (P/src/kv_cache.cpp:170-206; declared P/include/vsr/kv_cache.hpp:79):
+ * per head and key frame (grid_k order), the coarse-score softmax mass of every q-block
+ * (fp64, coarse-allowed blocks only) summed into key blocks and split over their member
+ * tokens' frames.  coarse: DEVICE fp32 [heads][bnq][bnk] (fvsr_plan_sparse's output);
+ * mass: DEVICE double [heads][grid_k->n_frames].  Within 1e-12 relative of the reference
+ * (device exp and reduction order differ in the last ulps). */
+FVSR_API int32_t fvsr_frame_attention_mass(fvsr_ctx* ctx, int32_t heads, const fvsr_grid* grid_q,
+                                  const fvsr_grid* grid_k, const fvsr_mask* mask,
+                                  const float* coarse, double* mass, fvsr_stream_t stream);
+/* The same for the plan of the preceding fvsr_ring_attention on this ctx (same layer, same
+ * q frames and mask, stream order; call before evicting): head_attention's frame_scores
+ * (P/src/stream.cpp:190).  mass: DEVICE double [heads][n] aligned with fvsr_ring_frame_ids. */
+FVSR_API int32_t fvsr_ring_frame_mass(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer,
+                             const int32_t* q_frame_ids, int32_t nq, const fvsr_mask* mask,
+                             double* mass, fvsr_stream_t stream);
+/* KVCache::evict (P/src/kv_cache.cpp:97-137): FVSR_EVICT_SLIDING ignores scores;
+ * FVSR_EVICT_UNIFORM sums HOST scores [heads][n] (aligned with fvsr_ring_frame_ids) over heads
+ * and drops the lowest-scored non-newest frames (older first on ties) from every head.
+ * FVSR_EVICT_HEAD_WISE is accepted only when every head picks the same victims (the device
+ * ring keeps head-identical sets), else FVSR_E_CONFIG.  NULL scores while over budget on a
+ * scored strategy: FVSR_E_CONFIG (kv_cache.cpp:112-113). */
+FVSR_API int32_t fvsr_ring_evict(fvsr_ring* ring, int32_t layer, int32_t strategy, const double* scores);
 
 /* One streaming layer-step from HOST buffers (the end-to-end path): H2D copy of the new
  * frame's q/k/v ([heads][rows*cols][d] bf16; pinned memory recommended), ring append,

@@ -19,6 +19,7 @@ seeded cases and both against the committed fixtures in ``tests/golden/``.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from dataclasses import dataclass
@@ -262,6 +263,10 @@ class Ref:
             lib.vsrref_report.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                           C.POINTER(C.c_uint64), C.c_char_p, C.c_int]
             lib.vsrref_dense.argtypes = [C.c_void_p, C.c_float, C.POINTER(C.c_float), C.c_char_p, C.c_int]
+            lib.vsrref_frame_mass.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_char_p, C.c_int]
+            lib.vsrref_kv_evict.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                            C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                            C.c_char_p, C.c_int]
             lib.vsrref_head_attention.argtypes = [C.c_void_p, C.c_long, C.c_float, C.c_uint, C.c_int,
                                                   C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float),
                                                   C.c_char_p, C.c_int]
@@ -349,6 +354,15 @@ class Ref:
                 raise OracleError(st, err.value.decode())
             return {"density": dens.value, "executed_flops": ex.value, "dense_flops": dn.value}
 
+        def frame_mass(self) -> np.ndarray:
+            """vsr::frame_attention_mass(plan, grid_k) (P/src/kv_cache.cpp:170-206)."""
+            out = np.zeros(len(self.kf), np.float64)
+            err = C.create_string_buffer(512)
+            st = self.lib.vsrref_frame_mass(self.h, _ptr(out, C.c_double), err, 512)
+            if st:
+                raise OracleError(st, err.value.decode())
+            return out
+
         def dense(self, scale: float) -> np.ndarray:
             out = np.zeros((self.lq, self.q.shape[1]), np.float32)
             err = C.create_string_buffer(512)
@@ -365,6 +379,22 @@ class Ref:
                                                 _ptr(out, C.c_float) if out is not None else None, err, 512)
             if st:
                 raise OracleError(st, err.value.decode())
+
+    def kv_evict(self, strategy: int, window: int, ids, scores: Optional[np.ndarray], heads: int):
+        """KVCache(1, heads, window, strategy) holding `ids` on every head, then evict(0, scores)
+        (P/src/kv_cache.cpp:97-137).  Returns the retained ids per head."""
+        ids = _i32(ids)
+        n = len(ids)
+        sc = None if scores is None else np.ascontiguousarray(scores, np.float64).reshape(heads, n)
+        out = np.zeros((heads, n), np.int32)
+        cnt = np.zeros(heads, np.int32)
+        err = C.create_string_buffer(512)
+        st = self.lib.vsrref_kv_evict(strategy, heads, window, n, _ptr(ids, C.c_int),
+                                      _ptr(sc, C.c_double) if sc is not None else None,
+                                      _ptr(out, C.c_int), _ptr(cnt, C.c_int), err, 512)
+        if st:
+            raise OracleError(st, err.value.decode())
+        return [list(map(int, out[h, : cnt[h]])) for h in range(heads)]
 
     def case(self, q, k, v, qf, kf, rows, cols, mask: Optional[Mask] = None) -> "Ref.Case":
         return Ref.Case(self.lib, q, k, v, qf, kf, rows, cols, mask or Mask.all())
@@ -411,3 +441,67 @@ def synthetic_qkv(seed: int, lq: int, lk: int, d: int, gen=None, bf16: bool = Tr
     if bf16:
         q, k, v = bf16_round(q), bf16_round(k), bf16_round(v)
     return q, k, v
+
+
+# ----------------------------------------------------------------------------
+# Scored eviction: numpy restatement
+# ----------------------------------------------------------------------------
+
+def frame_attention_mass(plan: Plan, kf: Sequence[int], rows: int, cols: int) -> np.ndarray:
+    """Per-frame attention mass of a plan over its key grid (P/src/kv_cache.cpp:170-206).
+
+    For every q-block: softmax in double over the coarse-allowed key blocks of its fp32
+    coarse scores (max, exp(s - max), sum in key-block order; rows with no allowed block are
+    skipped); the per-key-block masses are summed over q-blocks in order, then each block's
+    mass is split over its member tokens and credited to their frames."""
+    coarse = plan.coarse.astype(np.float64)
+    allowed = plan.allowed.astype(bool)
+    bnq, bnk = coarse.shape
+    block_mass = np.zeros(bnk, np.float64)
+    for qb in range(bnq):
+        if not allowed[qb].any():
+            continue
+        mx = coarse[qb][allowed[qb]].max()
+        # math.exp is libm's exp, the function std::exp calls (numpy's SIMD exp differs in ulps)
+        row = np.array([math.exp(coarse[qb, kb] - mx) if allowed[qb, kb] else 0.0 for kb in range(bnk)])
+        denom = 0.0
+        for x in row:  # sequential, key-block order (kv_cache.cpp:184-189)
+            denom += x
+        block_mass += row / denom
+    assign, _ = Port().partition(kf, rows, cols)
+    per_frame_tok = rows * cols
+    members = np.bincount(assign, minlength=bnk).astype(np.float64)
+    out = np.zeros(len(kf), np.float64)
+    order = np.argsort(assign, kind="stable")  # key blocks ascending, members in token order
+    for tok in order:  # (kv_cache.cpp:193-203)
+        kb = assign[tok]
+        if block_mass[kb] != 0.0:
+            out[tok // per_frame_tok] += block_mass[kb] / members[kb]
+    return out
+
+
+def evict_victims(ids: Sequence[int], score: Sequence[float], excess: int):
+    """Victim order for one head (P/src/kv_cache.cpp:81-93): lowest score first, older frame
+    on ties, newest frame exempt."""
+    idx = sorted(range(len(ids) - 1), key=lambda i: (score[i], ids[i]))
+    return [int(ids[i]) for i in idx[:excess]]
+
+
+def evict(strategy: int, window: int, ids: Sequence[int], scores: Optional[np.ndarray], heads: int):
+    """KVCache::evict for one layer whose heads all hold `ids` (P/src/kv_cache.cpp:97-137).
+    strategy 0 sliding, 1 uniform (head scores summed), 2 head-wise.  Returns retained ids per head."""
+    ids = [int(i) for i in ids]
+    if strategy == 0 or len(ids) <= window:
+        return [ids[-window:] if len(ids) > window else list(ids) for _ in range(heads)]
+    sc = np.asarray(scores, np.float64).reshape(heads, len(ids))
+    if strategy == 1:
+        total = np.zeros(len(ids), np.float64)
+        for h in range(heads):
+            total += sc[h]
+        gone = set(evict_victims(ids, list(total), len(ids) - window))
+        return [[i for i in ids if i not in gone] for _ in range(heads)]
+    out = []
+    for h in range(heads):
+        gone = set(evict_victims(ids, list(sc[h]), len(ids) - window))
+        out.append([i for i in ids if i not in gone])
+    return out

@@ -11,6 +11,8 @@
 //   vsr::sparsity_report         P/src/sparse.cpp:256-285
 //   vsr::dense_attention_oracle  P/src/attention.cpp:40-56
 //   vsr::Rng::gaussian           P/include/vsr/rng.hpp:34-48
+//   vsr::frame_attention_mass    P/src/kv_cache.cpp:170-206
+//   vsr::KVCache::evict          P/src/kv_cache.cpp:97-137
 // (P = /root/reference/proj).  The shim only marshals arrays and maps the
 // reference exception taxonomy (P/include/vsr/common.hpp:10-48) to ints.
 #include <cstdint>
@@ -20,6 +22,7 @@
 #include <vector>
 
 #include "vsr/attention.hpp"
+#include "vsr/kv_cache.hpp"
 #include "vsr/mask.hpp"
 #include "vsr/partition.hpp"
 #include "vsr/rng.hpp"
@@ -256,6 +259,43 @@ int vsrref_head_attention(vsrref_case* c, long topk, float scale, unsigned threa
     vsr::TensorF32 o =
         vsr::sparse_attention_exec(c->q, c->k, c->v, plan, mask, scale, 0, SIZE_MAX, threads);
     if (out) std::memcpy(out, o.data.data(), o.data.size() * sizeof(float));
+  });
+}
+
+// Per-frame attention mass of the current plan over the key grid (ascending frame ids).
+int vsrref_frame_mass(const vsrref_case* c, double* out, char* err, int errlen) {
+  if (!c->have_plan) return kInvariant;
+  return guarded(err, errlen, [&] {
+    const std::vector<double> m = vsr::frame_attention_mass(c->plan, *c->grid_k);
+    std::memcpy(out, m.data(), m.size() * sizeof(double));
+  });
+}
+
+// One KVCache layer: every head holds frames ids[0..n), then evict(layer, scores) with
+// strategy 0 sliding / 1 uniform / 2 head_wise.  scores: [heads][n] (NULL -> {}).
+// out_ids: [heads][n] retained ids, out_n: [heads] retained counts.
+int vsrref_kv_evict(int strategy, int heads, int window, int n, const int* ids,
+                    const double* scores, int* out_ids, int* out_n, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const vsr::EvictStrategy st = strategy == 0 ? vsr::EvictStrategy::sliding_window
+                                  : strategy == 1 ? vsr::EvictStrategy::uniform
+                                                  : vsr::EvictStrategy::head_wise;
+    vsr::KVCache cache(1, static_cast<std::size_t>(heads), static_cast<std::size_t>(window), st);
+    for (int h = 0; h < heads; ++h)
+      for (int i = 0; i < n; ++i)
+        cache.append(0, static_cast<std::size_t>(h), ids[i], vsr::TensorF32({1, 1}),
+                     vsr::TensorF32({1, 1}));
+    std::vector<std::vector<double>> sc;
+    if (scores)
+      for (int h = 0; h < heads; ++h)
+        sc.emplace_back(scores + static_cast<std::size_t>(h) * n,
+                        scores + static_cast<std::size_t>(h + 1) * n);
+    cache.evict(0, sc);
+    for (int h = 0; h < heads; ++h) {
+      const std::vector<int> r = cache.frame_ids(0, static_cast<std::size_t>(h));
+      out_n[h] = static_cast<int>(r.size());
+      std::memcpy(out_ids + static_cast<std::size_t>(h) * n, r.data(), r.size() * sizeof(int));
+    }
   });
 }
 

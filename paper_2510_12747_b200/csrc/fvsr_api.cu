@@ -87,6 +87,8 @@ struct fvsr_ctx {
   // coarse block scores for the top-k pass (plan / ring attention without a user buffer)
   float* d_scores = nullptr;
   size_t scores_cap = 0;
+  // shape of the scores the last two-kernel selection left in d_scores (fvsr_ring_frame_mass)
+  int scores_heads = 0, scores_bnq = 0, scores_bnk = 0;
 };
 
 struct fvsr_ring {
@@ -409,6 +411,7 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
     return e && std::atoi(e) != 0;
   }();
   if (fused_select && smem_f <= 200 * 1024 && g.bnk <= 32 * 16) {
+    ctx->scores_heads = ctx->scores_bnq = ctx->scores_bnk = 0;
     p.coarse = coarse;
     dim3 gf((g.bnq + kFQB - 1) / kFQB, heads);
     if (g.bnk <= 32 * 8) {
@@ -431,9 +434,13 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
   // coarse scores -> workspace (L2-resident, heads*bnq*bnk floats), then per-row top-k
   const size_t n_scores = (size_t)heads * g.bnq * g.bnk;
   float* scores = coarse;
+  ctx->scores_heads = ctx->scores_bnq = ctx->scores_bnk = 0;
   if (!scores) {
     if (ctx_reserve_scores(ctx, n_scores) != FVSR_OK) return FVSR_E_CUDA;
     scores = ctx->d_scores;
+    ctx->scores_heads = heads;
+    ctx->scores_bnq = g.bnq;
+    ctx->scores_bnk = g.bnk;
   }
   p.coarse = nullptr;  // the score kernel writes `scores` directly
   if (g.d % 4 != 0) return fail(FVSR_E_CONFIG, "plan_sparse: head_dim must be a multiple of 4 (got %d)", g.d);
@@ -1059,6 +1066,111 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   p.qn2_head_stride = (long long)g.nqf * g.n_tiles;
   FVSR_TRY(launch_attention(ctx, g, dm, p, r->heads, unit_begin, unit_end, s));
   return after_launch(ctx, s, 4);
+}
+
+// ---- scored eviction ------------------------------------------------------
+namespace {
+int launch_frame_mass(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads, const float* coarse,
+                      double* mass, cudaStream_t s) {
+  const size_t smem = (size_t)(2 * g.bnq + g.bnk) * sizeof(double);
+  if (smem > 200 * 1024) return fail(FVSR_E_CONFIG, "frame_attention_mass: %d x %d blocks too large", g.bnq, g.bnk);
+  static size_t configured = 48 * 1024;
+  if (smem > configured) {
+    FVSR_CUDA(cudaFuncSetAttribute(frame_mass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  FVSR_CUDA(launch_k(frame_mass_kernel, dim3(heads), dim3(kMassThreads), smem, s, g, dm, coarse, mass));
+  return after_launch(ctx, s, 1);
+}
+
+// victim order for one head (P/src/kv_cache.cpp:81-93): lowest score first, older frame on
+// ties, the newest frame exempt
+std::vector<int> evict_victims(const std::vector<int>& ids, const double* score, size_t excess) {
+  std::vector<size_t> idx;
+  for (size_t i = 0; i + 1 < ids.size(); ++i) idx.push_back(i);
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
+    if (score[a] != score[b]) return score[a] < score[b];
+    return ids[a] < ids[b];
+  });
+  std::vector<int> out;
+  for (size_t i = 0; i < excess && i < idx.size(); ++i) out.push_back(ids[idx[i]]);
+  std::sort(out.begin(), out.end());
+  return out;
+}
+}  // namespace
+
+int32_t fvsr_frame_attention_mass(fvsr_ctx* ctx, int32_t heads, const fvsr_grid* grid_q, const fvsr_grid* grid_k,
+                                  const fvsr_mask* mask, const float* coarse, double* mass, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  if (!coarse || !mass) return fail(FVSR_E_SHAPE, "frame_attention_mass: null tensor");
+  if (heads < 1) return fail(FVSR_E_SHAPE, "frame_attention_mass: heads must be >= 1");
+  DevGeom g;
+  FVSR_TRY(build_geom(grid_q, grid_k, 4, nullptr, g));
+  DevMask dm;
+  FVSR_TRY(build_mask(mask, g, grid_tokens(grid_k), dm));
+  return launch_frame_mass(ctx, g, dm, heads, coarse, mass, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int32_t fvsr_ring_frame_mass(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const int32_t* q_frame_ids, int32_t nq,
+                             const fvsr_mask* mask, double* mass, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  if (!r || !q_frame_ids || !mass) return fail(FVSR_E_SHAPE, "ring_frame_mass: null argument");
+  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
+  const auto& c = r->ctx[layer];
+  if (c.empty()) return fail(FVSR_E_CONFIG, "ring_frame_mass: empty context");
+  std::vector<int> kids, kslots;
+  for (auto& fs : c) {
+    kids.push_back(fs.first);
+    kslots.push_back(fs.second);
+  }
+  fvsr_grid gq{q_frame_ids, nq, r->rows, r->cols};
+  fvsr_grid gk{kids.data(), (int)kids.size(), r->rows, r->cols};
+  DevGeom g;
+  FVSR_TRY(build_geom(&gq, &gk, r->d, kslots.data(), g));
+  DevMask dm;
+  FVSR_TRY(build_mask(mask, g, grid_tokens(&gk), dm));
+  if (ctx->scores_heads != r->heads || ctx->scores_bnq != g.bnq || ctx->scores_bnk != g.bnk)
+    return fail(FVSR_E_CONFIG,
+                "ring_frame_mass: no coarse scores of this layer-step on the context (call right after "
+                "fvsr_ring_attention of the same layer, before evicting)");
+  return launch_frame_mass(ctx, g, dm, r->heads, ctx->d_scores, mass, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int32_t fvsr_ring_evict(fvsr_ring* r, int32_t layer, int32_t strategy, const double* scores) {
+  if (!r) return fail(FVSR_E_CONFIG, "null ring");
+  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
+  if (strategy < FVSR_EVICT_SLIDING || strategy > FVSR_EVICT_HEAD_WISE)
+    return fail(FVSR_E_CONFIG, "unknown eviction strategy: %d", strategy);
+  if (strategy == FVSR_EVICT_SLIDING) return fvsr_ring_evict_sliding(r, layer);  // kv_cache.cpp:100-106
+  auto& c = r->ctx[layer];
+  const size_t n = c.size();
+  if ((int)n <= r->window) return FVSR_OK;  // kv_cache.cpp:108-111
+  if (!scores) return fail(FVSR_E_CONFIG, "KVCache: importance scores required for scored eviction");
+  std::vector<int> ids;
+  for (auto& fs : c) ids.push_back(fs.first);
+  const size_t excess = n - (size_t)r->window;
+  std::vector<int> gone;
+  if (strategy == FVSR_EVICT_UNIFORM) {  // kv_cache.cpp:118-128: head scores summed, one decision
+    std::vector<double> total(n, 0.0);
+    for (int h = 0; h < r->heads; ++h)
+      for (size_t i = 0; i < n; ++i) total[i] += scores[(size_t)h * n + i];
+    gone = evict_victims(ids, total.data(), excess);
+  } else {  // head_wise (kv_cache.cpp:130-135): per-head decisions
+    gone = evict_victims(ids, scores, excess);
+    for (int h = 1; h < r->heads; ++h)
+      if (evict_victims(ids, scores + (size_t)h * n, excess) != gone)
+        return fail(FVSR_E_CONFIG,
+                    "ring_evict: head-wise victims differ across heads; the device ring keeps head-identical "
+                    "frame sets (use one ring per head for head-wise eviction)");
+  }
+  for (int id : gone)
+    for (size_t i = 0; i < c.size(); ++i)
+      if (c[i].first == id) {
+        r->used[layer][c[i].second] = 0;
+        c.erase(c.begin() + (long)i);
+        break;
+      }
+  return FVSR_OK;
 }
 
 int32_t fvsr_ring_step_host(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* q_host,

@@ -10,6 +10,11 @@ slots directly, so no context is ever copied.
     ring.append(layer, t, k, v)             # KVCache::append for every head
     out  = ring.attention(layer, q, [t], mask, topk)   # head_attention, all heads
     ring.evict(layer)                       # KVCache::evict (sliding window)
+
+Scored eviction (P/src/kv_cache.cpp:97-137, 170-206): right after ``attention``,
+``mass = ring.frame_mass(layer, [t], mask)`` gives head_attention's frame_scores from the
+coarse scores the mask builder left on the device, and
+``ring.evict_scored(layer, EVICT_UNIFORM, mass)`` applies KVCache::evict(uniform).
 """
 from __future__ import annotations
 
@@ -22,6 +27,9 @@ import torch
 from . import _abi
 from ._abi import ShapeError, check
 from .sparse import Context, Mask, _heads3, _stream
+
+
+EVICT_SLIDING, EVICT_UNIFORM, EVICT_HEAD_WISE = 0, 1, 2  # vsr::EvictStrategy (kv_cache.hpp:12)
 
 
 class KVRing:
@@ -62,6 +70,33 @@ class KVRing:
             check(self.ctx.lib.fvsr_ring_evict_sliding(self.h, layer))
         else:
             check(self.ctx.lib.fvsr_ring_evict_keep(self.h, layer, int(keep)))
+
+    def frame_mass(self, layer: int, q_frame_ids: Sequence[int], mask: Optional[Mask] = None,
+                   check_errors: bool = True) -> torch.Tensor:
+        """frame_attention_mass of the plan of the preceding ``attention`` call on this
+        layer (same q frames and mask): float64 [heads, retained frames] on the device."""
+        mask = mask or Mask.all_allowed()
+        nq = len(q_frame_ids)
+        ids = (C.c_int32 * nq)(*[int(f) for f in q_frame_ids])
+        md = mask.c()
+        mass = torch.empty((self.heads, self.retained(layer)), dtype=torch.float64,
+                           device=torch.device("cuda", torch.cuda.current_device()))
+        check(self.ctx.lib.fvsr_ring_frame_mass(self.ctx.h, self.h, layer, ids, nq, C.byref(md), mass.data_ptr(),
+                                                _stream()))
+        if check_errors:
+            self.ctx.check_errors()
+        return mass
+
+    def evict_scored(self, layer: int, strategy: int, scores=None) -> None:
+        """KVCache::evict(layer, scores) (P/src/kv_cache.cpp:97-137); scores [heads, frames]
+        aligned with frame_ids (a device tensor is copied to the host first)."""
+        buf = None
+        if scores is not None:
+            t = torch.as_tensor(scores, dtype=torch.float64).detach().cpu().contiguous()
+            if t.shape != (self.heads, self.retained(layer)):
+                raise ShapeError("KVCache: score count must match retained frames")
+            buf = t
+        check(self.ctx.lib.fvsr_ring_evict(self.h, layer, int(strategy), buf.data_ptr() if buf is not None else None))
 
     def frame_ids(self, layer: int):
         buf = (C.c_int32 * 64)()

@@ -279,6 +279,29 @@ def sparse_attention_exec(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pla
     return out[0] if squeeze else out
 
 
+def frame_attention_mass(plan: SparsePlan, key_grid: Optional[TokenGrid] = None, mask: Optional[Mask] = None, *,
+                         ctx: Optional[Context] = None, check_errors: bool = True) -> torch.Tensor:
+    """frame_attention_mass (P/src/kv_cache.cpp:170-206) on device: float64 [heads, frames]
+    of key_grid (default plan.grid_k).  `mask` must be the one the plan was built with (it
+    defines the coarse-allowed blocks); the plan must keep its coarse scores."""
+    ctx = ctx or Context.default()
+    mask = mask or Mask.all_allowed()
+    key_grid = key_grid or plan.grid_k
+    if plan.coarse is None:
+        raise ConfigError("frame_attention_mass: plan was built without coarse scores (keep_scores=False)")
+    if key_grid.token_count() != plan.grid_k.token_count():
+        raise ShapeError("frame_attention_mass: plan does not match key grid")
+    mass = torch.empty((plan.heads, key_grid.frame_count()), dtype=torch.float64, device=plan.coarse.device)
+    gq, kq = plan.grid_q.c()
+    gk, kk = key_grid.c()
+    md = mask.c()
+    check(ctx.lib.fvsr_frame_attention_mass(ctx.h, plan.heads, C.byref(gq), C.byref(gk), C.byref(md),
+                                            plan.coarse.data_ptr(), mass.data_ptr(), _stream()))
+    if check_errors:
+        ctx.check_errors()
+    return mass
+
+
 def sparsity_report(plan: SparsePlan, mask: Optional[Mask] = None, *, ctx: Optional[Context] = None) -> SparsityReport:
     """sparsity_report (P/src/sparse.cpp:256-285), summed over heads."""
     ctx = ctx or Context.default()
