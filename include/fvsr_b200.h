@@ -180,6 +180,16 @@ FVSR_API int32_t fvsr_sparsity_report(fvsr_ctx* ctx, int32_t heads, const fvsr_g
                              uint64_t* selected_blocks, uint64_t* allowed_blocks,
                              fvsr_stream_t stream);
 
+/* ---- token-mask builders (DEVICE MaskMatrix words for FVSR_MASK_BITMASK) -------------- */
+/* build_segment_mask (P/src/mask.cpp:67-84): bits [L][(L+63)/64] (DEVICE), allowed iff
+ * seg[i] == seg[j].  seg: HOST [L]; ids must be >= 0 and contiguous (FVSR_E_CONFIG). */
+FVSR_API int32_t fvsr_build_segment_mask(fvsr_ctx* ctx, const int32_t* seg, int64_t L, uint64_t* bits,
+                                fvsr_stream_t stream);
+/* build_causal_mask (P/src/mask.cpp:86-101): allowed iff frame[j] <= frame[i] + lookahead.
+ * frame: HOST [L], non-decreasing; lookahead >= 0 (FVSR_E_CONFIG otherwise). */
+FVSR_API int32_t fvsr_build_causal_mask(fvsr_ctx* ctx, const int32_t* frame, int64_t L, int32_t lookahead,
+                               uint64_t* bits, fvsr_stream_t stream);
+
 /* ---- device ring-buffer KV cache (streaming) ---------------------------------------- */
 /* window_frames + 1 slots per (layer, head): the current frame is appended before
  * attention, exactly as step() does (P/src/stream.cpp:228-229; KVCache::validate allows

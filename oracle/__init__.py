@@ -263,6 +263,10 @@ class Ref:
             lib.vsrref_report.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                           C.POINTER(C.c_uint64), C.c_char_p, C.c_int]
             lib.vsrref_dense.argtypes = [C.c_void_p, C.c_float, C.POINTER(C.c_float), C.c_char_p, C.c_int]
+            lib.vsrref_segment_mask.argtypes = [C.POINTER(C.c_int), C.c_long, C.POINTER(C.c_uint64), C.c_char_p,
+                                                C.c_int]
+            lib.vsrref_causal_mask.argtypes = [C.POINTER(C.c_int), C.c_long, C.c_int, C.POINTER(C.c_uint64),
+                                               C.c_char_p, C.c_int]
             lib.vsrref_frame_mass.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_char_p, C.c_int]
             lib.vsrref_kv_evict.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
                                             C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -379,6 +383,28 @@ class Ref:
                                                 _ptr(out, C.c_float) if out is not None else None, err, 512)
             if st:
                 raise OracleError(st, err.value.decode())
+
+    def segment_mask(self, seg) -> np.ndarray:
+        """vsr::build_segment_mask (P/src/mask.cpp:67-84) as MaskMatrix words."""
+        seg = _i32(seg)
+        L = len(seg)
+        out = np.zeros((L, (L + 63) // 64), np.uint64)
+        err = C.create_string_buffer(512)
+        st = self.lib.vsrref_segment_mask(_ptr(seg, C.c_int), L, _ptr(out, C.c_uint64), err, 512)
+        if st:
+            raise OracleError(st, err.value.decode())
+        return out
+
+    def causal_mask(self, frame, lookahead: int) -> np.ndarray:
+        """vsr::build_causal_mask (P/src/mask.cpp:86-101) as MaskMatrix words."""
+        frame = _i32(frame)
+        L = len(frame)
+        out = np.zeros((L, (L + 63) // 64), np.uint64)
+        err = C.create_string_buffer(512)
+        st = self.lib.vsrref_causal_mask(_ptr(frame, C.c_int), L, int(lookahead), _ptr(out, C.c_uint64), err, 512)
+        if st:
+            raise OracleError(st, err.value.decode())
+        return out
 
     def kv_evict(self, strategy: int, window: int, ids, scores: Optional[np.ndarray], heads: int):
         """KVCache(1, heads, window, strategy) holding `ids` on every head, then evict(0, scores)
@@ -505,3 +531,41 @@ def evict(strategy: int, window: int, ids: Sequence[int], scores: Optional[np.nd
         gone = set(evict_victims(ids, list(sc[h]), len(ids) - window))
         out.append([i for i in ids if i not in gone])
     return out
+
+
+# ----------------------------------------------------------------------------
+# Token-mask builders: numpy restatement, MaskMatrix word layout
+# ----------------------------------------------------------------------------
+
+def _pack_rows(allowed: np.ndarray) -> np.ndarray:
+    """bool [L][L] -> uint64 words [L][(L+63)/64], bit j%64 of word j/64 (mask.hpp:16-59)."""
+    L, Lk = allowed.shape
+    wpr = (Lk + 63) // 64
+    pad = np.zeros((L, wpr * 64), bool)
+    pad[:, :Lk] = allowed
+    w = pad.reshape(L, wpr, 64).astype(np.uint64) << np.arange(64, dtype=np.uint64)
+    return np.bitwise_or.reduce(w, axis=2)
+
+
+def segment_mask(seg) -> np.ndarray:
+    """build_segment_mask (P/src/mask.cpp:67-84): allowed iff seg[i] == seg[j]; ids must be
+    >= 0 and contiguous (ConfigError otherwise)."""
+    seg = np.asarray(seg, np.int64)
+    if seg.size < 1:
+        raise OracleError(2, "build_segment_mask: no tokens labeled")
+    if (seg < 0).any():
+        raise OracleError(2, "build_segment_mask: negative segment id")
+    if len(np.unique(seg)) != seg.max() + 1:
+        raise OracleError(2, "build_segment_mask: segment ids not contiguous")
+    return _pack_rows(seg[:, None] == seg[None, :])
+
+
+def causal_mask(frame, lookahead: int) -> np.ndarray:
+    """build_causal_mask (P/src/mask.cpp:86-101): allowed iff frame[j] <= frame[i] + lookahead;
+    frames non-decreasing, lookahead >= 0."""
+    frame = np.asarray(frame, np.int64)
+    if lookahead < 0:
+        raise OracleError(2, "build_causal_mask: negative lookahead")
+    if (np.diff(frame) < 0).any():
+        raise OracleError(2, "build_causal_mask: frame indices must be non-decreasing")
+    return _pack_rows(frame[None, :] <= frame[:, None] + lookahead)

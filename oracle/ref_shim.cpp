@@ -11,6 +11,8 @@
 //   vsr::sparsity_report         P/src/sparse.cpp:256-285
 //   vsr::dense_attention_oracle  P/src/attention.cpp:40-56
 //   vsr::Rng::gaussian           P/include/vsr/rng.hpp:34-48
+//   vsr::build_segment_mask      P/src/mask.cpp:67-84
+//   vsr::build_causal_mask       P/src/mask.cpp:86-101
 //   vsr::frame_attention_mass    P/src/kv_cache.cpp:170-206
 //   vsr::KVCache::evict          P/src/kv_cache.cpp:97-137
 // (P = /root/reference/proj).  The shim only marshals arrays and maps the
@@ -259,6 +261,29 @@ int vsrref_head_attention(vsrref_case* c, long topk, float scale, unsigned threa
     vsr::TensorF32 o =
         vsr::sparse_attention_exec(c->q, c->k, c->v, plan, mask, scale, 0, SIZE_MAX, threads);
     if (out) std::memcpy(out, o.data.data(), o.data.size() * sizeof(float));
+  });
+}
+
+// Token masks from the reference builders, as MaskMatrix words [L][(L+63)/64].
+int vsrref_segment_mask(const int* seg, long L, std::uint64_t* out, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    vsr::SegmentLabels lab;
+    lab.seg.assign(seg, seg + L);
+    const vsr::MaskMatrix m = vsr::build_segment_mask(lab);
+    const std::size_t wpr = m.words_per_row();
+    for (std::size_t i = 0; i < m.rows(); ++i) std::memcpy(out + i * wpr, m.row_words(i), wpr * 8);
+  });
+}
+
+int vsrref_causal_mask(const int* frame, long L, int lookahead, std::uint64_t* out, char* err,
+                       int errlen) {
+  return guarded(err, errlen, [&] {
+    vsr::CausalSpec spec;
+    spec.frame.assign(frame, frame + L);
+    spec.lookahead = lookahead;
+    const vsr::MaskMatrix m = vsr::build_causal_mask(spec, static_cast<std::size_t>(L));
+    const std::size_t wpr = m.words_per_row();
+    for (std::size_t i = 0; i < m.rows(); ++i) std::memcpy(out + i * wpr, m.row_words(i), wpr * 8);
   });
 }
 

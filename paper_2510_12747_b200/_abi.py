@@ -102,6 +102,8 @@ SIGNATURES = {
     "fvsr_ring_frame_ids": (I32, [P, I32, C.POINTER(I32), I32, C.POINTER(I32)]),
     "fvsr_ring_attention": (I32, [P, P, I32, P, C.POINTER(I32), I32, MP, I64, F32, I64, I64, P, I32, I32, P, P,
                                   P]),
+    "fvsr_build_segment_mask": (I32, [P, C.POINTER(I32), I64, P, P]),
+    "fvsr_build_causal_mask": (I32, [P, C.POINTER(I32), I64, I32, P, P]),
     "fvsr_frame_attention_mass": (I32, [P, I32, GP, GP, MP, P, P, P]),
     "fvsr_ring_frame_mass": (I32, [P, P, I32, C.POINTER(I32), I32, MP, P, P]),
     "fvsr_ring_evict": (I32, [P, I32, I32, P]),

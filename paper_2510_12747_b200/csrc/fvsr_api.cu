@@ -1114,10 +1114,11 @@ int32_t fvsr_frame_attention_mass(fvsr_ctx* ctx, int32_t heads, const fvsr_grid*
 int32_t fvsr_ring_frame_mass(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const int32_t* q_frame_ids, int32_t nq,
                              const fvsr_mask* mask, double* mass, fvsr_stream_t stream) {
   FVSR_TRY(check_ctx(ctx));
-  if (!r || !q_frame_ids || !mass) return fail(FVSR_E_SHAPE, "ring_frame_mass: null argument");
+  if (!r || !q_frame_ids) return fail(FVSR_E_SHAPE, "ring_frame_mass: null argument");
   if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
   const auto& c = r->ctx[layer];
   if (c.empty()) return fail(FVSR_E_CONFIG, "ring_frame_mass: empty context");
+  if (!mass) return fail(FVSR_E_SHAPE, "ring_frame_mass: null output");
   std::vector<int> kids, kslots;
   for (auto& fs : c) {
     kids.push_back(fs.first);
@@ -1171,6 +1172,62 @@ int32_t fvsr_ring_evict(fvsr_ring* r, int32_t layer, int32_t strategy, const dou
         break;
       }
   return FVSR_OK;
+}
+
+// ---- token-mask builders ----------------------------------------------------
+namespace {
+int launch_token_mask(fvsr_ctx* ctx, const int32_t* labels_host, long long L, int kind, int lookahead,
+                      uint64_t* bits, cudaStream_t s) {
+  const size_t smem = (size_t)L * sizeof(int);
+  if (smem > 200 * 1024) return fail(FVSR_E_CONFIG, "token mask: %lld tokens exceed the builder limit", L);
+  int st;
+  void* ws = ws_get(ctx, smem, &st);
+  if (!ws) return st;
+  FVSR_CUDA(cudaMemcpyAsync(ws, labels_host, smem, cudaMemcpyHostToDevice, s));
+  static size_t configured = 48 * 1024;
+  if (smem > configured) {
+    FVSR_CUDA(cudaFuncSetAttribute(token_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  int sms = 148;
+  (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const long long tasks = L * (((L + 63) / 64 + 31) / 32);
+  const long long ctas = std::min<long long>((tasks + kMaskThreads / 32 - 1) / (kMaskThreads / 32), 4LL * sms);
+  FVSR_CUDA(launch_k(token_mask_kernel, dim3((unsigned)ctas), dim3(kMaskThreads), smem, s,
+                     static_cast<const int*>(ws), L, kind, lookahead, reinterpret_cast<unsigned long long*>(bits)));
+  // the host labels may be released on return (pageable copy is staged before returning)
+  return after_launch(ctx, s, 1);
+}
+}  // namespace
+
+int32_t fvsr_build_segment_mask(fvsr_ctx* ctx, const int32_t* seg, int64_t L, uint64_t* bits,
+                                fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  if (!bits || (L > 0 && !seg)) return fail(FVSR_E_SHAPE, "build_segment_mask: null argument");
+  // P/src/mask.cpp:69-78
+  if (L < 1) return fail(FVSR_E_CONFIG, "build_segment_mask: no tokens labeled");
+  int max_id = -1;
+  for (long long i = 0; i < L; ++i) {
+    if (seg[i] < 0) return fail(FVSR_E_CONFIG, "build_segment_mask: negative segment id");
+    max_id = std::max(max_id, (int)seg[i]);
+  }
+  std::vector<char> seen((size_t)max_id + 1, 0);
+  for (long long i = 0; i < L; ++i) seen[(size_t)seg[i]] = 1;
+  for (char c : seen)
+    if (!c) return fail(FVSR_E_CONFIG, "build_segment_mask: segment ids not contiguous");
+  return launch_token_mask(ctx, seg, L, 0, 0, bits, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int32_t fvsr_build_causal_mask(fvsr_ctx* ctx, const int32_t* frame, int64_t L, int32_t lookahead, uint64_t* bits,
+                               fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  if (!bits || (L > 0 && !frame)) return fail(FVSR_E_SHAPE, "build_causal_mask: null argument");
+  if (L < 1) return fail(FVSR_E_SHAPE, "build_causal_mask: frame list length does not match L");
+  // P/src/mask.cpp:89-92
+  if (lookahead < 0) return fail(FVSR_E_CONFIG, "build_causal_mask: negative lookahead");
+  for (long long i = 1; i < L; ++i)
+    if (frame[i] < frame[i - 1]) return fail(FVSR_E_CONFIG, "build_causal_mask: frame indices must be non-decreasing");
+  return launch_token_mask(ctx, frame, L, 1, lookahead, bits, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int32_t fvsr_ring_step_host(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* q_host,

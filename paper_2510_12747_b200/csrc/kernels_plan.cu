@@ -889,4 +889,47 @@ __global__ void __launch_bounds__(kMassThreads) frame_mass_kernel(const __grid_c
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// token-mask builders: build_segment_mask / build_causal_mask
+// (P/src/mask.cpp:67-101) straight into MaskMatrix words ([L][(L+63)/64] uint64, bit j of
+// row i = mask(i, j), P/include/vsr/mask.hpp:16-59).  Byte work, HBM-write bound: the labels
+// are staged in shared memory once per CTA; a warp builds 32 consecutive words of a row with
+// two ballots per word (lane b tests keys 64w+b and 64w+32+b, conflict-free), keeps word
+// w in lane w%32 and stores the 32 words as one coalesced 256 B run.
+// kind 0: segment (seg[i] == seg[j]); kind 1: causal (frame[j] <= frame[i] + lookahead).
+// ---------------------------------------------------------------------------------------
+constexpr int kMaskThreads = 256;
+
+__global__ void __launch_bounds__(kMaskThreads) token_mask_kernel(const int* __restrict__ labels, long long L,
+                                                                  int kind, int lookahead,
+                                                                  unsigned long long* __restrict__ bits) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ int tm_lab[];
+  for (long long j = threadIdx.x; j < L; j += kMaskThreads) tm_lab[j] = labels[j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long wpr = (L + 63) / 64;
+  const long long groups = (wpr + 31) / 32;  // 32-word runs per row
+  const long long total = L * groups;
+  const long long warp_id = (long long)blockIdx.x * (kMaskThreads / 32) + (threadIdx.x >> 5);
+  const long long nwarps = (long long)gridDim.x * (kMaskThreads / 32);
+  for (long long task = warp_id; task < total; task += nwarps) {
+    const long long i = task / groups;
+    const long long w0 = (task - i * groups) * 32;
+    const int li = tm_lab[i];
+    const int limit = li + lookahead;
+    unsigned long long mine = 0;
+    for (int u = 0; u < 32 && w0 + u < wpr; ++u) {
+      const long long j0 = (w0 + u) * 64 + lane, j1 = j0 + 32;
+      bool a = false, b = false;
+      if (j0 < L) a = kind == 0 ? tm_lab[j0] == li : tm_lab[j0] <= limit;
+      if (j1 < L) b = kind == 0 ? tm_lab[j1] == li : tm_lab[j1] <= limit;
+      const unsigned lo = __ballot_sync(0xffffffffu, a), hi = __ballot_sync(0xffffffffu, b);
+      if (lane == u) mine = ((unsigned long long)hi << 32) | lo;
+    }
+    if (w0 + lane < wpr) bits[i * wpr + w0 + lane] = mine;
+  }
+}
+
 }  // namespace fvsr

@@ -279,6 +279,37 @@ def sparse_attention_exec(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pla
     return out[0] if squeeze else out
 
 
+def _labels(x, name):
+    a = torch.as_tensor(x).detach().to("cpu", torch.int32).contiguous()
+    if a.dim() != 1:
+        raise ShapeError(f"{name}: labels must be 1-D")
+    return a
+
+
+def build_segment_mask(seg, *, ctx: Optional[Context] = None, device=None) -> Mask:
+    """build_segment_mask (P/src/mask.cpp:67-84) on device -> a bitmask Mask (Lq = Lk = L)."""
+    ctx = ctx or Context.default()
+    lab = _labels(seg, "build_segment_mask")
+    L = lab.numel()
+    bits = torch.empty((max(L, 1), (L + 63) // 64 or 1), dtype=torch.int64,
+                       device=device or torch.device("cuda", torch.cuda.current_device()))
+    check(ctx.lib.fvsr_build_segment_mask(ctx.h, C.cast(lab.data_ptr(), C.POINTER(C.c_int32)), L, bits.data_ptr(),
+                                          _stream()))
+    return Mask.bitmask(bits)
+
+
+def build_causal_mask(frame, lookahead: int = 0, *, ctx: Optional[Context] = None, device=None) -> Mask:
+    """build_causal_mask (P/src/mask.cpp:86-101) on device -> a bitmask Mask."""
+    ctx = ctx or Context.default()
+    lab = _labels(frame, "build_causal_mask")
+    L = lab.numel()
+    bits = torch.empty((max(L, 1), (L + 63) // 64 or 1), dtype=torch.int64,
+                       device=device or torch.device("cuda", torch.cuda.current_device()))
+    check(ctx.lib.fvsr_build_causal_mask(ctx.h, C.cast(lab.data_ptr(), C.POINTER(C.c_int32)), L, int(lookahead),
+                                         bits.data_ptr(), _stream()))
+    return Mask.bitmask(bits)
+
+
 def frame_attention_mass(plan: SparsePlan, key_grid: Optional[TokenGrid] = None, mask: Optional[Mask] = None, *,
                          ctx: Optional[Context] = None, check_errors: bool = True) -> torch.Tensor:
     """frame_attention_mass (P/src/kv_cache.cpp:170-206) on device: float64 [heads, frames]
@@ -287,16 +318,16 @@ def frame_attention_mass(plan: SparsePlan, key_grid: Optional[TokenGrid] = None,
     ctx = ctx or Context.default()
     mask = mask or Mask.all_allowed()
     key_grid = key_grid or plan.grid_k
-    if plan.coarse is None:
+    if plan.coarse_scores is None:
         raise ConfigError("frame_attention_mass: plan was built without coarse scores (keep_scores=False)")
     if key_grid.token_count() != plan.grid_k.token_count():
         raise ShapeError("frame_attention_mass: plan does not match key grid")
-    mass = torch.empty((plan.heads, key_grid.frame_count()), dtype=torch.float64, device=plan.coarse.device)
+    mass = torch.empty((plan.heads, key_grid.frame_count()), dtype=torch.float64, device=plan.coarse_scores.device)
     gq, kq = plan.grid_q.c()
     gk, kk = key_grid.c()
     md = mask.c()
     check(ctx.lib.fvsr_frame_attention_mass(ctx.h, plan.heads, C.byref(gq), C.byref(gk), C.byref(md),
-                                            plan.coarse.data_ptr(), mass.data_ptr(), _stream()))
+                                            plan.coarse_scores.data_ptr(), mass.data_ptr(), _stream()))
     if check_errors:
         ctx.check_errors()
     return mass

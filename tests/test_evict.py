@@ -78,3 +78,29 @@ def test_oracle_frame_mass_matches_reference_seeded(seed, qf, kf, spec):
     c = oracle.Ref().case(q, k, v, qf, kf, rows, cols, _mask(spec))
     plan = c.plan(3)
     assert np.array_equal(oracle.frame_attention_mass(plan, kf, rows, cols), c.frame_mass())
+
+
+# ---- token-mask builders ------------------------------------------------
+MASKS = os.path.join(HERE, "golden", "token_masks.npz")
+MASK_SIZES = (1, 63, 64, 65, 300, 768)
+
+
+@pytest.mark.parametrize("L", MASK_SIZES)
+def test_oracle_token_masks_match_reference_fixture(L):
+    z = np.load(MASKS)
+    assert np.array_equal(oracle.segment_mask(z[f"seg{L}.labels"]), z[f"seg{L}.bits"])
+    for la in (0, 1):
+        assert np.array_equal(oracle.causal_mask(z[f"causal{L}.labels"], la), z[f"causal{L}.la{la}.bits"])
+
+
+@pytest.mark.parametrize("bad", [[0, 2], [-1, 0], []])
+def test_oracle_segment_mask_errors(bad):  # mask.cpp:69-78
+    with pytest.raises(oracle.OracleError):
+        oracle.segment_mask(bad)
+
+
+def test_oracle_causal_mask_errors():  # mask.cpp:87-92
+    with pytest.raises(oracle.OracleError):
+        oracle.causal_mask([1, 0], 0)
+    with pytest.raises(oracle.OracleError):
+        oracle.causal_mask([0, 1], -1)

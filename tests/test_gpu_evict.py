@@ -42,7 +42,7 @@ def test_frame_mass_matches_reference_fixture(idx):
     fmask, _ = _masks(c["mask"])
     gq, gk = fv.TokenGrid(c["qf"], c["rows"], c["cols"]), fv.TokenGrid(c["kf"], c["rows"], c["cols"])
     plan = fv.plan_sparse(to_dev(q[None]), to_dev(k[None]), gq, gk, fmask, c["topk"])
-    assert np.array_equal(plan.coarse[0].cpu().numpy().view(np.uint32), z[f"{c['name']}.coarse"].view(np.uint32))
+    assert np.array_equal(plan.coarse_scores[0].cpu().numpy().view(np.uint32), z[f"{c['name']}.coarse"].view(np.uint32))
     mass = fv.frame_attention_mass(plan, gk, fmask).cpu().numpy()[0]
     want = z[f"{c['name']}.mass"]
     assert _close(mass, want), (mass, want)
