@@ -202,6 +202,15 @@ FVSR_API void fvsr_ring_destroy(fvsr_ring* ring);
 /* KVCache::append for every head of `layer`: k, v are [heads][rows*cols][d] (DEVICE). */
 FVSR_API int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer, int32_t frame_id,
                          const uint16_t* k, const uint16_t* v, fvsr_stream_t stream);
+/* Fused RoPE: from now on fvsr_ring_append rotates K and fvsr_ring_attention
+ * rotates Q at their absolute (frame, row, col) positions inside the pack/pool pass, before
+ * pooling and the tensor-core layout — apply_rope (P/src/rope.cpp:30-62) as make_frame_kv /
+ * step call it (P/src/stream.cpp:134-152, 240), without an HBM round trip.  Inputs are then
+ * the un-rotated projections.  theta0 > 1; axis_split = channels for (t, h, w), positive,
+ * even, summing to d (NULL = RopeConfig::split_default: d/2, d/4, d/4).  Rotation is fp32
+ * without FMA from the reference's float-rounded double cos/sin, then bf16 RNE: bit-exact
+ * with bf16(apply_rope(x)).  At most 4 query frames per fvsr_ring_attention call. */
+FVSR_API int32_t fvsr_ring_set_rope(fvsr_ring* ring, double theta0, const int32_t* axis_split);
 /* KVCache::evict with the sliding_window strategy (P/src/kv_cache.cpp:100-106). */
 FVSR_API int32_t fvsr_ring_evict_sliding(fvsr_ring* ring, int32_t layer);
 /* Sliding eviction down to `keep` frames (oldest first).  Chunked streaming of Tq frames per

@@ -263,6 +263,8 @@ class Ref:
             lib.vsrref_report.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                           C.POINTER(C.c_uint64), C.c_char_p, C.c_int]
             lib.vsrref_dense.argtypes = [C.c_void_p, C.c_float, C.POINTER(C.c_float), C.c_char_p, C.c_int]
+            lib.vsrref_apply_rope.argtypes = [C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                              C.POINTER(C.c_int), C.POINTER(C.c_float), C.c_char_p, C.c_int]
             lib.vsrref_segment_mask.argtypes = [C.POINTER(C.c_int), C.c_long, C.POINTER(C.c_uint64), C.c_char_p,
                                                 C.c_int]
             lib.vsrref_causal_mask.argtypes = [C.POINTER(C.c_int), C.c_long, C.c_int, C.POINTER(C.c_uint64),
@@ -383,6 +385,18 @@ class Ref:
                                                 _ptr(out, C.c_float) if out is not None else None, err, 512)
             if st:
                 raise OracleError(st, err.value.decode())
+
+    def apply_rope(self, x, frame_ids, rows: int, cols: int, theta0: float = 10000.0, axis_split=None):
+        """vsr::apply_rope over TokenGrid(frame_ids, rows, cols).positions() (P/src/rope.cpp:30-62)."""
+        x = np.array(x, dtype=np.float32, copy=True, order="C")
+        fids = _i32(frame_ids)
+        sp = None if axis_split is None else _i32(axis_split)
+        err = C.create_string_buffer(512)
+        st = self.lib.vsrref_apply_rope(_ptr(fids, C.c_int), len(fids), rows, cols, x.shape[1], float(theta0),
+                                        _ptr(sp, C.c_int) if sp is not None else None, _ptr(x, C.c_float), err, 512)
+        if st:
+            raise OracleError(st, err.value.decode())
+        return x
 
     def segment_mask(self, seg) -> np.ndarray:
         """vsr::build_segment_mask (P/src/mask.cpp:67-84) as MaskMatrix words."""
@@ -569,3 +583,38 @@ def causal_mask(frame, lookahead: int) -> np.ndarray:
     if (np.diff(frame) < 0).any():
         raise OracleError(2, "build_causal_mask: frame indices must be non-decreasing")
     return _pack_rows(frame[None, :] <= frame[:, None] + lookahead)
+
+
+# ----------------------------------------------------------------------------
+# RoPE: numpy restatement of apply_rope
+# ----------------------------------------------------------------------------
+
+def apply_rope(x: np.ndarray, frame_ids: Sequence[int], rows: int, cols: int, theta0: float = 10000.0,
+               axis_split=None) -> np.ndarray:
+    """apply_rope (P/src/rope.cpp:30-62) at TokenGrid positions (t = absolute frame id, h, w;
+    P/include/vsr/grid.hpp:74-79): per axis pair i, inv_freq = theta0^(-2i/d_axis) and
+    angle = pos * inv_freq in double (libm pow/cos/sin), cos/sin rounded to float, then
+    x0*c - x1*s and x0*s + x1*c in fp32 with separate multiply and add.  Default split
+    RopeConfig::split_default: (d/2, d/4, d/4)."""
+    x = np.asarray(x, np.float32)
+    L, d = x.shape
+    split = list(axis_split) if axis_split is not None else [d // 2, d // 4, d // 4]
+    n = rows * cols
+    tok = np.arange(L)
+    pos = [np.asarray(frame_ids, np.int64)[tok // n], (tok % n) // cols, tok % cols]
+    out = x.copy()
+    base = 0
+    for axis in range(3):
+        da = split[axis]
+        for i in range(da // 2):
+            inv = math.pow(theta0, -2.0 * i / float(da))
+            vals = np.unique(pos[axis])
+            c_of = {int(p): np.float32(math.cos(1.0 * int(p) * inv)) for p in vals}
+            s_of = {int(p): np.float32(math.sin(1.0 * int(p) * inv)) for p in vals}
+            c = np.array([c_of[int(p)] for p in pos[axis]], np.float32)
+            s = np.array([s_of[int(p)] for p in pos[axis]], np.float32)
+            x0, x1 = x[:, base + 2 * i], x[:, base + 2 * i + 1]
+            out[:, base + 2 * i] = (x0 * c) - (x1 * s)
+            out[:, base + 2 * i + 1] = (x0 * s) + (x1 * c)
+        base += da
+    return out

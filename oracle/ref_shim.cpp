@@ -13,6 +13,7 @@
 //   vsr::Rng::gaussian           P/include/vsr/rng.hpp:34-48
 //   vsr::build_segment_mask      P/src/mask.cpp:67-84
 //   vsr::build_causal_mask       P/src/mask.cpp:86-101
+//   vsr::apply_rope              P/src/rope.cpp:30-62
 //   vsr::frame_attention_mass    P/src/kv_cache.cpp:170-206
 //   vsr::KVCache::evict          P/src/kv_cache.cpp:97-137
 // (P = /root/reference/proj).  The shim only marshals arrays and maps the
@@ -25,6 +26,8 @@
 
 #include "vsr/attention.hpp"
 #include "vsr/kv_cache.hpp"
+#include "vsr/rope.hpp"
+#include "vsr/grid.hpp"
 #include "vsr/mask.hpp"
 #include "vsr/partition.hpp"
 #include "vsr/rng.hpp"
@@ -261,6 +264,24 @@ int vsrref_head_attention(vsrref_case* c, long topk, float scale, unsigned threa
     vsr::TensorF32 o =
         vsr::sparse_attention_exec(c->q, c->k, c->v, plan, mask, scale, 0, SIZE_MAX, threads);
     if (out) std::memcpy(out, o.data.data(), o.data.size() * sizeof(float));
+  });
+}
+
+// apply_rope over a TokenGrid's positions (x: [frames*rows*cols][d] fp32, in place).
+// axis_split NULL -> RopeConfig::split_default(d).
+int vsrref_apply_rope(const int* fids, int nf, int rows, int cols, int d, double theta0,
+                      const int* axis_split, float* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const vsr::TokenGrid g(std::vector<int>(fids, fids + nf), static_cast<std::size_t>(rows),
+                           static_cast<std::size_t>(cols));
+    vsr::RopeConfig rc = vsr::RopeConfig::split_default(d);
+    if (axis_split) rc.axis_split = {axis_split[0], axis_split[1], axis_split[2]};
+    rc.theta0 = theta0;
+    const std::size_t L = g.token_count();
+    vsr::TensorF32 t({L, static_cast<std::size_t>(d)},
+                     std::vector<float>(x, x + L * static_cast<std::size_t>(d)));
+    const vsr::TensorF32 o = vsr::apply_rope(t, g.positions(), rc);
+    std::memcpy(x, o.data.data(), o.data.size() * sizeof(float));
   });
 }
 

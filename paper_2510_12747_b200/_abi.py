@@ -97,6 +97,7 @@ SIGNATURES = {
     "fvsr_ring_create": (I32, [P, I32, I32, I32, I32, I32, I32, C.POINTER(P)]),
     "fvsr_ring_destroy": (None, [P]),
     "fvsr_ring_append": (I32, [P, P, I32, I32, P, P, P]),
+    "fvsr_ring_set_rope": (I32, [P, C.c_double, C.POINTER(I32)]),
     "fvsr_ring_evict_sliding": (I32, [P, I32]),
     "fvsr_ring_evict_keep": (I32, [P, I32, I32]),
     "fvsr_ring_frame_ids": (I32, [P, I32, C.POINTER(I32), I32, C.POINTER(I32)]),

@@ -99,6 +99,14 @@ struct fvsr_ring {
   float* s0 = nullptr;
   float* s1 = nullptr;
   float* kn2 = nullptr;  // max squared key-row norm per (layer, head, slot, tile)
+  // fused RoPE (fvsr_ring_set_rope): device (cos, sin) tables per axis position
+  bool rope = false;
+  double rope_theta0 = 10000.0;
+  int rope_split[3] = {0, 0, 0};
+  float2* rope_t = nullptr;  // [rope_t_cap][split0/2]
+  float2* rope_h = nullptr;  // [rows][split1/2]
+  float2* rope_w = nullptr;  // [cols][split2/2]
+  int rope_t_cap = 0;
   std::vector<std::vector<std::pair<int, int>>> ctx;  // per layer: (frame_id, slot), ascending
   std::vector<std::vector<char>> used;                // per layer: slot occupancy
   long long kv_head_stride() const { return (long long)slots * n_tiles * (long long)tile_bytes; }
@@ -865,7 +873,98 @@ void fvsr_ring_destroy(fvsr_ring* ring) {
   cudaFree(ring->s0);
   cudaFree(ring->s1);
   cudaFree(ring->kn2);
+  cudaFree(ring->rope_t);
+  cudaFree(ring->rope_h);
+  cudaFree(ring->rope_w);
   delete ring;
+}
+
+// ---- fused RoPE tables (apply_rope, P/src/rope.cpp:30-62) ------------------------------------
+namespace {
+// (cos, sin) of pos * theta0^(-2i/d_axis) for pos in [p0, p1): the reference's double math,
+// rounded to float exactly as apply_rope does
+std::vector<float2> rope_table(double theta0, int d_axis, int p0, int p1) {
+  std::vector<float2> t((size_t)(p1 - p0) * (d_axis / 2));
+  for (int p = p0; p < p1; ++p)
+    for (int i = 0; i < d_axis / 2; ++i) {
+      const double inv_freq = std::pow(theta0, -2.0 * i / static_cast<double>(d_axis));
+      const double angle = 1.0 * p * inv_freq;
+      t[(size_t)(p - p0) * (d_axis / 2) + i] = make_float2(static_cast<float>(std::cos(angle)),
+                                                           static_cast<float>(std::sin(angle)));
+    }
+  return t;
+}
+
+// frame ids [0, need) covered by the t-axis table (grown on demand; synchronous, rare)
+int rope_reserve_t(fvsr_ring* r, int need) {
+  if (need <= r->rope_t_cap) return FVSR_OK;
+  int cap = std::max(need, std::max(1024, 2 * r->rope_t_cap));
+  const std::vector<float2> t = rope_table(r->rope_theta0, r->rope_split[0], 0, cap);
+  float2* d = nullptr;
+  if (cudaMalloc(&d, t.size() * sizeof(float2)) != cudaSuccess)
+    return fail(FVSR_E_NOMEM, "rope table allocation failed");
+  FVSR_CUDA(cudaMemcpy(d, t.data(), t.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  if (r->rope_t) {
+    FVSR_CUDA(cudaDeviceSynchronize());  // in-flight kernels may still read the old table
+    cudaFree(r->rope_t);
+  }
+  r->rope_t = d;
+  r->rope_t_cap = cap;
+  return FVSR_OK;
+}
+
+int rope_args(fvsr_ring* r, const int* fids, int n, PackPoolArgs& a) {
+  if (!r->rope) return FVSR_OK;
+  if (n > 4) return fail(FVSR_E_CONFIG, "fused RoPE: at most 4 query frames per call (got %d)", n);
+  int mx = 0;
+  for (int i = 0; i < n; ++i) mx = std::max(mx, fids[i]);
+  FVSR_TRY(rope_reserve_t(r, mx + 1));
+  a.rope_t = r->rope_t;
+  a.rope_h = r->rope_h;
+  a.rope_w = r->rope_w;
+  a.rope_dt = r->rope_split[0];
+  a.rope_dh = r->rope_split[1];
+  a.rope_dw = r->rope_split[2];
+  for (int i = 0; i < n; ++i) a.rope_fid[i] = fids[i];
+  return FVSR_OK;
+}
+}  // namespace
+
+int32_t fvsr_ring_set_rope(fvsr_ring* r, double theta0, const int32_t* axis_split) {
+  if (!r) return fail(FVSR_E_CONFIG, "null ring");
+  int split[3];
+  if (axis_split) {
+    for (int i = 0; i < 3; ++i) split[i] = axis_split[i];
+  } else {  // RopeConfig::split_default (P/src/rope.cpp:11-17), StreamConfig::rope (stream.cpp:8-10)
+    split[0] = r->d / 2;
+    split[1] = r->d / 4;
+    split[2] = r->d / 4;
+  }
+  // RopeConfig::validate (P/src/rope.cpp:19-28)
+  int sum = 0;
+  for (int part : split) {
+    if (part <= 0 || part % 2 != 0) return fail(FVSR_E_CONFIG, "RopeConfig: axis split parts must be positive and even");
+    sum += part;
+  }
+  if (sum != r->d) return fail(FVSR_E_CONFIG, "RopeConfig: axis split must sum to dim");
+  if (!(theta0 > 1.0)) return fail(FVSR_E_CONFIG, "RopeConfig: theta0 must exceed 1");
+  r->rope_theta0 = theta0;
+  for (int i = 0; i < 3; ++i) r->rope_split[i] = split[i];
+  FVSR_CUDA(cudaDeviceSynchronize());
+  cudaFree(r->rope_t);
+  cudaFree(r->rope_h);
+  cudaFree(r->rope_w);
+  r->rope_t = r->rope_h = r->rope_w = nullptr;
+  r->rope_t_cap = 0;
+  const std::vector<float2> th = rope_table(theta0, split[1], 0, r->rows);
+  const std::vector<float2> tw = rope_table(theta0, split[2], 0, r->cols);
+  if (cudaMalloc(&r->rope_h, th.size() * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&r->rope_w, tw.size() * sizeof(float2)) != cudaSuccess)
+    return fail(FVSR_E_NOMEM, "rope table allocation failed");
+  FVSR_CUDA(cudaMemcpy(r->rope_h, th.data(), th.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  FVSR_CUDA(cudaMemcpy(r->rope_w, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  r->rope = true;
+  return rope_reserve_t(r, 1);
 }
 
 int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* k,
@@ -914,6 +1013,7 @@ int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t fra
   a.tiles_w = r->tiles_w;
   a.n_tiles = r->n_tiles;
   a.d = r->d;
+  FVSR_TRY(rope_args(r, &frame_id, 1, a));
   PoolGroups pg{};
   pg.first[0] = 0;
   pg.count[0] = 1;
@@ -1022,6 +1122,7 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
     a.tiles_w = g.tiles_w;
     a.n_tiles = g.n_tiles;
     a.d = d;
+    FVSR_TRY(rope_args(r, q_frame_ids, nq, a));
     PoolGroups pg{};
     SlotList sl{};
     for (int t = 0; t < g.nq_trows; ++t) {

@@ -155,6 +155,13 @@ struct PackPoolArgs {
   float* norm2;                // optional: max squared row norm of src per frame-tile [slot][tile]
   long long norm2_head_stride; // elements
   int rows, cols, tiles_w, n_tiles, d;
+  // optional fused RoPE of src (apply_rope, P/src/rope.cpp:30-62) before pooling / packing:
+  // (cos, sin) tables per axis position, float-rounded from the reference's double math
+  const float2* rope_t;  // [frame id][dt/2]
+  const float2* rope_h;  // [row][dh/2]
+  const float2* rope_w;  // [col][dw/2]
+  int rope_dt, rope_dh, rope_dw;
+  int rope_fid[4];       // absolute frame id of source frame index 0..3
 };
 
 constexpr int kPPThreads = 128;
@@ -204,6 +211,30 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
   }
   __syncthreads();
   mbar_wait(bar, 0);
+  if (a.rope_t) {  // rotate the staged src rows in place: x0*c - x1*s, x0*s + x1*c (no FMA), bf16 RNE
+    const int npairs = d >> 1, ht = a.rope_dt >> 1, hh = a.rope_dh >> 1, hw = a.rope_dw >> 1;
+    for (int fi = 0; fi < cnt; ++fi) {
+      uint8_t* st = stage(fi, 0);
+      const float2* tt = a.rope_t + (long long)a.rope_fid[f0 + fi] * ht;
+      for (int e = tid; e < 64 * npairs; e += kPPThreads) {
+        const int r = e / npairs, pi = e - r * npairs;
+        const int rh = r >> 3, rw = r & 7;
+        if (rh >= hc || rw >= wc) continue;
+        float2 cs;
+        if (pi < ht) cs = tt[pi];
+        else if (pi < ht + hh) cs = a.rope_h[(8 * th + rh) * hh + (pi - ht)];
+        else cs = a.rope_w[(8 * tw + rw) * hw + (pi - ht - hh)];
+        uint32_t* pp = reinterpret_cast<uint32_t*>(st + (r * d + 2 * pi) * 2);
+        const uint32_t v = *pp;
+        const float x0 = __uint_as_float(v << 16), x1 = __uint_as_float(v & 0xffff0000u);
+        const float y0 = __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
+        const float y1 = __fadd_rn(__fmul_rn(x0, cs.y), __fmul_rn(x1, cs.x));
+        const __nv_bfloat162 b = __floats2bfloat162_rn(y0, y1);
+        *pp = *reinterpret_cast<const uint32_t*>(&b);
+      }
+    }
+    __syncthreads();
+  }
   // pooling (exact token order; rows past the frame are skipped, not added as zeros)
   if (2 * tid < d) {
     const int c = 2 * tid;

@@ -64,6 +64,12 @@ class KVRing:
         check(self.ctx.lib.fvsr_ring_append(self.ctx.h, self.h, layer, int(frame_id), k3.data_ptr(), v3.data_ptr(),
                                             _stream()))
 
+    def set_rope(self, theta0: float = 10000.0, axis_split: Optional[Sequence[int]] = None) -> None:
+        """Fuse apply_rope (P/src/rope.cpp:30-62) into the ring: append rotates K and attention
+        rotates Q at absolute (frame, row, col) positions; inputs become un-rotated projections."""
+        sp = None if axis_split is None else (C.c_int32 * 3)(*[int(a) for a in axis_split])
+        check(self.ctx.lib.fvsr_ring_set_rope(self.h, float(theta0), sp))
+
     def evict(self, layer: int, keep: Optional[int] = None) -> None:
         """KVCache::evict(sliding): down to the window, or to `keep` frames (chunked streaming)."""
         if keep is None:
