@@ -303,12 +303,15 @@ int launch_pack_pool(const PackPoolArgs& a, const PoolGroups& pg, const SlotList
   if ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.src2)) % 16 != 0)
     return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
   const size_t smem = pack_pool_smem(a.d, max_cnt, a.src2 != nullptr);
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
-    FVSR_CUDA(cudaFuncSetAttribute(pack_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
+  // the RoPE variant is a separate instantiation so the plain pack/pool pass is unchanged
+  auto kern = a.rope_t ? pack_pool_kernel<true> : pack_pool_kernel<false>;
+  static size_t configured[2] = {48 * 1024, 48 * 1024};
+  size_t& conf = configured[a.rope_t ? 1 : 0];
+  if (smem > conf) {
+    FVSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    conf = smem;
   }
-  FVSR_CUDA(launch_k(pack_pool_kernel, dim3(grid), dim3(kPPThreads), smem, s, a, pg, sl));
+  FVSR_CUDA(launch_k(kern, dim3(grid), dim3(kPPThreads), smem, s, a, pg, sl));
   return FVSR_OK;
 }
 

@@ -171,6 +171,7 @@ inline size_t pack_pool_smem(int d, int max_cnt, bool two) {
   return (size_t)max_cnt * (two ? 2 : 1) * 64 * d * 2 + 16;
 }
 
+template <bool ROPE>
 __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_constant__ PackPoolArgs a,
                                                                const __grid_constant__ PoolGroups groups,
                                                                const __grid_constant__ SlotList slots) {
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
   }
   __syncthreads();
   mbar_wait(bar, 0);
-  if (a.rope_t) {  // rotate the staged src rows in place: x0*c - x1*s, x0*s + x1*c (no FMA), bf16 RNE
+  if constexpr (ROPE) {  // rotate the staged src rows in place: x0*c - x1*s, x0*s + x1*c (no FMA), bf16 RNE
     const int npairs = d >> 1, ht = a.rope_dt >> 1, hh = a.rope_dh >> 1, hw = a.rope_dw >> 1;
     for (int fi = 0; fi < cnt; ++fi) {
       uint8_t* st = stage(fi, 0);

@@ -35,7 +35,7 @@ from paper_2510_12747_b200 import _abi  # noqa: E402
 PEAK = 1700.6
 
 
-def run_point(rows, cols, heads, d, window, topk, mask, nq=1, layers=8, steps=40, warmup=8, seed=7):
+def run_point(rows, cols, heads, d, window, topk, mask, nq=1, layers=8, steps=40, warmup=8, seed=7, rope=False):
     dev = torch.device("cuda")
     ctx = fv.Context.default()
     n = rows * cols
@@ -44,6 +44,8 @@ def run_point(rows, cols, heads, d, window, topk, mask, nq=1, layers=8, steps=40
              for i in range(3)] for _ in range(3)]
     # chunks of nq frames: W + nq slots, evict to W before each chunk
     ring = fv.KVRing(layers, heads, d, rows, cols, window + nq - 1, ctx=ctx)
+    if rope:  # fused apply_rope in append (K) and the mask builder's Q pass
+        ring.set_rope()
     t0 = 2 * window + 4
     for l in range(layers):
         for f in range(t0 - window, t0):
@@ -111,6 +113,7 @@ def main():
     all_ = fv.Mask.all_allowed()
     # headline shape and the Tq=2 chunk
     add("768x1408 W4 k27 (headline)", rows=48, cols=88, heads=12, d=128, window=4, topk=27, mask=all_)
+    add("768x1408 W4 k27 fused RoPE", rows=48, cols=88, heads=12, d=128, window=4, topk=27, mask=all_, rope=True)
     add("768x1408 Tq=2 chunk W4 k36", rows=48, cols=88, heads=12, d=128, window=4, topk=36, mask=all_, nq=2)
     # 1440p
     add("1440p W4 k98 all-allowed", rows=90, cols=160, heads=12, d=128, window=4, topk=98, mask=all_, layers=4)
