@@ -951,6 +951,7 @@ int32_t fvsr_ring_set_rope(fvsr_ring* r, double theta0, const int32_t* axis_spli
   }
   if (sum != r->d) return fail(FVSR_E_CONFIG, "RopeConfig: axis split must sum to dim");
   if (!(theta0 > 1.0)) return fail(FVSR_E_CONFIG, "RopeConfig: theta0 must exceed 1");
+  if (kPPThreads % (r->d / 2) != 0) return fail(FVSR_E_CONFIG, "fused RoPE: head_dim %d unsupported", r->d);
   r->rope_theta0 = theta0;
   for (int i = 0; i < 3; ++i) r->rope_split[i] = split[i];
   FVSR_CUDA(cudaDeviceSynchronize());

@@ -213,18 +213,20 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
   __syncthreads();
   mbar_wait(bar, 0);
   if constexpr (ROPE) {  // rotate the staged src rows in place: x0*c - x1*s, x0*s + x1*c (no FMA), bf16 RNE
+    // thread -> fixed pair pi (consecutive threads, consecutive smem words: conflict-free),
+    // rows strided by kPPThreads / npairs; the t-axis (cos, sin) is loaded once per frame
     const int npairs = d >> 1, ht = a.rope_dt >> 1, hh = a.rope_dh >> 1, hw = a.rope_dw >> 1;
+    const int pi = tid % npairs, r0 = tid / npairs, rstep = kPPThreads / npairs;
+    const int axis = pi < ht ? 0 : (pi < ht + hh ? 1 : 2);
     for (int fi = 0; fi < cnt; ++fi) {
       uint8_t* st = stage(fi, 0);
-      const float2* tt = a.rope_t + (long long)a.rope_fid[f0 + fi] * ht;
-      for (int e = tid; e < 64 * npairs; e += kPPThreads) {
-        const int r = e / npairs, pi = e - r * npairs;
+      const float2 ct = axis == 0 ? a.rope_t[(long long)a.rope_fid[f0 + fi] * ht + pi] : make_float2(1.0f, 0.0f);
+      for (int r = r0; r < 64; r += rstep) {
         const int rh = r >> 3, rw = r & 7;
         if (rh >= hc || rw >= wc) continue;
-        float2 cs;
-        if (pi < ht) cs = tt[pi];
-        else if (pi < ht + hh) cs = a.rope_h[(8 * th + rh) * hh + (pi - ht)];
-        else cs = a.rope_w[(8 * tw + rw) * hw + (pi - ht - hh)];
+        const float2 cs = axis == 0 ? ct
+                          : axis == 1 ? a.rope_h[(8 * th + rh) * hh + (pi - ht)]
+                                      : a.rope_w[(8 * tw + rw) * hw + (pi - ht - hh)];
         uint32_t* pp = reinterpret_cast<uint32_t*>(st + (r * d + 2 * pi) * 2);
         const uint32_t v = *pp;
         const float x0 = __uint_as_float(v << 16), x1 = __uint_as_float(v & 0xffff0000u);

@@ -11,6 +11,13 @@ so the (head, q-tile) work units shard with no exchange except gathering the out
     output = tile-major shard [per, 64, d]  ->  NCCL all_gather_into_tensor (equal chunks)
              -> untile() back to [heads, Lq, d] token order when a consumer needs it.
 
+Uniform scored eviction (KVCache::evict, P/src/kv_cache.cpp:118-128) sums frame scores over
+ALL heads, but a rank's ring holds only heads [h0, h1).  full_frame_mass() is the one extra
+exchange: each rank writes its heads' rows into a [heads, frames] float64 matrix (zeros
+elsewhere) and an all-reduce(MAX) assembles it (masses are >= 0; a head held by two ranks has
+identical rows on both, so MAX takes it once).  uniform_evict() then applies the global
+decision to the local ring: every rank evicts the same frames.
+
 The gather of layer l runs on NCCL's stream while layer l+1 computes (async_op, double
 buffered); the step's host code never waits on it until the buffer is reused.
 """
@@ -119,3 +126,35 @@ class Gatherer:
             if self.work[i] is not None:
                 self.work[i].wait()
                 self.work[i] = None
+
+
+def full_frame_mass(local: torch.Tensor, sh: Shard, heads_total: int, group=None) -> torch.Tensor:
+    """[heads_total, frames] float64 frame masses on every rank from each rank's
+    [sh.heads, frames] rows (KVRing.frame_mass of its ring)."""
+    import torch.distributed as dist
+    full = torch.zeros((heads_total, local.shape[1]), dtype=torch.float64, device=local.device)
+    if sh.heads:
+        full[sh.h0:sh.h1] = local.to(torch.float64)
+    if dist.is_initialized() and sh.world > 1:
+        dist.all_reduce(full, op=dist.ReduceOp.MAX, group=group)
+    return full
+
+
+def uniform_total(full: torch.Tensor):
+    """Per-frame sum over heads in head order, in double (kv_cache.cpp:123-125)."""
+    rows = full.detach().cpu().tolist()
+    total = [0.0] * len(rows[0])
+    for r in rows:
+        for i, x in enumerate(r):
+            total[i] += x
+    return total
+
+
+def uniform_evict(ring, layer: int, full: torch.Tensor) -> None:
+    """KVCache::evict(uniform) with the GLOBAL head sum applied to this rank's ring: the total
+    goes in row 0 and the other rows are zero, so the ring's own head sum reproduces it exactly."""
+    from .kv_ring import EVICT_UNIFORM
+    total = uniform_total(full)
+    scores = torch.zeros((ring.heads, len(total)), dtype=torch.float64)
+    scores[0] = torch.tensor(total, dtype=torch.float64)
+    ring.evict_scored(layer, EVICT_UNIFORM, scores)

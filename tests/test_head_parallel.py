@@ -8,7 +8,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2510_12747_b200.head_parallel import Gatherer, shard, untile, untile_index
+from paper_2510_12747_b200.head_parallel import Gatherer, full_frame_mass, shard, uniform_total, untile, untile_index
 
 
 @pytest.mark.parametrize("heads,nq,tiles,world", [(12, 1, 66, 1), (12, 1, 66, 2), (12, 1, 66, 4),
@@ -98,3 +98,45 @@ def test_gather_world2_gloo(heads, rows, cols, nq):
     for p in procs:
         p.join(timeout=60)
     assert all(r[1] == "ok" for r in results), results
+
+
+def _mass_worker(rank, world, port, heads, uph, n, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.manual_seed(1)
+        full = torch.rand(heads, n, dtype=torch.float64)  # what one GPU's ring would report
+        sh = shard(heads * uph, uph, world, rank)
+        got = full_frame_mass(full[sh.h0:sh.h1].clone(), sh, heads)
+        q.put((rank, "ok" if torch.equal(got, full) else "mismatch", uniform_total(got)))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+
+
+@pytest.mark.parametrize("heads,uph", [(12, 66), (3, 5)])  # (3, 5): head 1 is split across the two ranks
+def test_uniform_eviction_scores_world2_gloo(heads, uph):
+    """Uniform eviction under head-parallel sharding (kv_cache.cpp:118-128): the all-reduce
+    rebuilds every head's frame masses on every rank, so all ranks take the same decision,
+    equal to the single-process one (oracle.evict)."""
+    import numpy as np
+    import oracle
+    world, n = 2, 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mass_worker, args=(r, world, port, heads, uph, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] == "ok" for r in results), results
+    assert results[0][2] == results[1][2]
+    torch.manual_seed(1)
+    full = torch.rand(heads, n, dtype=torch.float64).numpy()
+    ids = [3, 4, 5, 6, 7]
+    want = oracle.evict(1, 3, ids, full, heads)[0]
+    total = results[0][2]
+    got = [i for i in ids if i not in oracle.evict_victims(ids, total, len(ids) - 3)]
+    assert got == want
