@@ -302,7 +302,10 @@ int launch_pack_pool(const PackPoolArgs& a, const PoolGroups& pg, const SlotList
   if (a.d % 8 != 0) return fail(FVSR_E_CONFIG, "pack_pool: head_dim must be a multiple of 8 (got %d)", a.d);
   if ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.src2)) % 16 != 0)
     return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
-  const size_t smem = pack_pool_smem(a.d, max_cnt, a.src2 != nullptr);
+  const size_t smem = pack_pool_smem(a.d, max_cnt, a.src2 != nullptr) +
+                      (a.rope_t ? (size_t)(max_cnt * (a.rope_dt / 2) + 8 * (a.rope_dh / 2) + 8 * (a.rope_dw / 2)) *
+                                      sizeof(float2)
+                                : 0);
   // the RoPE variant is a separate instantiation so the plain pack/pool pass is unchanged
   auto kern = a.rope_t ? pack_pool_kernel<true> : pack_pool_kernel<false>;
   static size_t configured[2] = {48 * 1024, 48 * 1024};

@@ -210,6 +210,26 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
         }
       }
   }
+  // RoPE tables of this tile -> shared memory while the bulk copies are in flight:
+  // t: [cnt][dt/2], h: [8 tile rows][dh/2], w: [8 tile cols][dw/2]
+  float2* rtab = reinterpret_cast<float2*>(sm_pp + (size_t)cnt * nt * tile_bytes + 16);
+  if constexpr (ROPE) {
+    const int ht = a.rope_dt >> 1, hh = a.rope_dh >> 1, hw = a.rope_dw >> 1;
+    for (int i = tid; i < cnt * ht; i += kPPThreads) {
+      const int fi = i / ht, p = i - fi * ht;
+      rtab[i] = a.rope_t[(long long)a.rope_fid[f0 + fi] * ht + p];
+    }
+    float2* rh_t = rtab + cnt * ht;
+    for (int i = tid; i < 8 * hh; i += kPPThreads) {
+      const int k = i / hh, p = i - k * hh;
+      if (8 * th + k < a.rows) rh_t[i] = a.rope_h[(8 * th + k) * hh + p];
+    }
+    float2* rw_t = rh_t + 8 * hh;
+    for (int i = tid; i < 8 * hw; i += kPPThreads) {
+      const int k = i / hw, p = i - k * hw;
+      if (8 * tw + k < a.cols) rw_t[i] = a.rope_w[(8 * tw + k) * hw + p];
+    }
+  }
   __syncthreads();
   mbar_wait(bar, 0);
   if constexpr (ROPE) {  // rotate the staged src rows in place: x0*c - x1*s, x0*s + x1*c (no FMA), bf16 RNE
@@ -218,15 +238,16 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
     const int npairs = d >> 1, ht = a.rope_dt >> 1, hh = a.rope_dh >> 1, hw = a.rope_dw >> 1;
     const int pi = tid % npairs, r0 = tid / npairs, rstep = kPPThreads / npairs;
     const int axis = pi < ht ? 0 : (pi < ht + hh ? 1 : 2);
+    const float2* rh_t = rtab + cnt * ht;
+    const float2* rw_t = rh_t + 8 * hh;
     for (int fi = 0; fi < cnt; ++fi) {
       uint8_t* st = stage(fi, 0);
-      const float2 ct = axis == 0 ? a.rope_t[(long long)a.rope_fid[f0 + fi] * ht + pi] : make_float2(1.0f, 0.0f);
+      const float2 ct = axis == 0 ? rtab[fi * ht + pi] : make_float2(1.0f, 0.0f);
+#pragma unroll 4
       for (int r = r0; r < 64; r += rstep) {
         const int rh = r >> 3, rw = r & 7;
         if (rh >= hc || rw >= wc) continue;
-        const float2 cs = axis == 0 ? ct
-                          : axis == 1 ? a.rope_h[(8 * th + rh) * hh + (pi - ht)]
-                                      : a.rope_w[(8 * tw + rw) * hw + (pi - ht - hh)];
+        const float2 cs = axis == 0 ? ct : axis == 1 ? rh_t[rh * hh + (pi - ht)] : rw_t[rw * hw + (pi - ht - hh)];
         uint32_t* pp = reinterpret_cast<uint32_t*>(st + (r * d + 2 * pi) * 2);
         const uint32_t v = *pp;
         const float x0 = __uint_as_float(v << 16), x1 = __uint_as_float(v & 0xffff0000u);
