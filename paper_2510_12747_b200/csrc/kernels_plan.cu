@@ -171,6 +171,16 @@ inline size_t pack_pool_smem(int d, int max_cnt, bool two) {
   return (size_t)max_cnt * (two ? 2 : 1) * 64 * d * 2 + 16;
 }
 
+// one bf16 channel pair (x0 | x1 << 16) rotated by (cos, sin): x0*c - x1*s, x0*s + x1*c in
+// fp32 with separate multiply and add (apply_rope, P/src/rope.cpp:50-55), then bf16 RNE
+__device__ __forceinline__ uint32_t rope_word(uint32_t v, float2 cs) {
+  const float x0 = __uint_as_float(v << 16), x1 = __uint_as_float(v & 0xffff0000u);
+  const float y0 = __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
+  const float y1 = __fadd_rn(__fmul_rn(x0, cs.y), __fmul_rn(x1, cs.x));
+  const __nv_bfloat162 b = __floats2bfloat162_rn(y0, y1);
+  return *reinterpret_cast<const uint32_t*>(&b);
+}
+
 template <bool ROPE>
 __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_constant__ PackPoolArgs a,
                                                                const __grid_constant__ PoolGroups groups,
@@ -232,33 +242,15 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
   }
   __syncthreads();
   mbar_wait(bar, 0);
-  if constexpr (ROPE) {  // rotate the staged src rows in place: x0*c - x1*s, x0*s + x1*c (no FMA), bf16 RNE
-    // thread -> fixed pair pi (consecutive threads, consecutive smem words: conflict-free),
-    // rows strided by kPPThreads / npairs; the t-axis (cos, sin) is loaded once per frame
-    const int npairs = d >> 1, ht = a.rope_dt >> 1, hh = a.rope_dh >> 1, hw = a.rope_dw >> 1;
-    const int pi = tid % npairs, r0 = tid / npairs, rstep = kPPThreads / npairs;
-    const int axis = pi < ht ? 0 : (pi < ht + hh ? 1 : 2);
-    const float2* rh_t = rtab + cnt * ht;
-    const float2* rw_t = rh_t + 8 * hh;
-    for (int fi = 0; fi < cnt; ++fi) {
-      uint8_t* st = stage(fi, 0);
-      const float2 ct = axis == 0 ? rtab[fi * ht + pi] : make_float2(1.0f, 0.0f);
-#pragma unroll 4
-      for (int r = r0; r < 64; r += rstep) {
-        const int rh = r >> 3, rw = r & 7;
-        if (rh >= hc || rw >= wc) continue;
-        const float2 cs = axis == 0 ? ct : axis == 1 ? rh_t[rh * hh + (pi - ht)] : rw_t[rw * hw + (pi - ht - hh)];
-        uint32_t* pp = reinterpret_cast<uint32_t*>(st + (r * d + 2 * pi) * 2);
-        const uint32_t v = *pp;
-        const float x0 = __uint_as_float(v << 16), x1 = __uint_as_float(v & 0xffff0000u);
-        const float y0 = __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
-        const float y1 = __fadd_rn(__fmul_rn(x0, cs.y), __fmul_rn(x1, cs.x));
-        const __nv_bfloat162 b = __floats2bfloat162_rn(y0, y1);
-        *pp = *reinterpret_cast<const uint32_t*>(&b);
-      }
-    }
-    __syncthreads();
-  }
+  // RoPE (ROPE): applied on the fly where the pooling and packing phases read the staged
+  // src rows (both round the rotated pair to bf16 the same way, so the pooled sums, the |k|
+  // bound and the stored tile agree); no serial rotate phase, no write-back
+  const int r_ht = a.rope_dt >> 1, r_hh = a.rope_dh >> 1, r_hw = a.rope_dw >> 1;
+  auto rope_cs = [&](int fi, int pi, int rh, int rw) -> float2 {
+    if (pi < r_ht) return rtab[fi * r_ht + pi];
+    if (pi < r_ht + r_hh) return rtab[cnt * r_ht + rh * r_hh + (pi - r_ht)];
+    return rtab[cnt * r_ht + 8 * r_hh + rw * r_hw + (pi - r_ht - r_hh)];
+  };
   // pooling (exact token order; rows past the frame are skipped, not added as zeros)
   if (2 * tid < d) {
     const int c = 2 * tid;
@@ -279,7 +271,8 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
 #pragma unroll
         for (int rw = 0; rw < 8; ++rw) {
           if (rw < wc) {
-            const uint32_t v = *reinterpret_cast<const uint32_t*>(st + ((rh * 8 + rw) * d + c) * 2);
+            uint32_t v = *reinterpret_cast<const uint32_t*>(st + ((rh * 8 + rw) * d + c) * 2);
+            if constexpr (ROPE) v = rope_word(v, rope_cs(fi, c >> 1, rh, rw));
             const float x = __uint_as_float(v << 16), y = __uint_as_float(v & 0xffff0000u);
             s0x = __fadd_rn(s0x, x);
             s0y = __fadd_rn(s0y, y);
@@ -319,7 +312,16 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
       for (int i = tid, k = 0; i < chunks; i += kPPThreads, ++k) {
         const int panel = i >> 9, r = (i >> 3) & 63, j = i & 7;
         const int c = panel * 64 + ((j ^ (r & 7)) << 3);
-        const uint4 v = *reinterpret_cast<const uint4*>(st + (r * d + c) * 2);
+        uint4 v = *reinterpret_cast<const uint4*>(st + (r * d + c) * 2);
+        if constexpr (ROPE) {
+          if (t == 0 && (r >> 3) < hc && (r & 7) < wc) {  // rows past the frame stay zero
+            const int p0 = c >> 1, rh = r >> 3, rw = r & 7;
+            v.x = rope_word(v.x, rope_cs(fi, p0, rh, rw));
+            v.y = rope_word(v.y, rope_cs(fi, p0 + 1, rh, rw));
+            v.z = rope_word(v.z, rope_cs(fi, p0 + 2, rh, rw));
+            v.w = rope_word(v.w, rope_cs(fi, p0 + 3, rh, rw));
+          }
+        }
         *reinterpret_cast<uint4*>(dst + (size_t)i * 16) = v;
         if (t == 0 && a.norm2) {
           const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
