@@ -267,12 +267,23 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
       const bool cont = fi == 1 || ext;
       const uint8_t* st = stage(fi, 0);
       float s0x = 0.0f, s0y = 0.0f;
+      // ROPE: this thread's pair is fixed, so its (cos, sin) depends on at most the row (h axis)
+      // or the column (w axis): the 8 column values live in registers, the row value is
+      // reloaded once per tile row
+      float2 cs_w[8];
+      if constexpr (ROPE) {
+#pragma unroll
+        for (int rw = 0; rw < 8; ++rw) cs_w[rw] = rope_cs(fi, c >> 1, 0, rw < wc ? rw : 0);
+      }
       for (int rh = 0; rh < hc; ++rh) {
+        float2 cs_h = make_float2(1.0f, 0.0f);
+        if constexpr (ROPE) cs_h = rope_cs(fi, c >> 1, rh, 0);
+        const bool by_row = (c >> 1) < r_ht + r_hh;  // t or h axis: constant along the tile row
 #pragma unroll
         for (int rw = 0; rw < 8; ++rw) {
           if (rw < wc) {
             uint32_t v = *reinterpret_cast<const uint32_t*>(st + ((rh * 8 + rw) * d + c) * 2);
-            if constexpr (ROPE) v = rope_word(v, rope_cs(fi, c >> 1, rh, rw));
+            if constexpr (ROPE) v = rope_word(v, by_row ? cs_h : cs_w[rw]);
             const float x = __uint_as_float(v << 16), y = __uint_as_float(v & 0xffff0000u);
             s0x = __fadd_rn(s0x, x);
             s0y = __fadd_rn(s0y, y);
