@@ -89,6 +89,9 @@ struct fvsr_ctx {
   size_t scores_cap = 0;
   // shape of the scores the last two-kernel selection left in d_scores (fvsr_ring_frame_mass)
   int scores_heads = 0, scores_bnq = 0, scores_bnk = 0;
+  // fp64 scratch of the frame-mass passes
+  double* d_mass_scratch = nullptr;
+  size_t mass_scratch_cap = 0;
 };
 
 struct fvsr_ring {
@@ -653,6 +656,7 @@ void fvsr_ctx_destroy(fvsr_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->d_scores) cudaFree(ctx->d_scores);
+  if (ctx->d_mass_scratch) cudaFree(ctx->d_mass_scratch);
   delete ctx;
 }
 
@@ -1180,15 +1184,28 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
 namespace {
 int launch_frame_mass(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads, const float* coarse,
                       double* mass, cudaStream_t s) {
-  const size_t smem = (size_t)(2 * g.bnq + g.bnk) * sizeof(double);
-  if (smem > 200 * 1024) return fail(FVSR_E_CONFIG, "frame_attention_mass: %d x %d blocks too large", g.bnq, g.bnk);
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
-    FVSR_CUDA(cudaFuncSetAttribute(frame_mass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
+  // scratch: row max / denominators [heads][bnq], block masses [heads][bnk] (fp64)
+  const size_t nrow = (size_t)heads * g.bnq, nblk = (size_t)heads * g.bnk;
+  if (!ctx->d_mass_scratch || ctx->mass_scratch_cap < 2 * nrow + nblk) {
+    cudaFree(ctx->d_mass_scratch);
+    ctx->d_mass_scratch = nullptr;
+    ctx->mass_scratch_cap = 0;
+    if (cudaMalloc(&ctx->d_mass_scratch, (2 * nrow + nblk) * sizeof(double)) != cudaSuccess)
+      return fail(FVSR_E_NOMEM, "frame_attention_mass: scratch allocation failed");
+    ctx->mass_scratch_cap = 2 * nrow + nblk;
   }
-  FVSR_CUDA(launch_k(frame_mass_kernel, dim3(heads), dim3(kMassThreads), smem, s, g, dm, coarse, mass));
-  return after_launch(ctx, s, 1);
+  double* rmax = ctx->d_mass_scratch;
+  double* rden = rmax + nrow;
+  double* bmass = rden + nrow;
+  const unsigned wpc = kMassThreads / 32;
+  FVSR_CUDA(launch_k(frame_mass_rows_kernel, dim3((unsigned)((nrow + wpc - 1) / wpc)), dim3(kMassThreads), 0, s, g, dm,
+                     coarse, rmax, rden, heads));
+  FVSR_CUDA(launch_k(frame_mass_blocks_kernel, dim3((unsigned)((g.bnk + 31) / 32), (unsigned)heads),
+                     dim3(kMassThreads), 0, s, g, dm, coarse, (const double*)rmax, (const double*)rden, bmass));
+  const int nf = heads * g.nkf;
+  FVSR_CUDA(launch_k(frame_mass_frames_kernel, dim3((unsigned)((nf + 127) / 128)), dim3(128), 0, s, g,
+                     (const double*)bmass, mass, heads));
+  return after_launch(ctx, s, 3);
 }
 
 // victim order for one head (P/src/kv_cache.cpp:81-93): lowest score first, older frame on

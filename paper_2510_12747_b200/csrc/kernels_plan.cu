@@ -888,73 +888,99 @@ __global__ void __launch_bounds__(128) sparsity_count_kernel(DevGeom g, DevMask 
 
 // ---------------------------------------------------------------------------------------
 // per-frame attention mass for scored eviction (frame_attention_mass, P/src/kv_cache.cpp:
-// 170-206).  One CTA per head over the fp32 coarse scores the selector already wrote:
-//   1. warp per q-block: max over coarse-allowed key blocks, then sum of exp(s - max)
-//      (double), rows with no allowed block are skipped (kv_cache.cpp:179-181);
-//   2. thread per key block: mass = sum over q-blocks IN ORDER of exp(s - max) / denom
-//      (the reference's block_mass accumulation order, :190);
-//   3. thread per key frame: the mass of every block of its temporal row, split over the
-//      block's member tokens and credited per token count (:193-203).
-// Shared memory: 2*bnq + bnk doubles.  Not on the attention hot path (once per layer-step
-// when a scored eviction strategy is used).
+// 170-206) from the fp32 coarse scores the selector already wrote, in three small passes
+// spread over the whole GPU (one CTA per head measured 66 us; fp64 exp chains are long):
+//   frame_mass_rows_kernel   warp per (head, q-block): max over coarse-allowed key blocks,
+//                            sum of exp(s - max) in fp64 (rows with no allowed block are
+//                            marked and skipped, kv_cache.cpp:179-181);
+//   frame_mass_blocks_kernel CTA per (head, 32 key blocks): warp w sums q-blocks w, w+8, ...
+//                            of exp(s - max) / denom, then a fixed-order 8-way combine
+//                            (deterministic; kv_cache.cpp:184-190);
+//   frame_mass_frames_kernel thread per (head, key frame): the mass of every block of its
+//                            temporal row, split over member tokens (kv_cache.cpp:193-203).
+// Device exp and the summation order differ from the reference in the last ulps (1e-12 rel).
 // ---------------------------------------------------------------------------------------
 constexpr int kMassThreads = 256;
 
-__global__ void __launch_bounds__(kMassThreads) frame_mass_kernel(const __grid_constant__ DevGeom g,
-                                                                  const __grid_constant__ DevMask m,
-                                                                  const float* __restrict__ coarse,
-                                                                  double* __restrict__ mass) {
+__global__ void __launch_bounds__(kMassThreads) frame_mass_rows_kernel(const __grid_constant__ DevGeom g,
+                                                                       const __grid_constant__ DevMask m,
+                                                                       const float* __restrict__ coarse,
+                                                                       double* __restrict__ rmax,
+                                                                       double* __restrict__ rden, int heads) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ double fm_smem[];
-  double* rmax = fm_smem;
-  double* rden = fm_smem + g.bnq;
-  double* bmass = fm_smem + 2 * g.bnq;
-  const int head = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float* sc = coarse + (long long)head * g.bnq * g.bnk;
-  for (int qb = warp; qb < g.bnq; qb += kMassThreads / 32) {
-    const int qtr = qb / g.n_tiles, qtile = qb - qtr * g.n_tiles;
-    const float* row = sc + (long long)qb * g.bnk;
-    double mx = -INFINITY;
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * (kMassThreads / 32) + (threadIdx.x >> 5);  // head * bnq + qb
+  if (row >= (long long)heads * g.bnq) return;
+  const int qb = (int)(row % g.bnq);
+  const int qtr = qb / g.n_tiles, qtile = qb - qtr * g.n_tiles;
+  const float* sc = coarse + row * g.bnk;
+  double mx = -INFINITY;
+  for (int kb = lane; kb < g.bnk; kb += 32)
+    if (coarse_allowed(g, m, qtr, qtile, kb / g.n_tiles, kb % g.n_tiles)) mx = fmax(mx, (double)sc[kb]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double den = 0.0;
+  if (mx != -INFINITY)
     for (int kb = lane; kb < g.bnk; kb += 32)
-      if (coarse_allowed(g, m, qtr, qtile, kb / g.n_tiles, kb % g.n_tiles)) mx = fmax(mx, (double)row[kb]);
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    double den = 0.0;
-    if (mx != -INFINITY)
-      for (int kb = lane; kb < g.bnk; kb += 32)
-        if (coarse_allowed(g, m, qtr, qtile, kb / g.n_tiles, kb % g.n_tiles)) den += exp((double)row[kb] - mx);
-    for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
-    if (lane == 0) {
-      rmax[qb] = mx;
-      rden[qb] = den;
-    }
+      if (coarse_allowed(g, m, qtr, qtile, kb / g.n_tiles, kb % g.n_tiles)) den += exp((double)sc[kb] - mx);
+  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+  if (lane == 0) {
+    rmax[row] = mx;
+    rden[row] = den;
   }
-  __syncthreads();
-  for (int kb = threadIdx.x; kb < g.bnk; kb += kMassThreads) {
-    const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
-    double acc = 0.0;
-    for (int qb = 0; qb < g.bnq; ++qb) {
-      if (rmax[qb] == -INFINITY) continue;
+}
+
+__global__ void __launch_bounds__(kMassThreads) frame_mass_blocks_kernel(const __grid_constant__ DevGeom g,
+                                                                         const __grid_constant__ DevMask m,
+                                                                         const float* __restrict__ coarse,
+                                                                         const double* __restrict__ rmax,
+                                                                         const double* __restrict__ rden,
+                                                                         double* __restrict__ bmass) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double part[kMassThreads / 32][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int head = blockIdx.y;
+  const int kb = blockIdx.x * 32 + lane;
+  const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+  const float* sc = coarse + (long long)head * g.bnq * g.bnk;
+  double acc = 0.0;
+  if (kb < g.bnk)
+    for (int qb = warp; qb < g.bnq; qb += kMassThreads / 32) {
+      const double mx = rmax[(long long)head * g.bnq + qb];
+      if (mx == -INFINITY) continue;
       const int qtr = qb / g.n_tiles, qtile = qb - qtr * g.n_tiles;
       if (coarse_allowed(g, m, qtr, qtile, ktr, ktile))
-        acc += exp((double)sc[(long long)qb * g.bnk + kb] - rmax[qb]) / rden[qb];
+        acc += exp((double)sc[(long long)qb * g.bnk + kb] - mx) / rden[(long long)head * g.bnq + qb];
     }
-    bmass[kb] = acc;
-  }
+  part[warp][lane] = acc;
   __syncthreads();
-  for (int f = threadIdx.x; f < g.nkf; f += kMassThreads) {
-    int tr = 0;
-    while (tr + 1 < g.nk_trows && g.k_tr_first[tr + 1] <= f) ++tr;
-    double acc = 0.0;
-    for (int tile = 0; tile < g.n_tiles; ++tile) {
-      const double bm = bmass[tr * g.n_tiles + tile];
-      if (bm == 0.0) continue;
-      const int tok = tile_h_count(g, tile) * tile_w_count(g, tile);
-      acc += bm / (double)(tok * g.k_tr_count[tr]) * (double)tok;
-    }
-    mass[(long long)head * g.nkf + f] = acc;
+  if (warp == 0 && kb < g.bnk) {
+    double t = part[0][lane];
+#pragma unroll
+    for (int w = 1; w < kMassThreads / 32; ++w) t += part[w][lane];
+    bmass[(long long)head * g.bnk + kb] = t;
   }
+}
+
+__global__ void __launch_bounds__(128) frame_mass_frames_kernel(const __grid_constant__ DevGeom g,
+                                                                const double* __restrict__ bmass,
+                                                                double* __restrict__ mass, int heads) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= heads * g.nkf) return;
+  const int head = i / g.nkf, f = i - head * g.nkf;
+  int tr = 0;
+  while (tr + 1 < g.nk_trows && g.k_tr_first[tr + 1] <= f) ++tr;
+  const double* bm = bmass + (long long)head * g.bnk + (long long)tr * g.n_tiles;
+  double acc = 0.0;
+  for (int tile = 0; tile < g.n_tiles; ++tile) {
+    if (bm[tile] == 0.0) continue;
+    const int tok = tile_h_count(g, tile) * tile_w_count(g, tile);
+    acc += bm[tile] / (double)(tok * g.k_tr_count[tr]) * (double)tok;
+  }
+  mass[i] = acc;
 }
 
 // ---------------------------------------------------------------------------------------
