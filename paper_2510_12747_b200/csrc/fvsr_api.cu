@@ -1203,7 +1203,7 @@ int launch_frame_mass(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int he
   FVSR_CUDA(launch_k(frame_mass_blocks_kernel, dim3((unsigned)((g.bnk + 31) / 32), (unsigned)heads),
                      dim3(kMassThreads), 0, s, g, dm, coarse, (const double*)rmax, (const double*)rden, bmass));
   const int nf = heads * g.nkf;
-  FVSR_CUDA(launch_k(frame_mass_frames_kernel, dim3((unsigned)((nf + 127) / 128)), dim3(128), 0, s, g,
+  FVSR_CUDA(launch_k(frame_mass_frames_kernel, dim3((unsigned)((nf + 3) / 4)), dim3(128), 0, s, g,
                      (const double*)bmass, mass, heads));
   return after_launch(ctx, s, 3);
 }

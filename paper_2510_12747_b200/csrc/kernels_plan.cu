@@ -896,7 +896,7 @@ __global__ void __launch_bounds__(128) sparsity_count_kernel(DevGeom g, DevMask 
 //   frame_mass_blocks_kernel CTA per (head, 32 key blocks): warp w sums q-blocks w, w+8, ...
 //                            of exp(s - max) / denom, then a fixed-order 8-way combine
 //                            (deterministic; kv_cache.cpp:184-190);
-//   frame_mass_frames_kernel thread per (head, key frame): the mass of every block of its
+//   frame_mass_frames_kernel warp per (head, key frame): the mass of every block of its
 //                            temporal row, split over member tokens (kv_cache.cpp:193-203).
 // Device exp and the summation order differ from the reference in the last ulps (1e-12 rel).
 // ---------------------------------------------------------------------------------------
@@ -968,19 +968,23 @@ __global__ void __launch_bounds__(128) frame_mass_frames_kernel(const __grid_con
                                                                 double* __restrict__ mass, int heads) {
   pdl_wait();
   pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // warp per (head, key frame); lanes stride the tiles of the frame's temporal row
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (i >= heads * g.nkf) return;
   const int head = i / g.nkf, f = i - head * g.nkf;
   int tr = 0;
   while (tr + 1 < g.nk_trows && g.k_tr_first[tr + 1] <= f) ++tr;
   const double* bm = bmass + (long long)head * g.bnk + (long long)tr * g.n_tiles;
   double acc = 0.0;
-  for (int tile = 0; tile < g.n_tiles; ++tile) {
-    if (bm[tile] == 0.0) continue;
+  for (int tile = lane; tile < g.n_tiles; tile += 32) {
+    const double b = bm[tile];
+    if (b == 0.0) continue;
     const int tok = tile_h_count(g, tile) * tile_w_count(g, tile);
-    acc += bm[tile] / (double)(tok * g.k_tr_count[tr]) * (double)tok;
+    acc += b / (double)(tok * g.k_tr_count[tr]) * (double)tok;
   }
-  mass[i] = acc;
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) mass[i] = acc;
 }
 
 // ---------------------------------------------------------------------------------------
