@@ -1309,17 +1309,18 @@ int launch_token_mask(fvsr_ctx* ctx, const int32_t* labels_host, long long L, in
   void* ws = ws_get(ctx, smem, &st);
   if (!ws) return st;
   FVSR_CUDA(cudaMemcpyAsync(ws, labels_host, smem, cudaMemcpyHostToDevice, s));
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
-    FVSR_CUDA(cudaFuncSetAttribute(token_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
+  auto kern = kind == 0 ? token_mask_kernel<0> : token_mask_kernel<1>;
+  static size_t configured[2] = {48 * 1024, 48 * 1024};
+  if (smem > configured[kind]) {
+    FVSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured[kind] = smem;
   }
   int sms = 148;
   (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   const long long tasks = L * (((L + 63) / 64 + 31) / 32);
   const long long ctas = std::min<long long>((tasks + kMaskThreads / 32 - 1) / (kMaskThreads / 32), 4LL * sms);
-  FVSR_CUDA(launch_k(token_mask_kernel, dim3((unsigned)ctas), dim3(kMaskThreads), smem, s,
-                     static_cast<const int*>(ws), L, kind, lookahead, reinterpret_cast<unsigned long long*>(bits)));
+  FVSR_CUDA(launch_k(kern, dim3((unsigned)ctas), dim3(kMaskThreads), smem, s, static_cast<const int*>(ws), (int)L,
+                     lookahead, reinterpret_cast<unsigned long long*>(bits)));
   // the host labels may be released on return (pageable copy is staged before returning)
   return after_launch(ctx, s, 1);
 }

@@ -998,35 +998,48 @@ __global__ void __launch_bounds__(128) frame_mass_frames_kernel(const __grid_con
 // ---------------------------------------------------------------------------------------
 constexpr int kMaskThreads = 256;
 
-__global__ void __launch_bounds__(kMaskThreads) token_mask_kernel(const int* __restrict__ labels, long long L,
-                                                                  int kind, int lookahead,
+// KIND 0 segment: ballots over the labels.  KIND 1 causal: frames are non-decreasing (host
+// checked), so row i's allowed keys are the prefix [0, p) with p = #{j : frame[j] <= frame[i]
+// + lookahead} (mask.cpp:96-98); p comes from a binary search in shared memory and every
+// word is closed-form (all ones / partial / zero) — pure write bandwidth.
+template <int KIND>
+__global__ void __launch_bounds__(kMaskThreads) token_mask_kernel(const int* __restrict__ labels, int L,
+                                                                  int lookahead,
                                                                   unsigned long long* __restrict__ bits) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ int tm_lab[];
-  for (long long j = threadIdx.x; j < L; j += kMaskThreads) tm_lab[j] = labels[j];
+  for (int j = threadIdx.x; j < L; j += kMaskThreads) tm_lab[j] = labels[j];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const long long wpr = (L + 63) / 64;
-  const long long groups = (wpr + 31) / 32;  // 32-word runs per row
-  const long long total = L * groups;
-  const long long warp_id = (long long)blockIdx.x * (kMaskThreads / 32) + (threadIdx.x >> 5);
-  const long long nwarps = (long long)gridDim.x * (kMaskThreads / 32);
-  for (long long task = warp_id; task < total; task += nwarps) {
-    const long long i = task / groups;
-    const long long w0 = (task - i * groups) * 32;
-    const int li = tm_lab[i];
-    const int limit = li + lookahead;
+  const int wpr = (L + 63) >> 6;
+  const int groups = (wpr + 31) >> 5;  // 32-word runs per row
+  const int total = L * groups;
+  const int nwarps = gridDim.x * (kMaskThreads / 32);
+  for (int task = blockIdx.x * (kMaskThreads / 32) + (threadIdx.x >> 5); task < total; task += nwarps) {
+    const int i = task / groups;
+    const int w0 = (task - i * groups) << 5;
     unsigned long long mine = 0;
-    for (int u = 0; u < 32 && w0 + u < wpr; ++u) {
-      const long long j0 = (w0 + u) * 64 + lane, j1 = j0 + 32;
-      bool a = false, b = false;
-      if (j0 < L) a = kind == 0 ? tm_lab[j0] == li : tm_lab[j0] <= limit;
-      if (j1 < L) b = kind == 0 ? tm_lab[j1] == li : tm_lab[j1] <= limit;
-      const unsigned lo = __ballot_sync(0xffffffffu, a), hi = __ballot_sync(0xffffffffu, b);
-      if (lane == u) mine = ((unsigned long long)hi << 32) | lo;
+    if constexpr (KIND == 0) {
+      const int li = tm_lab[i];
+      const int un = min(32, wpr - w0);
+      for (int u = 0; u < un; ++u) {
+        const int j0 = ((w0 + u) << 6) + lane, j1 = j0 + 32;
+        const unsigned lo = __ballot_sync(0xffffffffu, j0 < L && tm_lab[j0] == li);
+        const unsigned hi = __ballot_sync(0xffffffffu, j1 < L && tm_lab[j1] == li);
+        if (lane == u) mine = ((unsigned long long)hi << 32) | lo;
+      }
+    } else {
+      const int limit = tm_lab[i] + lookahead;
+      int lo = 0, hi = L;  // first j with frame[j] > limit
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (tm_lab[mid] <= limit) lo = mid + 1; else hi = mid;
+      }
+      const int w = w0 + lane, b0 = w << 6;
+      mine = lo >= b0 + 64 ? ~0ull : (lo <= b0 ? 0ull : ((1ull << (lo - b0)) - 1ull));
     }
-    if (w0 + lane < wpr) bits[i * wpr + w0 + lane] = mine;
+    if (w0 + lane < wpr) bits[(long long)i * wpr + w0 + lane] = mine;
   }
 }
 
