@@ -1302,25 +1302,41 @@ int32_t fvsr_ring_evict(fvsr_ring* r, int32_t layer, int32_t strategy, const dou
 // ---- token-mask builders ----------------------------------------------------
 namespace {
 int launch_token_mask(fvsr_ctx* ctx, const int32_t* labels_host, long long L, int kind, int lookahead,
-                      uint64_t* bits, cudaStream_t s) {
+                      uint64_t* bits, cudaStream_t s, int n_segments = 0) {
   const size_t smem = (size_t)L * sizeof(int);
   if (smem > 200 * 1024) return fail(FVSR_E_CONFIG, "token mask: %lld tokens exceed the builder limit", L);
+  const long long wpr = (L + 63) / 64;
+  // few segments: build one row per segment, then copy rows (rows of a segment are equal)
+  const bool by_segment = kind == 0 && n_segments > 0 && 4LL * n_segments <= L;
+  const size_t lab_bytes = (smem + 255) / 256 * 256;
+  const size_t row_bytes = by_segment ? (size_t)n_segments * wpr * 8 : 0;
   int st;
-  void* ws = ws_get(ctx, smem, &st);
+  void* ws = ws_get(ctx, lab_bytes + row_bytes, &st);
   if (!ws) return st;
   FVSR_CUDA(cudaMemcpyAsync(ws, labels_host, smem, cudaMemcpyHostToDevice, s));
-  auto kern = kind == 0 ? token_mask_kernel<0> : token_mask_kernel<1>;
-  static size_t configured[2] = {48 * 1024, 48 * 1024};
-  if (smem > configured[kind]) {
+  const int kk = by_segment ? 2 : kind;
+  auto kern = kk == 0 ? token_mask_kernel<0> : (kk == 1 ? token_mask_kernel<1> : token_mask_kernel<2>);
+  static size_t configured[3] = {48 * 1024, 48 * 1024, 48 * 1024};
+  if (smem > configured[kk]) {
     FVSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[kind] = smem;
+    configured[kk] = smem;
   }
   int sms = 148;
   (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-  const long long tasks = L * (((L + 63) / 64 + 31) / 32);
+  const long long nrows = by_segment ? n_segments : L;
+  const long long tasks = nrows * ((wpr + 31) / 32);
   const long long ctas = std::min<long long>((tasks + kMaskThreads / 32 - 1) / (kMaskThreads / 32), 4LL * sms);
+  auto* rows = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + lab_bytes);
   FVSR_CUDA(launch_k(kern, dim3((unsigned)ctas), dim3(kMaskThreads), smem, s, static_cast<const int*>(ws), (int)L,
-                     lookahead, reinterpret_cast<unsigned long long*>(bits)));
+                     lookahead, by_segment ? rows : reinterpret_cast<unsigned long long*>(bits), (int)nrows));
+  if (by_segment) {
+    const long long words = L * wpr;
+    const long long cc = std::min<long long>((words + kMaskThreads - 1) / kMaskThreads, 8LL * sms);
+    FVSR_CUDA(launch_k(token_rows_copy_kernel, dim3((unsigned)cc), dim3(kMaskThreads), 0, s,
+                       static_cast<const int*>(ws), (int)L, (const unsigned long long*)rows,
+                       reinterpret_cast<unsigned long long*>(bits)));
+    ctx->launches += 1;
+  }
   // the host labels may be released on return (pageable copy is staged before returning)
   return after_launch(ctx, s, 1);
 }
@@ -1341,7 +1357,7 @@ int32_t fvsr_build_segment_mask(fvsr_ctx* ctx, const int32_t* seg, int64_t L, ui
   for (long long i = 0; i < L; ++i) seen[(size_t)seg[i]] = 1;
   for (char c : seen)
     if (!c) return fail(FVSR_E_CONFIG, "build_segment_mask: segment ids not contiguous");
-  return launch_token_mask(ctx, seg, L, 0, 0, bits, reinterpret_cast<cudaStream_t>(stream));
+  return launch_token_mask(ctx, seg, L, 0, 0, bits, reinterpret_cast<cudaStream_t>(stream), max_id + 1);
 }
 
 int32_t fvsr_build_causal_mask(fvsr_ctx* ctx, const int32_t* frame, int64_t L, int32_t lookahead, uint64_t* bits,

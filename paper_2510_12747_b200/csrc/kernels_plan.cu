@@ -1002,10 +1002,13 @@ constexpr int kMaskThreads = 256;
 // checked), so row i's allowed keys are the prefix [0, p) with p = #{j : frame[j] <= frame[i]
 // + lookahead} (mask.cpp:96-98); p comes from a binary search in shared memory and every
 // word is closed-form (all ones / partial / zero) — pure write bandwidth.
+// KIND 2: segment rows — row s of the output is segment s's row (li = s, nrows = #segments);
+// token_rows_copy_kernel then gives token i the row of seg[i] (rows of one segment are equal).
 template <int KIND>
 __global__ void __launch_bounds__(kMaskThreads) token_mask_kernel(const int* __restrict__ labels, int L,
                                                                   int lookahead,
-                                                                  unsigned long long* __restrict__ bits) {
+                                                                  unsigned long long* __restrict__ bits,
+                                                                  int nrows) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ int tm_lab[];
@@ -1014,14 +1017,14 @@ __global__ void __launch_bounds__(kMaskThreads) token_mask_kernel(const int* __r
   const int lane = threadIdx.x & 31;
   const int wpr = (L + 63) >> 6;
   const int groups = (wpr + 31) >> 5;  // 32-word runs per row
-  const int total = L * groups;
+  const int total = nrows * groups;
   const int nwarps = gridDim.x * (kMaskThreads / 32);
   for (int task = blockIdx.x * (kMaskThreads / 32) + (threadIdx.x >> 5); task < total; task += nwarps) {
     const int i = task / groups;
     const int w0 = (task - i * groups) << 5;
     unsigned long long mine = 0;
-    if constexpr (KIND == 0) {
-      const int li = tm_lab[i];
+    if constexpr (KIND == 0 || KIND == 2) {
+      const int li = KIND == 2 ? i : tm_lab[i];
       const int un = min(32, wpr - w0);
       for (int u = 0; u < un; ++u) {
         const int j0 = ((w0 + u) << 6) + lane, j1 = j0 + 32;
@@ -1040,6 +1043,20 @@ __global__ void __launch_bounds__(kMaskThreads) token_mask_kernel(const int* __r
       mine = lo >= b0 + 64 ? ~0ull : (lo <= b0 ? 0ull : ((1ull << (lo - b0)) - 1ull));
     }
     if (w0 + lane < wpr) bits[(long long)i * wpr + w0 + lane] = mine;
+  }
+}
+
+__global__ void __launch_bounds__(kMaskThreads) token_rows_copy_kernel(const int* __restrict__ seg, int L,
+                                                                       const unsigned long long* __restrict__ rows,
+                                                                       unsigned long long* __restrict__ bits) {
+  pdl_wait();
+  pdl_trigger();
+  const int wpr = (L + 63) >> 6;
+  const long long total = (long long)L * wpr;
+  for (long long e = (long long)blockIdx.x * kMaskThreads + threadIdx.x; e < total;
+       e += (long long)gridDim.x * kMaskThreads) {
+    const int i = (int)(e / wpr), w = (int)(e - (long long)i * wpr);
+    bits[e] = rows[(long long)seg[i] * wpr + w];
   }
 }
 
