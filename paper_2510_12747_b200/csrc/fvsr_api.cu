@@ -1324,7 +1324,7 @@ int launch_token_mask(fvsr_ctx* ctx, const int32_t* labels_host, long long L, in
   int sms = 148;
   (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   const long long nrows = by_segment ? n_segments : L;
-  const long long tasks = nrows * ((wpr + 31) / 32);
+  const long long tasks = nrows * (kind == 1 ? 1 : (wpr + 31) / 32);
   const long long ctas = std::min<long long>((tasks + kMaskThreads / 32 - 1) / (kMaskThreads / 32), 4LL * sms);
   auto* rows = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + lab_bytes);
   FVSR_CUDA(launch_k(kern, dim3((unsigned)ctas), dim3(kMaskThreads), smem, s, static_cast<const int*>(ws), (int)L,

@@ -1016,7 +1016,8 @@ __global__ void __launch_bounds__(kMaskThreads) token_mask_kernel(const int* __r
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int wpr = (L + 63) >> 6;
-  const int groups = (wpr + 31) >> 5;  // 32-word runs per row
+  // 32-word runs per row; causal rows are one task each (one binary search per row)
+  const int groups = KIND == 1 ? 1 : (wpr + 31) >> 5;
   const int total = nrows * groups;
   const int nwarps = gridDim.x * (kMaskThreads / 32);
   for (int task = blockIdx.x * (kMaskThreads / 32) + (threadIdx.x >> 5); task < total; task += nwarps) {
@@ -1039,8 +1040,11 @@ __global__ void __launch_bounds__(kMaskThreads) token_mask_kernel(const int* __r
         const int mid = (lo + hi) >> 1;
         if (tm_lab[mid] <= limit) lo = mid + 1; else hi = mid;
       }
-      const int w = w0 + lane, b0 = w << 6;
-      mine = lo >= b0 + 64 ? ~0ull : (lo <= b0 ? 0ull : ((1ull << (lo - b0)) - 1ull));
+      for (int w = lane; w < wpr; w += 32) {
+        const int b0 = w << 6;
+        bits[(long long)i * wpr + w] = lo >= b0 + 64 ? ~0ull : (lo <= b0 ? 0ull : ((1ull << (lo - b0)) - 1ull));
+      }
+      continue;
     }
     if (w0 + lane < wpr) bits[(long long)i * wpr + w0 + lane] = mine;
   }
