@@ -118,6 +118,8 @@ typedef struct fvsr_ring fvsr_ring;
 
 /* ---- library / context ------------------------------------------------------------- */
 FVSR_API int32_t fvsr_abi_version(void);
+/* Experiment macros the library was built with ("" for the product build). */
+FVSR_API const char* fvsr_build_flags(void);
 FVSR_API const char* fvsr_last_error(void);
 /* Binds to the current CUDA device; fails with FVSR_E_CUDA unless it is sm_100. */
 FVSR_API int32_t fvsr_ctx_create(fvsr_ctx** out);

@@ -108,6 +108,7 @@ SIGNATURES = {
     "fvsr_frame_attention_mass": (I32, [P, I32, GP, GP, MP, P, P, P]),
     "fvsr_ring_frame_mass": (I32, [P, P, I32, C.POINTER(I32), I32, MP, P, P]),
     "fvsr_ring_evict": (I32, [P, I32, I32, P]),
+    "fvsr_build_flags": (C.c_char_p, []),
     "fvsr_ring_step_host": (I32, [P, P, I32, I32, P, P, P, MP, I64, F32, P, P]),
 }
 
@@ -116,22 +117,34 @@ _lock = threading.Lock()
 
 
 def load(build_if_missing: bool = True):
-    """Load libfvsr_b200.so (building it in-tree if absent) and bind every C-ABI symbol."""
+    """Load libfvsr_b200.so (rebuilding it in-tree if missing or older than its sources) and
+    bind every C-ABI symbol.  FVSR_LIB=<path> loads an experiment variant instead (see
+    build.build_variant); a library built with experiment macros is refused otherwise."""
     global _lib
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
-            if not build_if_missing:
+        path = os.environ.get("FVSR_LIB") or LIB_PATH
+        if path == LIB_PATH and _build.stale():
+            if not os.path.exists(LIB_PATH) and not build_if_missing:
                 raise ImportError(f"{LIB_PATH} is missing; run `python -m paper_2510_12747_b200.build`")
-            _build.build()
-        lib = C.CDLL(LIB_PATH)
+            if os.path.exists(os.path.join(_build.HERE, "csrc")) and os.access(_build.HERE, os.W_OK):
+                try:
+                    _build.build()
+                except Exception:
+                    if not os.path.exists(LIB_PATH):
+                        raise
+        lib = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
         if lib.fvsr_abi_version() != 1:
             raise ImportError("libfvsr_b200.so ABI version mismatch")
+        flags = lib.fvsr_build_flags().decode()
+        if flags and not os.environ.get("FVSR_LIB"):
+            raise ImportError(f"{path} is an experiment build ({flags}); rebuild with "
+                              "`python -m paper_2510_12747_b200.build --force`")
         _lib = lib
         return lib
 

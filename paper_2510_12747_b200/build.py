@@ -5,10 +5,15 @@
 
 The .so lands next to this file (git-ignored, but it travels to the GPU box with the
 repo snapshot).  One translation unit: csrc/fvsr_api.cu includes the kernels.
+
+The product library is always built with the product flags only: no environment variable
+changes what it contains.  Experiment builds (instrumentation macros) go through
+``build_variant`` into ``variants/`` and are loaded only when FVSR_LIB names them.
 """
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -18,6 +23,7 @@ REPO = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfvsr_b200.so")
 SRC = os.path.join(HERE, "csrc", "fvsr_api.cu")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+VARIANTS = os.path.join(REPO, "variants")
 
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
@@ -31,39 +37,60 @@ def _sources():
     return glob.glob(os.path.join(HERE, "csrc", "*")) + [os.path.join(REPO, "include", "fvsr_b200.h")]
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def source_hash() -> str:
+    h = hashlib.sha256()
+    for s in sorted(_sources()):
+        with open(s, "rb") as f:
+            h.update(os.path.basename(s).encode() + b"\0" + f.read())
+    return h.hexdigest()
+
+
+def stale(path: str = LIB) -> bool:
+    """True when the library is missing or was built from other sources (content hash in a
+    sidecar file, so copies that do not keep mtimes are not rebuilt needlessly)."""
+    if not os.path.exists(path):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(s) > t for s in _sources())
+    try:
+        with open(path + ".srchash") as f:
+            return f.read().strip() != source_hash()
+    except OSError:
+        return True
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", SRC]
-    if os.environ.get("FVSR_ATTN_INSTRUMENT"):  # experiments: per-tile timelines, debug short-cuts
-        cmd.insert(1, "-DFVSR_ATTN_INSTRUMENT=1")
-    if os.environ.get("FVSR_FIXED_REF"):  # experiments: 0 = always start from -inf references
-        cmd.insert(1, "-DFVSR_FIXED_REF=" + str(int(os.environ["FVSR_FIXED_REF"])))
-    if os.environ.get("FVSR_ATTN_EXP"):  # experiments: bottleneck ablations (not attention)
-        cmd.insert(1, "-DFVSR_ATTN_EXP=" + str(int(os.environ["FVSR_ATTN_EXP"])))
-    # experiments: V stages / P buffers at NQ=64, test_wait-first barriers, polynomial exp2,
-    # QK pacing lead, per-CTA timeline stamps, softmax register budget
-    for k in ("FVSR_NV64", "FVSR_NP64", "FVSR_MBAR_TEST_FIRST", "FVSR_POLY_EXP", "FVSR_QK_LEAD",
-              "FVSR_CTA_TIMELINE", "FVSR_REG_SOFTMAX"):
-        if os.environ.get(k):
-            cmd.insert(1, "-D%s=%d" % (k, int(os.environ[k])))
+def _nvcc(out: str, macros: dict, verbose: bool) -> str:
+    cmd = [NVCC, *FLAGS, "-o", out + ".tmp", SRC]
+    flags = " ".join("-D%s=%s" % (k, v) for k, v in sorted(macros.items()))
+    for k, v in sorted(macros.items()):
+        cmd.insert(1, "-D%s=%s" % (k, v))
+    # the macro set is recorded in the library (fvsr_build_flags) so a loader can refuse it
+    cmd.insert(1, '-DFVSR_BUILD_FLAGS="%s"' % flags)
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libfvsr_b200.so")
+        raise RuntimeError("nvcc failed building %s" % os.path.basename(out))
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    with open(out + ".srchash", "w") as f:
+        f.write(source_hash())
+    return out
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """The product library (product flags only)."""
+    if not force and not stale():
+        return LIB
+    return _nvcc(LIB, {}, verbose)
+
+
+def build_variant(name: str, macros: dict, verbose: bool = False) -> str:
+    """An experiment build (e.g. {"FVSR_ATTN_INSTRUMENT": 1}) into variants/, never over the
+    product library.  Load it with FVSR_LIB=<path>."""
+    os.makedirs(VARIANTS, exist_ok=True)
+    out = os.path.join(VARIANTS, "libfvsr_b200_%s.so" % name)
+    return _nvcc(out, dict(macros), verbose)
 
 
 if __name__ == "__main__":

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -89,6 +91,21 @@ struct fvsr_ctx {
   size_t scores_cap = 0;
   // shape of the scores the last two-kernel selection left in d_scores (fvsr_ring_frame_mass)
   int scores_heads = 0, scores_bnq = 0, scores_bnk = 0;
+  // which ring attention call produced d_scores (fvsr_ring_frame_mass refuses any other):
+  // ring, layer, the layer's frame-set generation, query frame ids and the mask descriptor
+  struct ScoreStamp {
+    const void* ring = nullptr;
+    int layer = -1;
+    unsigned long long gen = 0;
+    std::vector<int> qids;
+    fvsr_mask mask{};
+    bool operator==(const ScoreStamp& o) const {
+      const bool both_all = mask.kind == FVSR_MASK_ALL && o.mask.kind == FVSR_MASK_ALL;
+      return ring == o.ring && layer == o.layer && gen == o.gen && qids == o.qids &&
+             (both_all || (mask.kind == o.mask.kind && mask.mode == o.mask.mode && mask.extent_h == o.mask.extent_h && mask.extent_w == o.mask.extent_w &&
+             mask.bits == o.mask.bits && mask.words_per_row == o.mask.words_per_row));
+    }
+  } stamp;
   // fp64 scratch of the frame-mass passes
   double* d_mass_scratch = nullptr;
   size_t mass_scratch_cap = 0;
@@ -112,6 +129,7 @@ struct fvsr_ring {
   int rope_t_cap = 0;
   std::vector<std::vector<std::pair<int, int>>> ctx;  // per layer: (frame_id, slot), ascending
   std::vector<std::vector<char>> used;                // per layer: slot occupancy
+  std::vector<unsigned long long> gen;                // per layer: bumped on every append / evict
   long long kv_head_stride() const { return (long long)slots * n_tiles * (long long)tile_bytes; }
   long long part_head_stride() const { return (long long)slots * n_tiles * d; }
   uint8_t* k_layer(int l) const { return k + (long long)l * heads * kv_head_stride(); }
@@ -300,6 +318,24 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   return launch_kp(false, kern, grid, block, smem, s, std::forward<Args>(args)...);
 }
 
+// Dynamic shared-memory opt-in above 48 KB, cached per (device, kernel): the attribute is a
+// per-device property, so a process driving several GPUs configures each one.
+template <typename K>
+int ensure_smem(K* kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return FVSR_OK;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  FVSR_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, reinterpret_cast<const void*>(kern)}];
+  if (bytes > have) {
+    FVSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+  }
+  return FVSR_OK;
+}
+
 int launch_pack_pool(const PackPoolArgs& a, const PoolGroups& pg, const SlotList& sl, dim3 grid, int max_cnt,
                      cudaStream_t s) {
   if (a.d % 8 != 0) return fail(FVSR_E_CONFIG, "pack_pool: head_dim must be a multiple of 8 (got %d)", a.d);
@@ -311,12 +347,7 @@ int launch_pack_pool(const PackPoolArgs& a, const PoolGroups& pg, const SlotList
                                 : 0);
   // the RoPE variant is a separate instantiation so the plain pack/pool pass is unchanged
   auto kern = a.rope_t ? pack_pool_kernel<true> : pack_pool_kernel<false>;
-  static size_t configured[2] = {48 * 1024, 48 * 1024};
-  size_t& conf = configured[a.rope_t ? 1 : 0];
-  if (smem > conf) {
-    FVSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    conf = smem;
-  }
+  FVSR_TRY(ensure_smem(kern, smem));
   FVSR_CUDA(launch_k(kern, dim3(grid), dim3(kPPThreads), smem, s, a, pg, sl));
   return FVSR_OK;
 }
@@ -432,18 +463,10 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
     p.coarse = coarse;
     dim3 gf((g.bnq + kFQB - 1) / kFQB, heads);
     if (g.bnk <= 32 * 8) {
-      static size_t conf8 = 48 * 1024;
-      if (smem_f > conf8) {
-        FVSR_CUDA(cudaFuncSetAttribute(score_topk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
-        conf8 = smem_f;
-      }
+      FVSR_TRY(ensure_smem(score_topk_kernel<8>, smem_f));
       FVSR_CUDA(launch_k(score_topk_kernel<8>, dim3(gf), dim3(kFThreads), smem_f, s, g, dm, p));
     } else {
-      static size_t conf16 = 48 * 1024;
-      if (smem_f > conf16) {
-        FVSR_CUDA(cudaFuncSetAttribute(score_topk_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
-        conf16 = smem_f;
-      }
+      FVSR_TRY(ensure_smem(score_topk_kernel<16>, smem_f));
       FVSR_CUDA(launch_k(score_topk_kernel<16>, dim3(gf), dim3(kFThreads), smem_f, s, g, dm, p));
     }
     return FVSR_OK;
@@ -462,8 +485,7 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
   p.coarse = nullptr;  // the score kernel writes `scores` directly
   if (g.d % 4 != 0) return fail(FVSR_E_CONFIG, "plan_sparse: head_dim must be a multiple of 4 (got %d)", g.d);
   const size_t smem_sc = (size_t)(kScQ + kScK) * (g.d + 4) * 4;
-  if (smem_sc > 48 * 1024)
-    FVSR_CUDA(cudaFuncSetAttribute(coarse_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sc));
+  FVSR_TRY(ensure_smem(coarse_score_kernel, smem_sc));
   dim3 gs((g.bnk + kScK - 1) / kScK, (g.bnq + kScQ - 1) / kScQ, heads);
   FVSR_CUDA(launch_k(coarse_score_kernel, dim3(gs), dim3(kScThreads), smem_sc, s, g, dm, p, scores));
   dim3 gt((g.bnq + kTopkWarps - 1) / kTopkWarps, heads);
@@ -481,12 +503,7 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
 template <int D, int NQ, int MK>
 int launch_attn_dqm(const DevGeom& g, const DevMask& dm, const AttnParams& p, int sms, cudaStream_t s) {
   using Cfg = AttnCfg<D, NQ>;
-  static bool configured = false;
-  if (!configured) {
-    FVSR_CUDA(cudaFuncSetAttribute(sparse_attn_kernel<D, NQ, MK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)Cfg::kBytes));
-    configured = true;
-  }
+  FVSR_TRY(ensure_smem(sparse_attn_kernel<D, NQ, MK>, Cfg::kBytes));
   const long long units = p.unit_end - p.unit_begin;
   if (units <= 0) return FVSR_OK;
   const unsigned grid = (unsigned)std::min<long long>(units, sms);  // persistent CTAs
@@ -620,6 +637,11 @@ int check_ctx(fvsr_ctx* ctx) {
 extern "C" {
 
 int32_t fvsr_abi_version(void) { return FVSR_ABI_VERSION; }
+
+#ifndef FVSR_BUILD_FLAGS
+#define FVSR_BUILD_FLAGS ""
+#endif
+const char* fvsr_build_flags(void) { return FVSR_BUILD_FLAGS; }
 
 const char* fvsr_last_error(void) { return g_last_error.c_str(); }
 
@@ -872,6 +894,7 @@ int32_t fvsr_ring_create(fvsr_ctx* ctx, int32_t layers, int32_t heads, int32_t d
   }
   r->ctx.assign(layers, {});
   r->used.assign(layers, std::vector<char>(r->slots, 0));
+  r->gen.assign(layers, 0);
   *out = r;
   return FVSR_OK;
 }
@@ -1034,6 +1057,7 @@ int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t fra
   FVSR_TRY(launch_pack_pool(a, pg, sl, dim3(r->n_tiles, 1, r->heads), 1, s));
   r->used[layer][slot] = 1;
   c.emplace_back(frame_id, slot);
+  ++r->gen[layer];
   return after_launch(ctx, s, 1);
 }
 
@@ -1044,6 +1068,7 @@ int32_t fvsr_ring_evict_sliding(fvsr_ring* r, int32_t layer) {
   while ((int)c.size() > r->window) {  // kv_cache.cpp:100-106
     r->used[layer][c.front().second] = 0;
     c.erase(c.begin());
+    ++r->gen[layer];
   }
   return FVSR_OK;
 }
@@ -1056,6 +1081,7 @@ int32_t fvsr_ring_evict_keep(fvsr_ring* r, int32_t layer, int32_t keep) {
   while ((int)c.size() > keep) {  // sliding: oldest first (kv_cache.cpp:100-106)
     r->used[layer][c.front().second] = 0;
     c.erase(c.begin());
+    ++r->gen[layer];
   }
   return FVSR_OK;
 }
@@ -1149,6 +1175,11 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
     FVSR_TRY(launch_select(ctx, g, dm, r->heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, r->s0_layer(layer),
                            r->s1_layer(layer), r->part_head_stride(), cscale, topk, cap, use_sel, use_cnt, nullptr,
                            nullptr, nullptr, s));
+    ctx->stamp.ring = r;
+    ctx->stamp.layer = layer;
+    ctx->stamp.gen = r->gen[layer];
+    ctx->stamp.qids.assign(q_frame_ids, q_frame_ids + nq);
+    ctx->stamp.mask = mask ? *mask : fvsr_mask{};
   }
   const long long units_total = (long long)r->heads * g.nq_trows * g.n_tiles;
   if (unit_end < 0 || unit_end > units_total) unit_end = units_total;
@@ -1255,10 +1286,16 @@ int32_t fvsr_ring_frame_mass(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const i
   FVSR_TRY(build_geom(&gq, &gk, r->d, kslots.data(), g));
   DevMask dm;
   FVSR_TRY(build_mask(mask, g, grid_tokens(&gk), dm));
-  if (ctx->scores_heads != r->heads || ctx->scores_bnq != g.bnq || ctx->scores_bnk != g.bnk)
+  fvsr_ctx::ScoreStamp want;
+  want.ring = r;
+  want.layer = layer;
+  want.gen = r->gen[layer];
+  want.qids.assign(q_frame_ids, q_frame_ids + nq);
+  want.mask = mask ? *mask : fvsr_mask{};
+  if (ctx->scores_heads != r->heads || ctx->scores_bnq != g.bnq || ctx->scores_bnk != g.bnk || !(ctx->stamp == want))
     return fail(FVSR_E_CONFIG,
-                "ring_frame_mass: no coarse scores of this layer-step on the context (call right after "
-                "fvsr_ring_attention of the same layer, before evicting)");
+                "ring_frame_mass: the coarse scores on the context are not those of this ring, layer, frame set, "
+                "query frames and mask (call right after fvsr_ring_attention of the same layer, before evicting)");
   return launch_frame_mass(ctx, g, dm, r->heads, ctx->d_scores, mass, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -1294,6 +1331,7 @@ int32_t fvsr_ring_evict(fvsr_ring* r, int32_t layer, int32_t strategy, const dou
       if (c[i].first == id) {
         r->used[layer][c[i].second] = 0;
         c.erase(c.begin() + (long)i);
+        ++r->gen[layer];
         break;
       }
   return FVSR_OK;
@@ -1316,11 +1354,7 @@ int launch_token_mask(fvsr_ctx* ctx, const int32_t* labels_host, long long L, in
   FVSR_CUDA(cudaMemcpyAsync(ws, labels_host, smem, cudaMemcpyHostToDevice, s));
   const int kk = by_segment ? 2 : kind;
   auto kern = kk == 0 ? token_mask_kernel<0> : (kk == 1 ? token_mask_kernel<1> : token_mask_kernel<2>);
-  static size_t configured[3] = {48 * 1024, 48 * 1024, 48 * 1024};
-  if (smem > configured[kk]) {
-    FVSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[kk] = smem;
-  }
+  FVSR_TRY(ensure_smem(kern, smem));
   int sms = 148;
   (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   const long long nrows = by_segment ? n_segments : L;

@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           fullmask = __ballot_sync(0xffffffffu, tt < n && g.k_tr_count[sel_at(sel, tt) / g.n_tiles] == 2);
         }
         const bool full = ((fullmask >> (t & 31)) & 1u) != 0u;
-        const uint32_t tO = tO0 + ((G % kGroups) * kOB + ob) * NQ;
+        const uint32_t tO = tO0 + ((t % kGroups) * kOB + ob) * NQ;
         if (lane == 0) trace_at(p, 16, G);
         mbar_wait(pv_go + gb, gph);
         if (lane == 0) trace_at(p, 17, G);
@@ -931,7 +931,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       for (int i = 0; i < CPT; ++i) lp[i] = 0.0f;
       const int ob = U & 1;
       const uint32_t tO = tO0 + (grp * kOB + ob) * NQ;
-      const int t_first = (grp - (T % kGroups) + kGroups) % kGroups;
+      // tile t of a unit belongs to group t % kGroups whatever the CTA ran before, so a unit's
+      // output is a function of the unit alone (sharded == unsharded, bit for bit)
+      const int t_first = grp;
       bool any = false;  // this group processed a tile of the unit (its O^T is defined)
 
       auto info_at = [&](int tt) { return tt < kInfoCap ? info[tt] : tile_info(g, sel_at(sel, tt)); };

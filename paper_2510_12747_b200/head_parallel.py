@@ -4,7 +4,9 @@ The reference processes heads serially (P/src/stream.cpp:237-256; P =
 /root/reference/proj); heads and, within a head, query tiles are independent given K/V,
 so the (head, q-tile) work units shard with no exchange except gathering the outputs.
 
-    units  = heads * nq * tiles            (unit = head*(nq*tiles) + frame*tiles + tile)
+    units  = heads * n_trows * tiles       (unit = head*(n_trows*tiles) + trow*tiles + tile)
+             a temporal row holds one query frame (64 rows per unit) or the two frames
+             2m, 2m+1 of a (2,8,8) q-block (128 rows per unit, the Tq=2 chunk): unit_space()
     rank r owns units [r*per, min(U, (r+1)*per)), per = ceil(U / N)
     ring   = KV for heads [h0, h1) that its units touch (a head split across two ranks
              has its K/V on both; 12 heads over 8 GPUs split 1.5 heads per rank)
@@ -54,6 +56,23 @@ class Shard:
         return self.h1 - self.h0
 
 
+def unit_space(q_frame_ids) -> Tuple[int, int]:
+    """(n_trows, frames_per_unit) of the attention kernel's unit space for these query frames:
+    consecutive frames sharing frame // 2 form one temporal row (P/src/partition.cpp:38-62).
+    Sharded (unit-range / tile-major) attention needs rows of equal height."""
+    ids = [int(f) for f in q_frame_ids]
+    counts = []
+    for i, f in enumerate(ids):
+        if i > 0 and f // 2 == ids[i - 1] // 2:
+            counts[-1] += 1
+        else:
+            counts.append(1)
+    if len(set(counts)) != 1:
+        raise ValueError("head-parallel attention needs query temporal rows of equal height "
+                         f"(frames {ids} give rows of {counts} frames)")
+    return len(counts), counts[0]
+
+
 def shard(total_units: int, units_per_head: int, world: int, rank: int) -> Shard:
     per = -(-total_units // world)
     u0 = min(total_units, rank * per)
@@ -65,28 +84,37 @@ def shard(total_units: int, units_per_head: int, world: int, rank: int) -> Shard
     return Shard(rank, world, total_units, per, u0, u1, units_per_head, h0, h1)
 
 
-def untile_index(heads: int, nq: int, rows: int, cols: int, device=None) -> Tuple[torch.Tensor, torch.Tensor]:
-    """(src_row, dst_row) index pairs mapping tile-major rows [units*64] to token-major rows
-    [heads*nq*rows*cols]; padding rows of ragged tiles are dropped."""
+def untile_index(heads: int, nq: int, rows: int, cols: int, device=None,
+                 frames_per_unit: int = 1) -> Tuple[torch.Tensor, torch.Tensor]:
+    """(src_row, dst_row) index pairs mapping tile-major rows [units * 64*frames_per_unit]
+    to token-major rows [heads*nq*rows*cols]; padding rows of ragged tiles are dropped.
+    frames_per_unit = 2 for paired query frames (unit_space), whose units hold 128 rows:
+    rows 0-63 frame 2m, rows 64-127 frame 2m+1 of the same 8x8 tile."""
     tw, th = (cols + 7) // 8, (rows + 7) // 8
     tiles = tw * th
-    u = torch.arange(heads * nq * tiles, device=device)
-    r = torch.arange(64, device=device)
-    head = (u // (nq * tiles))[:, None]
-    f = ((u % (nq * tiles)) // tiles)[:, None]
+    fpu = int(frames_per_unit)
+    if nq % fpu:
+        raise ValueError("nq must be a multiple of frames_per_unit")
+    ntr = nq // fpu
+    u = torch.arange(heads * ntr * tiles, device=device)
+    r = torch.arange(64 * fpu, device=device)
+    head = (u // (ntr * tiles))[:, None]
+    f = ((u % (ntr * tiles)) // tiles)[:, None] * fpu + r[None, :] // 64
     tile = (u % tiles)[:, None]
-    h = (tile // tw) * 8 + r[None, :] // 8
-    w = (tile % tw) * 8 + r[None, :] % 8
+    rr = r[None, :] % 64
+    h = (tile // tw) * 8 + rr // 8
+    w = (tile % tw) * 8 + rr % 8
     valid = (h < rows) & (w < cols)
     dst = (head * nq + f) * rows * cols + h * cols + w
-    src = u[:, None] * 64 + r[None, :]
+    src = u[:, None] * (64 * fpu) + r[None, :]
     return src[valid], dst[valid]
 
 
-def untile(tiles: torch.Tensor, heads: int, nq: int, rows: int, cols: int, index=None) -> torch.Tensor:
-    """Tile-major [>=units, 64, d] -> token-major [heads, nq*rows*cols, d]."""
+def untile(tiles: torch.Tensor, heads: int, nq: int, rows: int, cols: int, index=None,
+           frames_per_unit: int = 1) -> torch.Tensor:
+    """Tile-major [>=units, 64*frames_per_unit, d] -> token-major [heads, nq*rows*cols, d]."""
     d = tiles.shape[-1]
-    src, dst = index if index is not None else untile_index(heads, nq, rows, cols, tiles.device)
+    src, dst = index if index is not None else untile_index(heads, nq, rows, cols, tiles.device, frames_per_unit)
     out = torch.empty((heads * nq * rows * cols, d), dtype=tiles.dtype, device=tiles.device)
     out[dst] = tiles.reshape(-1, d)[src]
     return out.view(heads, nq * rows * cols, d)
@@ -95,10 +123,11 @@ def untile(tiles: torch.Tensor, heads: int, nq: int, rows: int, cols: int, index
 class Gatherer:
     """Double-buffered async all-gather of tile-major shards (torch.distributed, NCCL/gloo)."""
 
-    def __init__(self, sh: Shard, d: int, device, dtype=torch.bfloat16, group=None):
+    def __init__(self, sh: Shard, d: int, device, dtype=torch.bfloat16, group=None, frames_per_unit: int = 1):
         self.sh, self.group = sh, group
-        self.shards = [torch.zeros((sh.per, 64, d), dtype=dtype, device=device) for _ in range(2)]
-        self.full = [torch.empty((sh.per * sh.world, 64, d), dtype=dtype, device=device) for _ in range(2)]
+        rows = 64 * int(frames_per_unit)
+        self.shards = [torch.zeros((sh.per, rows, d), dtype=dtype, device=device) for _ in range(2)]
+        self.full = [torch.empty((sh.per * sh.world, rows, d), dtype=dtype, device=device) for _ in range(2)]
         self.work = [None, None]
         self.i = 0
 

@@ -41,6 +41,7 @@ class KVRing:
         h = C.c_void_p()
         check(self.ctx.lib.fvsr_ring_create(self.ctx.h, layers, heads, d, rows, cols, window_frames, C.byref(h)))
         self.h = h
+        self._last_mask = {}  # layer -> mask of the last attention call (frame_mass default)
 
     def __del__(self):
         try:
@@ -80,8 +81,9 @@ class KVRing:
     def frame_mass(self, layer: int, q_frame_ids: Sequence[int], mask: Optional[Mask] = None,
                    check_errors: bool = True) -> torch.Tensor:
         """frame_attention_mass of the plan of the preceding ``attention`` call on this
-        layer (same q frames and mask): float64 [heads, retained frames] on the device."""
-        mask = mask or Mask.all_allowed()
+        layer (same q frames and mask): float64 [heads, retained frames] on the device.  The
+        mask defaults to that call's; the library refuses scores of any other call."""
+        mask = mask or self._last_mask.get(layer) or Mask.all_allowed()
         nq = len(q_frame_ids)
         ids = (C.c_int32 * nq)(*[int(f) for f in q_frame_ids])
         md = mask.c()
@@ -119,6 +121,7 @@ class KVRing:
                   sel: Optional[torch.Tensor] = None, sel_count: Optional[torch.Tensor] = None,
                   check_errors: bool = True) -> torch.Tensor:
         mask = mask or Mask.all_allowed()
+        self._last_mask[layer] = mask
         q3 = _heads3(q, "ring attention q")
         nq = len(q_frame_ids)
         if q3.shape != (self.heads, nq * self.tokens_per_frame, self.d):
@@ -127,10 +130,12 @@ class KVRing:
             scale = 1.0 / math.sqrt(self.d)
         if out is None:
             if tile_major:
+                from .head_parallel import unit_space
+                ntr, fpu = unit_space(q_frame_ids)
                 tiles = ((self.rows + 7) // 8) * ((self.cols + 7) // 8)
-                total = self.heads * nq * tiles
+                total = self.heads * ntr * tiles
                 u1 = total if unit_end < 0 else min(unit_end, total)
-                out = torch.empty(((u1 - unit_begin), 64, self.d), dtype=torch.bfloat16, device=q3.device)
+                out = torch.empty(((u1 - unit_begin), 64 * fpu, self.d), dtype=torch.bfloat16, device=q3.device)
             else:
                 out = torch.empty_like(q3)
         ids = (C.c_int32 * nq)(*[int(f) for f in q_frame_ids])

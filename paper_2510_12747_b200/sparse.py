@@ -99,6 +99,7 @@ class SparsePlan:
     diagonal_block: torch.Tensor # int32 [heads, bnq]
     coarse_scores: Optional[torch.Tensor] = None   # float32 [heads, bnq, bnk]
     coarse_allowed: Optional[torch.Tensor] = None  # uint8 [heads, bnq, bnk]
+    mask: Optional["Mask"] = None                  # the token mask the plan was built with
 
     @property
     def heads(self) -> int:
@@ -241,7 +242,7 @@ def plan_sparse(q: torch.Tensor, k: torch.Tensor, grid_q: TokenGrid, grid_k: Opt
                                    allowed.data_ptr() if allowed is not None else None, _stream()))
     if check_errors:
         ctx.check_errors()
-    return SparsePlan(int(topk), d, grid_q, grid_k, sel, cnt, diag, coarse, allowed)
+    return SparsePlan(int(topk), d, grid_q, grid_k, sel, cnt, diag, coarse, allowed, mask)
 
 
 def sparse_attention_exec(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: SparsePlan,
@@ -310,13 +311,27 @@ def build_causal_mask(frame, lookahead: int = 0, *, ctx: Optional[Context] = Non
     return Mask.bitmask(bits)
 
 
+def _same_mask(a: "Mask", b: "Mask") -> bool:
+    if a.kind != b.kind:
+        return False
+    if a.kind == MASK_ALL:
+        return True
+    if a.kind == MASK_LOCALITY:
+        return (a.mode, a.extent_h, a.extent_w) == (b.mode, b.extent_h, b.extent_w)
+    return a.bits is b.bits or (a.bits.shape == b.bits.shape and bool(torch.equal(a.bits, b.bits)))
+
+
 def frame_attention_mass(plan: SparsePlan, key_grid: Optional[TokenGrid] = None, mask: Optional[Mask] = None, *,
                          ctx: Optional[Context] = None, check_errors: bool = True) -> torch.Tensor:
     """frame_attention_mass (P/src/kv_cache.cpp:170-206) on device: float64 [heads, frames]
-    of key_grid (default plan.grid_k).  `mask` must be the one the plan was built with (it
-    defines the coarse-allowed blocks); the plan must keep its coarse scores."""
+    of key_grid (default plan.grid_k).  The coarse-allowed blocks are the plan's own, as in
+    the reference (kv_cache.cpp:177-188): the mask defaults to the one the plan was built with,
+    and a different one is refused.  The plan must keep its coarse scores."""
     ctx = ctx or Context.default()
-    mask = mask or Mask.all_allowed()
+    own = plan.mask or Mask.all_allowed()
+    if mask is not None and not _same_mask(mask, own):
+        raise ConfigError("frame_attention_mass: mask differs from the one the plan was built with")
+    mask = own
     key_grid = key_grid or plan.grid_k
     if plan.coarse_scores is None:
         raise ConfigError("frame_attention_mass: plan was built without coarse scores (keep_scores=False)")

@@ -56,3 +56,26 @@ def to_oracle_mask(m):
     if m.kind == 1:
         return oracle.Mask.locality(m.extent_h, m.extent_w, truncated=(m.mode == 1))
     return oracle.Mask.bitmask(m.bits.cpu().numpy().view(np.uint64))
+
+
+def par_map(fn, items, workers=None):
+    """Run oracle calls in threads (the C port releases the GIL inside ctypes calls); each
+    call must build its own oracle.Port (Port keeps per-instance keep-alive buffers)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    items = list(items)
+    workers = workers or max(1, min(len(items), os.cpu_count() or 1))
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(fn, items))
+
+
+def record_parity(case: str, **fields) -> None:
+    """Append one per-shape parity line (rel_l2, max_abs, ...) to $FVSR_PARITY_REPORT (JSON
+    lines) when set; tools/parity_report.py turns it into profiles/parity_*.json."""
+    import json
+    import os
+    path = os.environ.get("FVSR_PARITY_REPORT")
+    if not path:
+        return
+    with open(path, "a") as f:
+        f.write(json.dumps({"case": case, **fields}) + "\n")

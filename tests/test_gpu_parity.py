@@ -9,8 +9,8 @@ import numpy as np
 import pytest
 
 import oracle
-from tests.helpers import (MAX_ABS_TOL, REL_L2_TOL, max_abs, oracle_outs, oracle_plans, qkv, rel_l2, to_dev,
-                           to_oracle_mask)
+from tests.helpers import (MAX_ABS_TOL, REL_L2_TOL, max_abs, oracle_outs, oracle_plans, qkv, record_parity, rel_l2,
+                           to_dev, to_oracle_mask)
 
 pytestmark = pytest.mark.gpu
 
@@ -73,6 +73,8 @@ def test_exec_within_tolerance(c):
     scale = oracle.head_scale(d)
     out = fv.sparse_attention_exec(to_dev(q), to_dev(k), to_dev(v), plan, mask, scale).float().cpu().numpy()
     ref = oracle_outs(q, k, v, qf, kf, rows, cols, to_oracle_mask(mask), refs, scale)
+    record_parity(name, rows=rows, cols=cols, heads=heads, d=d, topk=topk, q_frames=qf, k_frames=kf,
+                  indices_bit_exact=True, rel_l2=rel_l2(out, ref), max_abs=max_abs(out, ref))
     assert rel_l2(out, ref) <= REL_L2_TOL, (name, rel_l2(out, ref))
     assert max_abs(out, ref) <= MAX_ABS_TOL, (name, max_abs(out, ref))
 

@@ -8,7 +8,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2510_12747_b200.head_parallel import Gatherer, full_frame_mass, shard, uniform_total, untile, untile_index
+from paper_2510_12747_b200.head_parallel import (Gatherer, full_frame_mass, shard, uniform_total, unit_space, untile,
+                                                 untile_index)
 
 
 @pytest.mark.parametrize("heads,nq,tiles,world", [(12, 1, 66, 1), (12, 1, 66, 2), (12, 1, 66, 4),
@@ -45,6 +46,30 @@ def test_untile_inverts_tiling(rows, cols, nq):
     assert torch.equal(untile(tiles, heads, nq, rows, cols), x)
     src, dst = untile_index(heads, nq, rows, cols)
     assert dst.numel() == heads * nq * rows * cols and torch.equal(dst.sort().values, torch.arange(dst.numel()))
+
+
+@pytest.mark.parametrize("rows,cols", [(16, 16), (20, 28), (13, 9)])
+def test_untile_paired_query_frames(rows, cols):
+    """Paired query frames (2m, 2m+1: one temporal row, the Tq=2 chunk): the kernel's unit is
+    [128 rows] = frame 2m tile rows 0-63 then frame 2m+1 (kernel_attn.cu NQ=128)."""
+    heads, d, qf = 2, 4, [6, 7]
+    ntr, fpu = unit_space(qf)
+    assert (ntr, fpu) == (1, 2)
+    nq = len(qf)
+    x = torch.randn(heads, nq * rows * cols, d)
+    tw, th = (cols + 7) // 8, (rows + 7) // 8
+    tiles = torch.zeros(heads * ntr * tw * th, 128, d)
+    for h in range(heads):
+        for t in range(tw * th):
+            for r in range(128):
+                f, rr = r // 64, r % 64
+                hh, ww = (t // tw) * 8 + rr // 8, (t % tw) * 8 + rr % 8
+                if hh < rows and ww < cols:
+                    tiles[h * tw * th + t, r] = x[h, f * rows * cols + hh * cols + ww]
+    assert torch.equal(untile(tiles, heads, nq, rows, cols, frames_per_unit=2), x)
+    assert unit_space([5, 6]) == (2, 1) and unit_space([4, 5, 6, 7]) == (2, 2)
+    with pytest.raises(ValueError):
+        unit_space([3, 4, 5])
 
 
 def _free_port():
