@@ -309,6 +309,7 @@ def run_b200(args):
     # per-kernel-class CUDA-event spans, in a separate pass after the timed region (events
     # between the kernels would serialise their programmatic-dependent-launch overlap)
     span_steps = min(args.steps, 200)
+    ctx.read_tiles()  # reset the key-tile counters
     ctx.timing(True)
     for _ in range(span_steps):
         step()
@@ -318,6 +319,7 @@ def run_b200(args):
     ctx.timing(False)
     ctx.check_errors()
     pairs_span = ctx.read_pairs()
+    tiles_span, full_span = ctx.read_tiles()
     attn_ms, attn_n = ctx.timing_read(_abi.TIME_ATTENTION)
     mb_ms, mb_n = ctx.timing_read(_abi.TIME_MASK_BUILDER)
     ap_ms, ap_n = ctx.timing_read(_abi.TIME_APPEND, clear=True)
@@ -429,6 +431,14 @@ def run_b200(args):
                 "flops_per_launch": 4.0 * D * pairs_per_launch,
                 "flop_def": "4*d per executed (mask-allowed, selected-block) token pair, counted by the kernel",
                 "avg_launch_us": attn_avg_ms * 1e3, "launches": attn_n}
+    # tile-level tensor work (every issued MMA, incl. masked/padding lanes): QK^T over 128 key
+    # rows and PV over the tile's valid rows (128, or 64 for a lone single-frame block)
+    nt_l, nf_l = tiles_span / max(1, attn_n), full_span / max(1, attn_n)
+    tile_flops = nt_l * 2 * 128 * 64 * D + (nf_l * 128 + (nt_l - nf_l) * 64) * 2 * 64 * D
+    roofline["tiles_per_launch"] = nt_l
+    roofline["full_tiles_per_launch"] = nf_l
+    roofline["tile_tflops"] = tile_flops / (attn_avg_ms / 1e3) / 1e12
+    roofline["tile_flops_per_launch"] = tile_flops
     mb_avg = mb_ms / max(1, mb_n)
     bnk = 3 * tiles  # context {28..32}: t_rows 14, 15, 16
     mb_bytes = nh * N * D * 2 + nh * bnk * D * 4 + nh * tiles * TOPK * 4  # Q once, pooled K, indices

@@ -139,6 +139,10 @@ FVSR_API int32_t fvsr_ctx_timing_read(fvsr_ctx* ctx, int32_t kind, double* total
 /* Executed (mask-allowed, selected-block) token pairs counted by the attention kernel since
  * the last read — the reference's sparsity_report definition; synchronizes and resets. */
 FVSR_API int32_t fvsr_ctx_read_pairs(fvsr_ctx* ctx, uint64_t* executed_pairs);
+/* Key tiles the attention kernel issued since the last read (and how many of them carried
+ * 128 key rows: two-frame blocks or two paired single-frame blocks); resets the counters.
+ * Tile-level tensor work = tiles x (QK^T 2*128*NQ*d) + PV over the valid key rows. */
+FVSR_API int32_t fvsr_ctx_read_tiles(fvsr_ctx* ctx, uint64_t* tiles, uint64_t* full_tiles);
 
 /* ---- geometry (host only) ----------------------------------------------------------- */
 /* Block counts of partition_blocks(grid_q) / partition_blocks(grid_k) (P/src/partition.cpp:38-62). */

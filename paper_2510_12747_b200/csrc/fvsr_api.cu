@@ -74,6 +74,7 @@ struct fvsr_ctx {
   int flags = 0;
   unsigned* d_err = nullptr;
   unsigned long long* d_pairs = nullptr;  // executed token pairs, accumulated by the attention kernel
+  unsigned long long* d_tiles = nullptr;  // [2] key tiles issued / of them with 128 key rows
   // optional CUDA-event spans per kernel class (fvsr_ctx_timing_enable)
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -531,20 +532,14 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
                      long long unit_begin, long long unit_end, cudaStream_t s) {
   if (g.d != 64 && g.d != 128)
     return fail(FVSR_E_CONFIG, "sparse_attention_exec: head_dim %d unsupported (64 or 128)", g.d);
+  // key-tile descriptors: 5-bit frame index (31 = empty half), 5-bit tile row, 6-bit tile column
+  if (g.nkf > kMaxKeyFrames)
+    return fail(FVSR_E_CONFIG, "sparse_attention_exec: %d key frames exceeds the kernel limit of %d", g.nkf,
+                kMaxKeyFrames);
+  if (g.tiles_h > kMaxTilesH || g.tiles_w > kMaxTilesW)
+    return fail(FVSR_E_CONFIG, "sparse_attention_exec: frame of %dx%d tokens exceeds the kernel limit of %dx%d",
+                g.rows, g.cols, 8 * kMaxTilesH, 8 * kMaxTilesW);
   const bool uniform = trows_uniform(g);
-  // experiments (builds with -DFVSR_ATTN_INSTRUMENT=1 only): debug short-cuts, timelines
-  if (kInstrument)
-    if (const char* dbg = std::getenv("FVSR_ATTN_DEBUG")) p.debug = std::atoi(dbg);
-  static long long* trace = nullptr;
-  static int trace_calls = 0;
-  const bool tracing =
-      (kInstrument || kCtaTimeline) && std::getenv("FVSR_ATTN_TRACE") != nullptr && ++trace_calls == 20;
-  if (tracing) {
-    const size_t tn = kTraceEvents * kTraceTiles + 1024 * kTraceCtaSlots;
-    if (!trace) cudaMalloc(&trace, tn * sizeof(long long));
-    cudaMemsetAsync(trace, 0, tn * sizeof(long long), s);
-    p.trace = trace;
-  }
   int sms = 0;
   FVSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
   SpanGuard sg(ctx, s, FVSR_TIME_ATTENTION);
@@ -563,60 +558,6 @@ int launch_attention(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, AttnPar
       st = nq == 1 ? launch_attn_dq<64, 64>(g, dm, p, sms, s) : launch_attn_dq<64, 128>(g, dm, p, sms, s);
     FVSR_TRY(st);
     ctx->launches += 1;
-  }
-  if (tracing) {  // experiments only: per-tile pipeline timeline of CTA 0
-    std::vector<long long> h(kTraceEvents * kTraceTiles + 1024 * kTraceCtaSlots);
-    cudaStreamSynchronize(s);
-    cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-    const char* names[kTraceEvents] = {"K",    "QK",   "S0",  "P0",  "PV",    "V",     "vote",  "rare",
-                                       "exps", "pbuf", "sts", "fence", "QKmma", "QKcmt", "PVmma", "PVcmt",
-                                       "wV",   "wP",   "wK",  "wS",    "ld0",   "vt0",   "ex0",   "st0",
-                                       "ld1",  "vt1",  "ex1", "st1",
-                                       "Ebeg", "El",   "Eof", "Eo",    "Est",   "Unx",   "Utab",  "Qiss"};
-    const long long base = h[0];
-    std::fprintf(stderr, "trace (cycles from first K issue), tiles 0..60\n  G");
-    for (int e = 0; e < kTraceEvents; ++e) std::fprintf(stderr, "%9s", names[e]);
-    std::fprintf(stderr, "\n");
-    for (int G = 0; G < 60; ++G) {
-      std::fprintf(stderr, "%3d", G);
-      for (int e = 0; e < kTraceEvents; ++e) std::fprintf(stderr, "%9lld", h[e * kTraceTiles + G] ? h[e * kTraceTiles + G] - base : -1);
-      std::fprintf(stderr, "\n");
-    }
-    std::fprintf(stderr, "per-unit (cycles from first K issue):\n");
-    for (int U = 0; U < 8; ++U) {
-      std::fprintf(stderr, "U%d", U);
-      for (int e = 28; e < kTraceEvents; ++e)
-        std::fprintf(stderr, " %s=%lld", names[e], h[e * kTraceTiles + U] ? h[e * kTraceTiles + U] - base : -1);
-      std::fprintf(stderr, "\n");
-    }
-    // per-CTA unit timeline (globaltimer ns)
-    const long long* ct = h.data() + kTraceEvents * kTraceTiles;
-    long long t0 = LLONG_MAX, tend = 0;
-    for (int b = 0; b < sms; ++b) if (ct[b * kTraceCtaSlots]) t0 = std::min(t0, ct[b * kTraceCtaSlots]);
-    std::vector<double> unit_us, end_us, start_us;
-    for (int b = 0; b < sms; ++b) {
-      const long long* r = ct + b * kTraceCtaSlots;
-      start_us.push_back((r[0] - t0) * 1e-3);
-      long long prev = r[0];
-      for (int k = 1; k < kTraceCtaSlots / 2 && r[k]; ++k) { unit_us.push_back((r[k] - prev) * 1e-3); prev = r[k]; }
-      end_us.push_back((prev - t0) * 1e-3);
-      tend = std::max(tend, prev);
-    }
-    std::sort(unit_us.begin(), unit_us.end());
-    std::sort(end_us.begin(), end_us.end());
-    std::sort(start_us.begin(), start_us.end());
-    auto pct = [](const std::vector<double>& v, double q) { return v.empty() ? 0.0 : v[(size_t)(q * (v.size() - 1))]; };
-    std::fprintf(stderr, "cta timeline: makespan %.1f us; start p0/p50/p100 %.1f/%.1f/%.1f; end p0/p50/p100 %.1f/%.1f/%.1f\n",
-                 (tend - t0) * 1e-3, pct(start_us, 0), pct(start_us, .5), pct(start_us, 1), pct(end_us, 0),
-                 pct(end_us, .5), pct(end_us, 1));
-    std::fprintf(stderr, "unit us: n=%zu p0 %.1f p10 %.1f p50 %.1f p90 %.1f p100 %.1f\n", unit_us.size(), pct(unit_us, 0),
-                 pct(unit_us, .1), pct(unit_us, .5), pct(unit_us, .9), pct(unit_us, 1));
-    const long long* r0 = ct;
-    std::fprintf(stderr, "cta0 units (us / kcycles / MHz):");
-    for (int k = 1; k < kTraceCtaSlots / 2 && r0[k]; ++k)
-      std::fprintf(stderr, " %.1f/%.1f/%.0f", (r0[k] - r0[k - 1]) * 1e-3, (r0[8 + k] - r0[8 + k - 1]) * 1e-3,
-                   (double)(r0[8 + k] - r0[8 + k - 1]) / (double)(r0[k] - r0[k - 1]) * 1e3);
-    std::fprintf(stderr, "\n");
   }
   return FVSR_OK;
 }
@@ -659,13 +600,16 @@ int32_t fvsr_ctx_create(fvsr_ctx** out) {
   auto* c = new fvsr_ctx();
   c->device = dev;
   if (cudaMalloc(&c->d_err, sizeof(unsigned)) != cudaSuccess ||
-      cudaMalloc(&c->d_pairs, sizeof(unsigned long long)) != cudaSuccess) {
+      cudaMalloc(&c->d_pairs, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&c->d_tiles, 2 * sizeof(unsigned long long)) != cudaSuccess) {
     cudaFree(c->d_err);
+    cudaFree(c->d_pairs);
     delete c;
     return fail(FVSR_E_NOMEM, "error word allocation failed");
   }
   cudaMemset(c->d_err, 0, sizeof(unsigned));
   cudaMemset(c->d_pairs, 0, sizeof(unsigned long long));
+  cudaMemset(c->d_tiles, 0, 2 * sizeof(unsigned long long));
   *out = c;
   return FVSR_OK;
 }
@@ -674,6 +618,7 @@ void fvsr_ctx_destroy(fvsr_ctx* ctx) {
   if (!ctx) return;
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_pairs);
+  cudaFree(ctx->d_tiles);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->stage) cudaFree(ctx->stage);
@@ -724,6 +669,17 @@ int32_t fvsr_ctx_read_pairs(fvsr_ctx* ctx, uint64_t* executed_pairs) {
   FVSR_CUDA(cudaMemcpy(&v, ctx->d_pairs, sizeof(v), cudaMemcpyDeviceToHost));
   FVSR_CUDA(cudaMemset(ctx->d_pairs, 0, sizeof(v)));
   if (executed_pairs) *executed_pairs = v;
+  return FVSR_OK;
+}
+
+int32_t fvsr_ctx_read_tiles(fvsr_ctx* ctx, uint64_t* tiles, uint64_t* full_tiles) {
+  FVSR_TRY(check_ctx(ctx));
+  FVSR_CUDA(cudaDeviceSynchronize());
+  unsigned long long v[2] = {0, 0};
+  FVSR_CUDA(cudaMemcpy(v, ctx->d_tiles, sizeof(v), cudaMemcpyDeviceToHost));
+  FVSR_CUDA(cudaMemset(ctx->d_tiles, 0, sizeof(v)));
+  if (tiles) *tiles = v[0];
+  if (full_tiles) *full_tiles = v[1];
   return FVSR_OK;
 }
 
@@ -832,6 +788,7 @@ int32_t fvsr_sparse_attention_exec(fvsr_ctx* ctx, const uint16_t* q, const uint1
   p.out_tile_major = 0;
   p.err = ctx->d_err;
   p.pairs = ctx->d_pairs;
+  p.tiles = ctx->d_tiles;
   FVSR_TRY(launch_attention(ctx, g, dm, p, heads, 0, -1, s));
   return after_launch(ctx, s, 3);
 }
@@ -869,8 +826,11 @@ int32_t fvsr_ring_create(fvsr_ctx* ctx, int32_t layers, int32_t heads, int32_t d
     return fail(FVSR_E_CONFIG, "KVCache: empty extents");  // kv_cache.cpp:31
   if (rows < 1 || cols < 1) return fail(FVSR_E_CONFIG, "TokenGrid: empty extents");
   if (d != 64 && d != 128) return fail(FVSR_E_CONFIG, "ring: head_dim %d unsupported (64 or 128)", d);
-  if (window_frames + 1 > kMaxFrames)
-    return fail(FVSR_E_CONFIG, "ring: window %d exceeds the kernel limit of %d frames", window_frames, kMaxFrames - 1);
+  if (window_frames + 1 > kMaxKeyFrames)
+    return fail(FVSR_E_CONFIG, "ring: window %d exceeds the kernel limit of %d frames", window_frames, kMaxKeyFrames - 1);
+  if ((rows + 7) / 8 > kMaxTilesH || (cols + 7) / 8 > kMaxTilesW)
+    return fail(FVSR_E_CONFIG, "ring: frame of %dx%d tokens exceeds the kernel limit of %dx%d", rows, cols,
+                8 * kMaxTilesH, 8 * kMaxTilesW);
   auto* r = new fvsr_ring();
   r->layers = layers;
   r->heads = heads;
@@ -1203,6 +1163,7 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   p.out_tile_major = out_layout == FVSR_OUT_TILE_MAJOR ? 1 : 0;
   p.err = ctx->d_err;
   p.pairs = ctx->d_pairs;
+  p.tiles = ctx->d_tiles;
   p.kn2 = r->kn2_layer(layer);
   p.kn2_head_stride = r->kn2_head_stride();
   p.qn2 = qn2;

@@ -12,28 +12,38 @@
 // and M=64 runs at half rate, so the kernel is TRANSPOSED: keys sit on the M=128 axis.
 //     S^T[128 keys x NQ]  = K_tile[128 x d] . Q^T                 (K-major A, K-major B)
 //     O^T[d x NQ]        += V_tile^T[d x 128] . P^T[128 keys x NQ] (MN-major A, MN-major B)
-// A key block is exactly one 128-row tile (frames 2m, 2m+1 of one 8x8 tile); a 64-row
-// block (one frame of the pair in context) issues only its 4 valid PV K-steps.
+//
+// Key tiles.  A selected block of two frames (2m, 2m+1 of one 8x8 tile) fills the 128 key
+// rows of a tile: rows 0-63 frame 2m, rows 64-127 frame 2m+1.  A single-frame block (the
+// current even frame, an odd frame whose partner was evicted) has 64 keys; consecutive
+// single-frame blocks of a selection are PAIRED into one tile (rows 0-63 the first, 64-127
+// the second), so every MMA tile and every softmax pass carries 128 real keys.  The order
+// of the keys only changes fp32 rounding: the softmax is order-free.  A tile descriptor is
+// two 16-bit halves (frame index, tile row, tile col), built per unit by the table builder.
 //
 // Softmax in the transposed layout: TMEM lane j holds key j's scores for all queries.
 // Softmax warps = 4 lane quarters x NQ/32 column groups; a column group (4 warps, 128
 // lanes) owns 32 query columns and keeps, per column, a running reference c (log2 units)
-// and per-thread partial denominators.  The reference only moves when a score exceeds it
-// by > 8 (FA4-style lazy rescale), decided by one bar.red.or across the group per tile;
-// on the rare exceed path (always on a column's first real tile) the exact column max is
-// a warp butterfly + smem, then O^T columns in TMEM and the partial sums are rescaled.
-// Denominators are reduced across lanes once per unit.
+// and per-thread partial denominators.  Fixed-reference units (|q||k| bounds every score)
+// keep c = 0; otherwise the reference only moves when a score exceeds it by > 8 (FA4-style
+// lazy rescale), decided by one bar.red.or across the group per tile.
 //
-// Persistent CTAs (round-robin over units).  Roles: softmax warps [0, SW), warp SW
-// Q/K producer, SW+1 MMA issuer (+ TMEM allocator), SW+2 V producer; producers and the
-// MMA issuer run warp-wide (uniform registers) and elect one lane to issue.  S^T has NS
-// TMEM buffers so QK runs NS-1 tiles ahead of PV; O^T is double-buffered across units.
+// Persistent CTAs (round-robin over units), 16 warps: 8 softmax (two ping-pong groups:
+// tile t of a unit belongs to group t % 2), Q/K producer, QK issuer (+ TMEM allocator),
+// V producer, PV issuer, and an epilogue warpgroup that merges the groups' O^T, stores the
+// output and builds each unit's tables one unit ahead.
 #include "fvsr_common.cuh"
 
 namespace fvsr {
 
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr int kInfoCap = 256;              // per-unit tile-info table entries
+constexpr int kInfoCap = 256;              // per-unit tile-descriptor table entries
+constexpr float kBoundSlack = 64.0f;       // log2 units: p <= 2^64 keeps O, l and bf16 P finite
+constexpr float kFixedBound = 60.0f;       // |s*scale*log2e| <= 60 for the unit: fixed reference 0
+constexpr int kQkLead = 3;                 // QK(G) waits for PV(G - kQkLead) to be issued
+constexpr uint32_t kHalfNone = 0xF800u;    // tile half without keys (frame index 31)
+constexpr int kMaxKeyFrames = 31;          // frame index 31 marks an empty half
+constexpr int kMaxTilesH = 32, kMaxTilesW = 64;  // tile coordinates of a 16-bit half
 
 struct AttnParams {
   const uint8_t* q;          // packed q frame-tiles [heads][nqf][n_tiles]
@@ -54,8 +64,7 @@ struct AttnParams {
   int out_tile_major;        // 1: out is [unit - unit_begin][NQ][d]
   unsigned* err;
   unsigned long long* pairs; // += executed (mask-allowed, selected-block) token pairs
-  int debug;                 // experiments only (FVSR_ATTN_DEBUG): 1 skip softmax math, 2 skip K/V loads
-  long long* trace;          // experiments only (FVSR_ATTN_TRACE): per-tile clock64 stamps of CTA 0
+  unsigned long long* tiles; // [0] += key tiles issued, [1] += of them with 128 key rows
   // Optional score bounds (null = always vote): max squared key-row norm per (slot, tile) and
   // query-row norm per (q frame, tile).  |s| <= |q||k| lets a column group skip the rescale
   // vote when no score of a tile can exceed the word's references by more than kBoundSlack.
@@ -64,68 +73,10 @@ struct AttnParams {
   const float* qn2;
   long long qn2_head_stride;  // elements
 };
-constexpr float kBoundSlack = 64.0f;  // log2 units: p <= 2^64 keeps O, l and bf16 P finite
-constexpr float kFixedBound = 60.0f;  // |s*scale*log2e| <= 60 for the unit: fixed reference 0
-#ifndef FVSR_FIXED_REF
-#define FVSR_FIXED_REF 1
-#endif
-
-// trace slots [event][tile]: 0 K issued, 1 QK issued, 2 S ready (softmax warp 0), 3 P done
-// (warp 0), 4 PV issued, 5 V issued, 6-11 S ready / P done of softmax warps 3/4/7, 12/13 QK
-// MMAs / commits issued, 14/15 PV MMAs / commits issued.
-constexpr int kTraceTiles = 512;
-constexpr int kTraceEvents = 36;  // 28-35: per-unit epilogue stamps (indexed by unit)
-constexpr int kTraceCtaSlots = 16;  // per CTA: [0] start, [1..7] unit ends (globaltimer ns); +8: clock64
-// Instrumentation (per-tile timeline, debug short-cuts) only exists in builds with
-// -DFVSR_ATTN_INSTRUMENT=1; the production kernel carries none of it.
-#ifndef FVSR_ATTN_INSTRUMENT
-#define FVSR_ATTN_INSTRUMENT 0
-#endif
-constexpr bool kInstrument = FVSR_ATTN_INSTRUMENT != 0;
-// Bottleneck experiments (results are NOT attention): -DFVSR_ATTN_EXP=mask of
-//   1 exp2 replaced by a constant (no MUFU), 2 S^T not read from TMEM (constant scores),
-//   4 no cross-warp rescale vote (exact path only on a group's first tile),
-//   16 no K/V traffic after the first stages (producers arrive without loading),
-//   32 no epilogue (O is never read or stored), 64 epilogue without TMEM loads, 128 epilogue
-//   without the output stores.
-#ifndef FVSR_ATTN_EXP
-#define FVSR_ATTN_EXP 0
-#endif
-constexpr int kExp = FVSR_ATTN_EXP;
-#ifndef FVSR_POLY_EXP
-#define FVSR_POLY_EXP 0
-#endif
-#ifndef FVSR_QK_LEAD
-#define FVSR_QK_LEAD 3
-#endif
-// QK(G) is issued only once PV(G - kQkLead) was issued (0: only the S buffers bound the
-// run-ahead), so PVs do not queue behind several tiles of QK MMAs in the in-order tensor pipe
-constexpr int kQkLead = FVSR_QK_LEAD;
-static_assert(kQkLead >= 0 && kQkLead <= 4, "the pv_iss ring has 4 barriers");
-constexpr int kPolyN = FVSR_POLY_EXP;  // of every 8 exp pairs of an unmasked word, on the FMA pipe
-constexpr bool kPolyExp = kPolyN != 0;
-__device__ __forceinline__ void trace_at(const AttnParams& p, int ev, int G) {
-  if (kInstrument && p.trace && blockIdx.x == 0 && G < kTraceTiles) p.trace[ev * kTraceTiles + G] = clock64();
-}
-__device__ __forceinline__ long long globaltimer() {
-  long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#ifndef FVSR_CTA_TIMELINE
-#define FVSR_CTA_TIMELINE 0
-#endif
-constexpr bool kCtaTimeline = FVSR_CTA_TIMELINE != 0;  // per-CTA unit stamps only (cheap)
-__device__ __forceinline__ void trace_cta(const AttnParams& p, int slot) {
-  if ((kInstrument || kCtaTimeline) && p.trace && slot < kTraceCtaSlots / 2) {
-    p.trace[kTraceEvents * kTraceTiles + blockIdx.x * kTraceCtaSlots + slot] = globaltimer();
-    p.trace[kTraceEvents * kTraceTiles + blockIdx.x * kTraceCtaSlots + 8 + slot] = clock64();
-  }
-}
 
 template <int D, int NQ>
 struct AttnCfg {
-  static constexpr int kSW = 8;                      // softmax warps (two warpgroups, 168 registers)
+  static constexpr int kSW = 8;                      // softmax warps (two warpgroups)
   static constexpr int kGroups = NQ == 64 ? 2 : 1;   // ping-pong softmax groups (tile parity)
   static constexpr int kWG = kSW / kGroups;          // warps per group
   static constexpr int kCGg = kWG / 4;               // column groups per group (4 lane quarters each)
@@ -135,30 +86,21 @@ struct AttnCfg {
   static constexpr int kQkWarp = kSW + 1;            // QK^T issuer (+ TMEM allocator)
   static constexpr int kVProducerWarp = kSW + 2;     // V tiles (decoupled so K runs ahead)
   static constexpr int kPvWarp = kSW + 3;            // PV issuer (own program order: QK never waits on P)
-  static constexpr int kEpiWarp = kSW + 4;           // epilogue warpgroup (merge, normalise, store)
+  static constexpr int kEpiWarp = kSW + 4;           // epilogue warpgroup (merge, normalise, store, tables)
   static constexpr int kThreads = kSW * 32 + 256;    // 16 warps
-#ifndef FVSR_REG_SOFTMAX
-#define FVSR_REG_SOFTMAX 184
-#endif
-  static constexpr int kRegSoftmax = FVSR_REG_SOFTMAX;  // setmaxnreg: 256 x 184 + 256 x 72 = 64K
+  static constexpr int kRegSoftmax = 184;            // setmaxnreg: 256 x 184 + 256 x 72 = 64K
   static constexpr int kRegOther = 256 - kRegSoftmax;
   static constexpr int kNS = NQ == 64 ? 4 : 2;       // S^T buffers in TMEM
   static constexpr int kNK = 2;                      // K stages (QK consumes them right away)
-#ifndef FVSR_NV64
-#define FVSR_NV64 2
-#endif
-#ifndef FVSR_NP64
-#define FVSR_NP64 4
-#endif
-  static constexpr int kNV = NQ == 64 ? FVSR_NV64 : 2;  // V stages (released only after PV: deeper)
+  static constexpr int kNV = 2;                      // V stages (released only after PV)
   static constexpr int kPB = 4;                      // pv_go / pv_done barrier ring (> kNV)
-  static constexpr int kNP = NQ == 64 ? FVSR_NP64 : 1;  // P^T buffers (per group: kNP / 2 for NQ=64)
+  static constexpr int kNP = NQ == 64 ? 4 : 1;       // P^T buffers
   static constexpr int kOB = 2;                      // O^T buffers per group (double-buffered units)
   static constexpr uint32_t kTileBytes = D * 128;    // one packed 64-row frame-tile
   static constexpr uint32_t kQSub = NQ * 128;        // Q sub-tile stride (NQ rows x 128 B)
   static constexpr uint32_t kQBytes = (D / 64) * kQSub;
   static constexpr uint32_t kKVBytes = 2 * kTileBytes;  // 128 rows
-  static constexpr uint32_t kPBytes = NQ * 256;      // 128 keys x NQ bf16 (also the O staging tile)
+  static constexpr uint32_t kPBytes = NQ * 256;      // 128 keys x NQ bf16
   static constexpr uint32_t kOffQ = 0;
   static constexpr uint32_t kOffK = kOffQ + kQBytes;
   static constexpr uint32_t kOffV = kOffK + kNK * kKVBytes;
@@ -167,10 +109,10 @@ struct AttnCfg {
   static constexpr uint32_t kScratch = NQ == 64 ? 13312 : 16384;
   // scratch layout (bytes): barriers 256 | c [2][2][128] f32 | alpha [2][128] | l [2][2][128] |
   // f [2][128] | red [2][CGg][4][CPT] | win [2][32] i32 | info [2][cap] | kn2 [2][cap] | qn2 [2] |
-  // c0 [2] | cmin [2][CGg][CPT/32] | unit [2][4] i32
+  // c0 [2] | cmin [2][CGg][CPT/32] | unit [2][8] i32 | prog [2] | kmax [4]
   static constexpr uint32_t kScratchUsed =
       256 + 4 * (512 + 256 + 512 + 256) + 4 * (2 * kCGg * 4 * kCPT) + 4 * 64 + 8 * 2 * 256 + 16 +
-      4 * (2 * kCGg * (kCPT / 32)) + 32 + 8 + 16;
+      4 * (2 * kCGg * (kCPT / 32)) + 64 + 8 + 16;
   static_assert(kScratchUsed <= kScratch, "scratch budget");
   static constexpr uint32_t kOffE = kOffS + kScratch;         // epilogue staging chunk
   static constexpr uint32_t kEpiBytes = 4096;
@@ -185,20 +127,6 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-
-// 2^x on the FMA/ALU pipes only (no MUFU, no conversion unit): round-to-nearest via the
-// 1.5*2^23 magic constant, q(f) ~ 2^f on [-0.5, 0.5] (degree-3 fit, max rel. error 1.6e-4,
-// far below the bf16 rounding of P), exponent added as an integer.  Valid for finite x; x is
-// clamped at -127 (result then ~1e-38, negligible), so it is only used on unmasked words.
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -127.0f);
-  const float j = xc + 12582912.0f;      // low mantissa bits = round(xc)
-  const float f = xc - (j - 12582912.0f);  // in [-0.5, 0.5]
-  float q = fmaf(0.0536014065f, f, 0.2423731536f);
-  q = fmaf(q, f, 0.6935025454f);
-  q = fmaf(q, f, 0.9999481440f);
-  return __int_as_float(__float_as_int(q) + (__float_as_int(j) << 23));
 }
 
 // Packed fp32 pairs (FMUL2 / FADD2 on sm_100): a * s and a += b on two lanes of a pair.
@@ -282,22 +210,8 @@ __device__ __forceinline__ void tmem_ld<64>(uint32_t taddr, uint32_t* r) {
 template <int N>
 __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t* r);
 template <>
-__device__ __forceinline__ void tmem_st<16>(uint32_t taddr, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
-}
-template <>
 __device__ __forceinline__ void tmem_st<32>(uint32_t taddr, const uint32_t* r) {
   tmem_st32(taddr, r);
-}
-template <>
-__device__ __forceinline__ void tmem_st<64>(uint32_t taddr, const uint32_t* r) {
-  tmem_st32(taddr, r);
-  tmem_st32(taddr + 32, r + 32);
 }
 
 // max of N values as a balanced tree (ILP instead of a serial chain)
@@ -313,13 +227,33 @@ __device__ __forceinline__ float tree_max(const float* v) {
   return t[0];
 }
 
-// Per-tile key geometry, packed: bits 0-1 key frames in the block (1|2), 2-7 first k-frame
-// index, 8-19 key tile row origin kh0, 20-31 key tile col origin kw0.
-__device__ __forceinline__ uint32_t tile_info(const DevGeom& g, int kb) {
-  const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
-  const int th = ktile / g.tiles_w, tw = ktile - th * g.tiles_w;
-  return (uint32_t)g.k_tr_count[ktr] | ((uint32_t)g.k_tr_first[ktr] << 2) | ((uint32_t)(8 * th) << 8) |
-         ((uint32_t)(8 * tw) << 20);
+// ---- key-tile descriptors -----------------------------------------------------------------
+// A half (64 key rows) is 16 bits: [15:11] k-frame index in the grid (31: empty half),
+// [10:6] tile row, [5:0] tile column.  A tile descriptor = half A | half B << 16.
+__device__ __forceinline__ uint32_t half16(const DevGeom& g, int kf, int kt) {
+  const int th = kt / g.tiles_w, tw = kt - th * g.tiles_w;
+  return ((uint32_t)kf << 11) | ((uint32_t)th << 6) | (uint32_t)tw;
+}
+__device__ __forceinline__ bool block_single(const DevGeom& g, int kb) { return g.k_tr_count[kb / g.n_tiles] == 1; }
+// one selected block on its own: A = its first frame, B = its partner frame or empty
+__device__ __forceinline__ uint32_t block_desc(const DevGeom& g, int kb) {
+  const int ktr = kb / g.n_tiles, kt = kb - ktr * g.n_tiles;
+  const int f0 = g.k_tr_first[ktr];
+  const uint32_t b = g.k_tr_count[ktr] == 2 ? half16(g, f0 + 1, kt) : kHalfNone;
+  return half16(g, f0, kt) | (b << 16);
+}
+// two single-frame blocks in one tile
+__device__ __forceinline__ uint32_t pair_desc(const DevGeom& g, int kb0, int kb1) {
+  const int r0 = kb0 / g.n_tiles, r1 = kb1 / g.n_tiles;
+  return half16(g, g.k_tr_first[r0], kb0 - r0 * g.n_tiles) |
+         (half16(g, g.k_tr_first[r1], kb1 - r1 * g.n_tiles) << 16);
+}
+__device__ __forceinline__ bool half_empty(uint32_t h) { return ((h >> 11) & 31u) == 31u; }
+// storage offset (in frame-tiles x kUnit) of a half's frame-tile
+template <uint32_t kUnit>
+__device__ __forceinline__ long long half_offset(const DevGeom& g, uint32_t h) {
+  const int kt = (int)((h >> 6) & 31u) * g.tiles_w + (int)(h & 63u);
+  return ((long long)g.k_slot[(h >> 11) & 31u] * g.n_tiles + kt) * kUnit;
 }
 
 // MK: token-mask kind (0 all-allowed, 1 locality window, 2 explicit bitmask), fixed at
@@ -347,7 +281,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   //   pv_go[G % PB]   V(G) landed (V producer expect_tx + TMA bytes) and P(G) written
   //   pv_done[G % PB] PV(G) complete (commit); frees V stage and P buffer
   //   o_full / o_empty  per unit: all PVs done / epilogue read O
-  //   tab_full[U & 1]  per-unit tables built (epilogue warpgroup, a unit ahead)
+  //   tab_full[U & 1]  per-unit tables built (epilogue warpgroup, a unit ahead); every role
+  //                    walks the units with work through these tables
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* qk_go = bars + 2;
@@ -356,7 +291,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   uint64_t* pv_done = pv_go + kPB;
   uint64_t* o_full = pv_done + kPB;
   uint64_t* o_empty = o_full + 2;
-  uint64_t* tab_full = o_empty + 2;   // per-unit tables built (producer)
+  uint64_t* tab_full = o_empty + 2;
   uint64_t* pv_iss = tab_full + 2;    // [4] PV(G) issued (PV issuer), paces the QK issuer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_iss + 4);
   float* c_s = reinterpret_cast<float*>(scratch + 256);  // [unit parity][group][128] column references
@@ -365,7 +300,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   float* f_s = l_s + 512;                                // [group][128] merge factors (incl. 1/l)
   float* red = f_s + 256;                                // [2][CGg][4][CPT] cross-quarter partials
   // Per-unit tables, double-buffered by unit parity and built a unit ahead by the epilogue warpgroup:
-  // locality windows [2][32], tile infos [2][kInfoCap], key-norm bounds [2][kInfoCap],
+  // locality windows [2][32], tile descriptors [2][kInfoCap], key-norm bounds [2][kInfoCap],
   // query-norm bound [2], initial reference [2]
   int* win2 = reinterpret_cast<int*>(red + 2 * Cfg::kCGg * 4 * CPT);
   uint32_t* info2 = reinterpret_cast<uint32_t*>(win2 + 64);
@@ -373,8 +308,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   float* qn2_2 = kn2_2 + 2 * kInfoCap;
   float* c0_2 = qn2_2 + 2;
   float* cmin_s = c0_2 + 2;                                         // [2][CGg][CPT/32] min reference
-  int* utab = reinterpret_cast<int*>(cmin_s + 2 * Cfg::kCGg * (CPT / 32));  // [2][4] n head qtr qtile
-  uint32_t* prog = reinterpret_cast<uint32_t*>(utab + 8);  // [0] QKs, [1] PVs known complete (count)
+  int* utab = reinterpret_cast<int*>(cmin_s + 2 * Cfg::kCGg * (CPT / 32));  // [2][8] tiles head qtr qtile nsel
+  uint32_t* prog = reinterpret_cast<uint32_t*>(utab + 16);  // [0] QKs, [1] PVs known complete (count)
   float* kmx = reinterpret_cast<float*>(prog + 2);          // [4] table builder's warp maxima
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -382,6 +317,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   // 13/14 (by unit parity) softmax end of unit -> epilogue
   constexpr int kStatBar0 = 13;
   constexpr int kStatCount = 128 + 32 * kGroups * Cfg::kCGg;
+  constexpr int kEpiBar = 12;
   const long long n_units = p.unit_end - p.unit_begin;
   const int units_per_head = p.n_trows * g.n_tiles;
 
@@ -400,9 +336,16 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     const int kb = sel[t];
     return kb < 0 ? 0 : (kb >= g.bnk ? g.bnk - 1 : kb);
   };
+  // descriptor of tile t of the unit in table slot sl (tables hold the first kInfoCap; a unit
+  // with more selected blocks than that runs them unpaired, one block per tile)
+  auto desc_at = [&](int sl, int t) -> uint32_t {
+    if (t < kInfoCap) return info2[sl * kInfoCap + t];
+    const int* sel =
+        p.sel + ((long long)utab[sl * 8 + 1] * g.bnq + utab[sl * 8 + 2] * g.n_tiles + utab[sl * 8 + 3]) * p.cap;
+    return block_desc(g, sel_at(sel, t));
+  };
 
   // ---- setup ----------------------------------------------------------------------------
-  if (threadIdx.x == 0) trace_cta(p, 0);
   if (warp == Cfg::kQkWarp) tmem_alloc(tmem_slot, Cfg::kTmemCols);
   if (threadIdx.x == 0) {
     prog[0] = 0;
@@ -414,7 +357,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     for (int i = 0; i < 2; ++i) { mbar_init(o_full + i, 1); mbar_init(o_empty + i, 4); }
     for (int i = 0; i < 2; ++i) mbar_init(tab_full + i, 1);
     for (int i = 0; i < 4; ++i) mbar_init(pv_iss + i, 1);
-
     fence_barrier_init();
   }
   tc_fence_before();
@@ -427,85 +369,97 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   // TMEM columns: S buffers [0, NS*NQ), then O^T buffers [group][unit parity]
   const uint32_t tS0 = tmem, tO0 = tmem + kNS * NQ;
 
-  // Per-lane metadata of tile (base + lane) of a unit's selection, fetched warp-wide once per
-  // 32 tiles and broadcast per tile with shuffles (no per-tile global round trip).
-  struct TileMeta {
-    int kcnt;
-    long long offA, offB;
-  };
-  auto fetch_meta = [&](const int* sel, int n, int base, int head) {
-    TileMeta mt{1, 0, 0};
-    const int t = base + lane;
-    if (t < n) {
-      if (sel[t] < 0 || sel[t] >= g.bnk) atomicOr(p.err, kErrInvariant);
-      const int kb = sel_at(sel, t);
-      const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
-      const int f0 = g.k_tr_first[ktr];
-      mt.kcnt = g.k_tr_count[ktr];
-      mt.offA = head * p.kv_head_stride + ((long long)g.k_slot[f0] * g.n_tiles + ktile) * Cfg::kTileBytes;
-      mt.offB = mt.kcnt == 2
-                    ? head * p.kv_head_stride + ((long long)g.k_slot[f0 + 1] * g.n_tiles + ktile) * Cfg::kTileBytes
-                    : mt.offA;
-    }
-    return mt;
-  };
-  auto bcast_meta = [&](const TileMeta& mt, int src) {
-    TileMeta r;
-    r.kcnt = __shfl_sync(0xffffffffu, mt.kcnt, src);
-    r.offA = (long long)__shfl_sync(0xffffffffu, (unsigned long long)mt.offA, src);
-    r.offB = (long long)__shfl_sync(0xffffffffu, (unsigned long long)mt.offB, src);
-    return r;
-  };
-  // K or V tile -> stage: frame A rows 0-63, frame B rows 64-127 of each 64-channel sub-tile
-  auto load_kv = [&](const uint8_t* base_ptr, uint8_t* dst, const TileMeta& mt, uint64_t* bar) {
-    mbar_arrive_expect_tx(bar, mt.kcnt * Cfg::kTileBytes);
+  // K or V tile -> stage: half A rows 0-63, half B rows 64-127 of each 64-channel sub-tile
+  auto load_kv = [&](const uint8_t* base_ptr, uint8_t* dst, uint32_t desc, long long head_off, uint64_t* bar) {
+    const uint32_t hb = desc >> 16;
+    const bool two = !half_empty(hb);
+    const uint8_t* a = base_ptr + head_off + half_offset<Cfg::kTileBytes>(g, desc & 0xffffu);
+    const uint8_t* b = base_ptr + head_off + (two ? half_offset<Cfg::kTileBytes>(g, hb) : 0);
+    mbar_arrive_expect_tx(bar, (two ? 2u : 1u) * Cfg::kTileBytes);
 #pragma unroll
     for (int s = 0; s < D / 64; ++s) {
-      bulk_g2s(dst + s * 16384, base_ptr + mt.offA + s * kSubBytes, kSubBytes, bar);
-      if (mt.kcnt == 2) bulk_g2s(dst + s * 16384 + kSubBytes, base_ptr + mt.offB + s * kSubBytes, kSubBytes, bar);
+      bulk_g2s(dst + s * 16384, a + s * kSubBytes, kSubBytes, bar);
+      if (two) bulk_g2s(dst + s * 16384 + kSubBytes, b + s * kSubBytes, kSubBytes, bar);
     }
   };
 
   // ================================ epilogue warpgroup ====================================
-  // Per unit (same order as every role): wait for both groups' references and denominators
-  // (named barrier 13 | 14) and all PVs (o_full), merge the groups' O^T accumulators,
-  // O = sum_g 2^(c_g - c) O_g / sum_g 2^(c_g - c) l_g, and store bf16 rows straight from
-  // registers (lane pairs swap one value so each lane writes a 2-channel word).  Runs beside
-  // the softmax warps, which move on to the next unit at once.
-  // Per-unit tables for the softmax warps (slot U & 1), built by the epilogue warpgroup a
-  // whole unit ahead: tile geometry, key-norm bounds, query-norm bound, initial reference,
-  // locality windows, and the unit descriptor (n < 0 ends the stream).
-  auto build_tables = [&](int sl, long long u, int n, int head, int qtr, int qtile, const int* sel) {
+  // Per-unit tables for every other role (slot U & 1), built a whole unit ahead: the tile
+  // list (single-frame blocks paired), key-norm bounds, query-norm bound, initial reference,
+  // locality windows, and the unit descriptor (tiles < 0 ends the stream).
+  auto build_tables = [&](int sl, int n, int head, int qtr, int qtile, const int* sel) {
     const int et = threadIdx.x - Cfg::kEpiWarp * 32;
-    constexpr int kEpiBar = 12;
     uint32_t* info = info2 + sl * kInfoCap;
     float* kn2_s = kn2_2 + sl * kInfoCap;
+    if (n <= kInfoCap) {
+      if (et < 32) {
+        // Pair runs of consecutive single-frame blocks: within a run, entries at even offsets
+        // take the next entry as their B half and entries at odd offsets emit nothing.  One
+        // warp, 32 entries per step: ballots give the run offsets, a prefix popcount the slot.
+        int out = 0, carry = 0;  // carry: parity of the run of singles crossing into this chunk
+        for (int base = 0; base < n; base += 32) {
+          const int i = base + lane;
+          const int kb = i < n ? sel_at(sel, i) : 0;
+          const bool single = i < n && block_single(g, kb);
+          const uint32_t sm = __ballot_sync(0xffffffffu, single);
+          const uint32_t below = (1u << lane) - 1u;
+          const uint32_t zeros = ~sm & below;
+          const int off = zeros ? lane - (31 - __clz(zeros)) - 1 : lane + carry;
+          const bool follower = single && (off & 1);
+          const bool emit = i < n && !follower;
+          const uint32_t em = __ballot_sync(0xffffffffu, emit);
+          if (emit) {
+            int kb1 = -1;
+            if (single && i + 1 < n) {
+              const int nb = sel_at(sel, i + 1);
+              if (block_single(g, nb)) kb1 = nb;
+            }
+            info[out + __popc(em & below)] = kb1 >= 0 ? pair_desc(g, kb, kb1) : block_desc(g, kb);
+          }
+          out += __popc(em);
+          carry = __shfl_sync(0xffffffffu, single ? off + 1 : 0, 31) & 1;
+        }
+        if (lane == 0) utab[sl * 8] = out;
+      }
+    } else {
+      for (int i = et; i < kInfoCap; i += 128) info[i] = block_desc(g, sel_at(sel, i));
+      if (et == 0) utab[sl * 8] = n;
+    }
+    if (MK == 1 && et >= 32 && et < 40) {
+      const int e = et - 32;
+      const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
+      int lo, hi;
+      locality_range(m.mode, qh0 + e, m.extent_h, g.rows, lo, hi);
+      win2[sl * 32 + e] = lo;
+      win2[sl * 32 + 8 + e] = hi;
+      locality_range(m.mode, qw0 + e, m.extent_w, g.cols, lo, hi);
+      win2[sl * 32 + 16 + e] = lo;
+      win2[sl * 32 + 24 + e] = hi;
+    }
+    named_bar_sync(kEpiBar, 128);
+    const int nt = utab[sl * 8];
     float kmax = 0.0f;
-    for (int i = et; i < min(n, kInfoCap); i += 128) {
-      const int kb = sel_at(sel, i);
-      info[i] = tile_info(g, kb);
+    uint32_t nfull = 0;
+    for (int i = et; i < min(nt, kInfoCap); i += 128) {
+      const uint32_t desc = info[i];
       float kn = INFINITY;
       if (p.kn2) {
-        const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles, kf = g.k_tr_first[ktr];
-        const float* kh = p.kn2 + head * p.kn2_head_stride + ktile;
-        kn = kh[(long long)g.k_slot[kf] * g.n_tiles];
-        if (g.k_tr_count[ktr] == 2) kn = fmaxf(kn, kh[(long long)g.k_slot[kf + 1] * g.n_tiles]);
+        const float* kh = p.kn2 + head * p.kn2_head_stride;
+        kn = kh[half_offset<1>(g, desc & 0xffffu)];
+        if (!half_empty(desc >> 16)) kn = fmaxf(kn, kh[half_offset<1>(g, desc >> 16)]);
       }
+      nfull += half_empty(desc >> 16) ? 0u : 1u;
       kn2_s[i] = kn;
       kmax = fmaxf(kmax, kn);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    if (lane == 0) kmx[warp & 3] = kmax;
-    if (MK == 1 && et < 8) {
-      const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
-      int lo, hi;
-      locality_range(m.mode, qh0 + et, m.extent_h, g.rows, lo, hi);
-      win2[sl * 32 + et] = lo;
-      win2[sl * 32 + 8 + et] = hi;
-      locality_range(m.mode, qw0 + et, m.extent_w, g.cols, lo, hi);
-      win2[sl * 32 + 16 + et] = lo;
-      win2[sl * 32 + 24 + et] = hi;
+    for (int o = 16; o > 0; o >>= 1) {
+      kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+      nfull += __shfl_xor_sync(0xffffffffu, nfull, o);
+    }
+    if (lane == 0) {
+      kmx[warp & 3] = kmax;
+      if (p.tiles && nfull) atomicAdd(p.tiles + 1, (unsigned long long)nfull);
     }
     named_bar_sync(kEpiBar, 128);
     if (et == 0) {
@@ -522,13 +476,14 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       // barrier-free fast path and no first tile needs an exact column max.  Otherwise the
       // references start at -inf (exact lazy-rescale path).
       const float b2 = qn * kmax * (p.scale_log2 * p.scale_log2) * 1.0002f;
-      const bool fixed = FVSR_FIXED_REF && n <= kInfoCap && b2 <= kFixedBound * kFixedBound;
-      utab[sl * 4 + 0] = n;
-      utab[sl * 4 + 1] = head;
-      utab[sl * 4 + 2] = qtr;
-      utab[sl * 4 + 3] = qtile;
+      const bool fixed = n <= kInfoCap && b2 <= kFixedBound * kFixedBound;
+      if (p.tiles) atomicAdd(p.tiles, (unsigned long long)nt);
+      utab[sl * 8 + 1] = head;
+      utab[sl * 8 + 2] = qtr;
+      utab[sl * 8 + 3] = qtile;
+      utab[sl * 8 + 4] = n;
       qn2_2[sl] = qn;
-      c0_2[sl] = ((kInstrument && (p.debug & 1)) || fixed) ? 0.0f : -INFINITY;
+      c0_2[sl] = fixed ? 0.0f : -INFINITY;
       mbar_arrive(tab_full + sl);
     }
   };
@@ -548,20 +503,32 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     const int* sel;
     k = k < 0 ? -1 : next_work(k, u, head, qtr, qtile, n, sel);
     if (k >= 0) {
-      build_tables(sl, u, n, head, qtr, qtile, sel);
+      build_tables(sl, n, head, qtr, qtile, sel);
       ++k;
     } else if (threadIdx.x == Cfg::kEpiWarp * 32) {
-      utab[sl * 4] = -1;
+      utab[sl * 8] = -1;
       mbar_arrive(tab_full + sl);
     }
   };
+  // the unit in table slot U & 1 (every role but the epilogue walks the units with work this way)
+  struct UnitTab {
+    int nt, head, qtr, qtile;
+  };
+  auto wait_unit = [&](int U) {
+    const int sl = U & 1;
+    mbar_wait(tab_full + sl, (uint32_t)(U >> 1) & 1);
+    return UnitTab{utab[sl * 8], utab[sl * 8 + 1], utab[sl * 8 + 2], utab[sl * 8 + 3]};
+  };
 
+  // Per unit (same order as every role): wait for both groups' references and denominators
+  // (named barrier 13 | 14) and all PVs (o_full), merge the groups' O^T accumulators,
+  // O = sum_g 2^(c_g - c) O_g / sum_g 2^(c_g - c) l_g, stage bf16 rows and bulk-store them.
+  // Runs beside the softmax warps, which move on to the next unit at once.
   auto epilogue_warps = [&]() {
     const int q4 = warp & 3;                   // TMEM lane quarter = channel rows 32*q4..
     const int et = threadIdx.x - Cfg::kEpiWarp * 32;
     const int dj = q4 * 32 + lane;             // output channel of this lane
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    constexpr int kEpiBar = 12;
     constexpr int kEC = Cfg::kEpiCols;
     uint16_t* stage = reinterpret_cast<uint16_t*>(smem + Cfg::kOffE);  // [kEC][D] bf16
     int kb = 0;  // item index from which the next table is searched (-1: stream ended)
@@ -593,7 +560,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       // warp costs no issue slots (ids alternate by unit parity: the softmax cannot run two
       // units ahead, it needs the tables this epilogue releases)
       named_bar_sync(kStatBar0 + par, kStatCount);
-      if (et == 0) trace_at(p, 30, U);
       // merge factors per query column: f_g = 2^(c_g - c) / l, l = sum_g l_g 2^(c_g - c);
       // zero for columns outside [row_begin, row_end) (their rows are written as zeros)
       if (et < NQ) {
@@ -619,24 +585,18 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       }
       mbar_wait_sleep(o_full + par, (uint32_t)(U >> 1) & 1, 128);
       tc_fence_after();
-      if (et == 0) trace_at(p, 31, U);
       named_bar_sync(kEpiBar, 128);  // factors visible
       // O in chunks of kEC query columns: TMEM -> merged bf16 -> staging -> bulk store
 #pragma unroll 1
-      for (int c0 = 0; c0 < ((kExp & 32) ? 0 : NQ); c0 += kEC) {
+      for (int c0 = 0; c0 < NQ; c0 += kEC) {
         float acc[kEC];
 #pragma unroll
         for (int i = 0; i < kEC; ++i) acc[i] = 0.0f;
 #pragma unroll
         for (int gi = 0; gi < kGroups; ++gi) {
           uint32_t o[kEC];
-          if (kExp & 64) {
-#pragma unroll
-            for (int i = 0; i < kEC; ++i) o[i] = 0x3f800000u;
-          } else {
-            tmem_ld<kEC>(tO0 + (gi * kOB + par) * NQ + c0 + lane_off, o);
-            tc_wait_ld();
-          }
+          tmem_ld<kEC>(tO0 + (gi * kOB + par) * NQ + c0 + lane_off, o);
+          tc_wait_ld();
           const float* fg = f_s + gi * 128 + c0;
 #pragma unroll
           for (int i = 0; i < kEC; i += 4) {
@@ -649,14 +609,14 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           }
         }
         if (et == 0) bulk_wait_read();  // the previous chunk's stores have read the staging
-        if (!(kExp & 512)) named_bar_sync(kEpiBar, 128);
-        if (dj < D && !(kExp & 256)) {
+        named_bar_sync(kEpiBar, 128);
+        if (dj < D) {
 #pragma unroll
           for (int i = 0; i < kEC; ++i) stage[i * D + dj] = __bfloat16_as_ushort(__float2bfloat16_rn(acc[i]));
         }
-        if (!(kExp & 256)) fence_proxy_async_smem();
-        if (!(kExp & 512)) named_bar_sync(kEpiBar, 128);
-        if (et == 0 && !(kExp & 128)) {
+        fence_proxy_async_smem();
+        named_bar_sync(kEpiBar, 128);
+        if (et == 0) {
           if (p.out_tile_major) {
             bulk_s2g(p.out + (u * NQ + c0) * D, stage, kEC * D * 2);
           } else {
@@ -675,11 +635,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty + par);   // O^T buffers of this parity free for unit U + 2
-      // slot par (tables, c, l) is free: the softmax finished unit U; build unit U + 2's tables
+      // slot par (tables, c, l) is free: every role finished unit U; build unit U + 2's tables
       named_bar_sync(kEpiBar, 128);
       build_next(par, kb);
-      if (et == 0) trace_at(p, 32, U);
-      if (et == 0) trace_cta(p, 1 + U);
       ++U;
     }
     if (et == 0) bulk_wait_all();
@@ -690,29 +648,15 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   if (warp == Cfg::kProducerWarp) {
     // ================================ Q / K producer (warp-wide) =========================
     int T = 0;  // tiles of this CTA so far
-    int U = 0;  // units with work
-    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int head, qtr, qtile, n;
-      const int* sel;
-      decode(u, head, qtr, qtile, n, sel);
-      if (n == 0) continue;
-      // the next unit's Q into L2 now: its load below waits for this unit's last QK and
-      // would otherwise pay the full HBM latency between units
-      if (lane < 2 && u + gridDim.x < n_units) {
-        int nh, ntr, ntile, nn;
-        const int* nsel;
-        decode(u + gridDim.x, nh, ntr, ntile, nn, nsel);
-        if (lane < g.q_tr_count[ntr])
-          bulk_prefetch_l2(p.q + nh * p.q_head_stride +
-                               ((long long)(g.q_tr_first[ntr] + lane) * g.n_tiles + ntile) * Cfg::kTileBytes,
-                           Cfg::kTileBytes);
-      }
+    for (int U = 0;; ++U) {
+      const UnitTab ut = wait_unit(U);
+      if (ut.nt < 0) break;
+      const int sl = U & 1;
       if (U >= 1) mbar_wait(q_empty, (U - 1) & 1);
       if (elect_one()) {
-        trace_at(p, 35, U);
         mbar_arrive_expect_tx(q_full, Cfg::kQBytes);
-        const int f0 = g.q_tr_first[qtr];
-        const uint8_t* qa = p.q + head * p.q_head_stride + ((long long)f0 * g.n_tiles + qtile) * Cfg::kTileBytes;
+        const int f0 = g.q_tr_first[ut.qtr];
+        const uint8_t* qa = p.q + ut.head * p.q_head_stride + ((long long)f0 * g.n_tiles + ut.qtile) * Cfg::kTileBytes;
 #pragma unroll
         for (int s = 0; s < D / 64; ++s) {
           bulk_g2s(sQ + s * Cfg::kQSub, qa + s * kSubBytes, kSubBytes, q_full);
@@ -722,149 +666,122 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         }
       }
       __syncwarp();
-      TileMeta mine{};
-      for (int t = 0; t < n; ++t, ++T) {
-        if ((t & 31) == 0) mine = fetch_meta(sel, n, t, head);
-        const TileMeta mt = bcast_meta(mine, t & 31);
+      // the next unit's Q into L2 now if its table is built: its load waits for this unit's
+      // last QK and would otherwise pay the full HBM latency between units
+      {
+        const int nsl = sl ^ 1;
+        if (lane < 2 && mbar_test(tab_full + nsl, (uint32_t)((U + 1) >> 1) & 1) && utab[nsl * 8] > 0) {
+          const int nqtr = utab[nsl * 8 + 2];
+          if (lane < g.q_tr_count[nqtr])
+            bulk_prefetch_l2(p.q + utab[nsl * 8 + 1] * p.q_head_stride +
+                                 ((long long)(g.q_tr_first[nqtr] + lane) * g.n_tiles + utab[nsl * 8 + 3]) *
+                                     Cfg::kTileBytes,
+                             Cfg::kTileBytes);
+        }
+      }
+      const long long hoff = ut.head * p.kv_head_stride;
+      for (int t = 0; t < ut.nt; ++t, ++T) {
+        const uint32_t desc = desc_at(sl, t);
         const int ks = T % kNK;
         // K stage ks is free once QK(T - NK) completed
         if (T >= kNK) {
           mbar_wait(s_full + (T - kNK) % kNS, (uint32_t)((T - kNK) / kNS) & 1);
           if (lane == 0) st_release_shared(prog + 0, (uint32_t)(T - kNK + 1));  // QKs complete
         }
-        if (elect_one()) {
-          if (((kInstrument && (p.debug & 2)) || (kExp & 16)) && T >= kNK) {  // experiment: no K traffic after the first stages
-            mbar_arrive(qk_go + T % kNS);
-          } else {
-            trace_at(p, 0, T);
-            load_kv(p.k, sK + ks * Cfg::kKVBytes, mt, qk_go + T % kNS);
-          }
-        }
+        if (elect_one()) load_kv(p.k, sK + ks * Cfg::kKVBytes, desc, hoff, qk_go + T % kNS);
         __syncwarp();
       }
-      ++U;
     }
   } else if (warp == Cfg::kVProducerWarp) {
     // ================================ V producer (warp-wide) =============================
     int T = 0;
-    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int head, qtr, qtile, n;
-      const int* sel;
-      decode(u, head, qtr, qtile, n, sel);
-      TileMeta mine{};
-      for (int t = 0; t < n; ++t, ++T) {
-        if ((t & 31) == 0) mine = fetch_meta(sel, n, t, head);
-        const TileMeta mt = bcast_meta(mine, t & 31);
+    for (int U = 0;; ++U) {
+      const UnitTab ut = wait_unit(U);
+      if (ut.nt < 0) break;
+      const long long hoff = ut.head * p.kv_head_stride;
+      for (int t = 0; t < ut.nt; ++t, ++T) {
+        const uint32_t desc = desc_at(U & 1, t);
         const int vs = T % kNV;
         // V stage vs is free once PV(T - NV) completed
         if (T >= kNV) {
           mbar_wait(pv_done + (T - kNV) % kPB, (uint32_t)((T - kNV) / kPB) & 1);
           if (lane == 0) st_release_shared(prog + 1, (uint32_t)(T - kNV + 1));  // PVs complete
         }
-        if (elect_one()) {
-          if (((kInstrument && (p.debug & 2)) || (kExp & 16)) && T >= kNV) {
-            mbar_arrive(pv_go + T % kPB);
-          } else {
-            trace_at(p, 5, T);
-            load_kv(p.v, sV + vs * Cfg::kKVBytes, mt, pv_go + T % kPB);
-          }
-        }
+        if (elect_one()) load_kv(p.v, sV + vs * Cfg::kKVBytes, desc, hoff, pv_go + T % kPB);
         __syncwarp();
       }
     }
   } else if (warp == Cfg::kQkWarp) {
     // ================================ QK^T issuer (warp-wide, elected lane issues) =========
     // S^T(G) = K(G) . Q^T into S buffer G % NS once K(G) landed and the buffer is free
-    // (qk_go); runs ahead of the softmax by up to NS tiles, independent of PV progress.
+    // (qk_go); runs ahead of the softmax by up to NS tiles, paced by PV issue (kQkLead).
     constexpr uint32_t idesc_qk = umma_idesc_bf16(128, NQ, 0, 0);
     const uint32_t aQ = smem_u32(sQ);
     const uint32_t aK0 = smem_u32(sK);
-    int G = 0, U = 0, sb = 0, ks = 0;
+    int G = 0, sb = 0, ks = 0;
     uint32_t sph = 0;
-    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int head, qtr, qtile, n;
-      const int* sel;
-      decode(u, head, qtr, qtile, n, sel);
-      if (n == 0) continue;
+    for (int U = 0;; ++U) {
+      const UnitTab ut = wait_unit(U);
+      if (ut.nt < 0) break;
       mbar_wait(q_full, U & 1);
-      for (int t = 0; t < n; ++t, ++G) {
-        if (lane == 0) trace_at(p, 18, G);
-        if (kQkLead > 0 && G >= kQkLead) mbar_wait(pv_iss + (G - kQkLead) % 4, (uint32_t)((G - kQkLead) / 4) & 1);
-        if (lane == 0) trace_at(p, 7, G);
+      for (int t = 0; t < ut.nt; ++t, ++G) {
+        if (G >= kQkLead) mbar_wait(pv_iss + (G - kQkLead) % 4, (uint32_t)((G - kQkLead) / 4) & 1);
         mbar_wait(qk_go + sb, sph);
-        if (lane == 0) trace_at(p, 19, G);
         tc_fence_after();
         const uint32_t aK = aK0 + ks * Cfg::kKVBytes;
         if (elect_one()) {
-          trace_at(p, 1, G);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint64_t da = umma_desc_sw128(aK + (kk >> 2) * 16384 + (kk & 3) * 32, 16u, 1024u);
             const uint64_t db = umma_desc_sw128(aQ + (kk >> 2) * Cfg::kQSub + (kk & 3) * 32, 16u, 1024u);
             tc_mma_f16(tS0 + sb * NQ, da, db, idesc_qk, kk > 0 ? 1u : 0u);
           }
-          trace_at(p, 12, G);
           tc_commit(s_full + sb);
-          if (t == n - 1) tc_commit(q_empty);
-          trace_at(p, 13, G);
+          if (t == ut.nt - 1) tc_commit(q_empty);
         }
         __syncwarp();
         if (++sb == kNS) { sb = 0; sph ^= 1u; }
         if (++ks == kNK) ks = 0;
       }
-      ++U;
     }
   } else if (warp == Cfg::kPvWarp) {
     // ================================ PV issuer (warp-wide, elected lane issues) ==========
-    // O^T[group(G)] += V(G)^T . P(G)^T once V(G) landed and the softmax wrote P(G) (pv_go).
+    // O^T[group(t)] += V(G)^T . P(G)^T once V(G) landed and the softmax wrote P(G) (pv_go).
     constexpr uint32_t idesc_pv = umma_idesc_bf16(128, NQ, 1, 1);
     const uint32_t aV0 = smem_u32(sV), aP0 = smem_u32(sP);
-    int G = 0, U = 0, vs = 0, pb = 0, gb = 0;
+    int G = 0, vs = 0, pb = 0, gb = 0;
     uint32_t gph = 0;
-    for (long long u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int head, qtr, qtile, n;
-      const int* sel;
-      decode(u, head, qtr, qtile, n, sel);
-      if (n == 0) continue;
+    for (int U = 0;; ++U) {
+      const UnitTab ut = wait_unit(U);
+      if (ut.nt < 0) break;
       const int ob = U & 1;
       if (U >= 2) mbar_wait(o_empty + ob, ((U >> 1) - 1) & 1);  // epilogue of unit U-2 done
-      uint32_t fullmask = 0;  // bit i: tile (chunk base + i) is a 128-row block
-      for (int t = 0; t < n; ++t, ++G) {
-        if ((t & 31) == 0) {
-          const int tt = t + lane;
-          fullmask = __ballot_sync(0xffffffffu, tt < n && g.k_tr_count[sel_at(sel, tt) / g.n_tiles] == 2);
-        }
-        const bool full = ((fullmask >> (t & 31)) & 1u) != 0u;
+      for (int t = 0; t < ut.nt; ++t, ++G) {
+        const bool full = !half_empty(desc_at(U & 1, t) >> 16);  // 128 key rows (else rows 0-63)
         const uint32_t tO = tO0 + ((t % kGroups) * kOB + ob) * NQ;
-        if (lane == 0) trace_at(p, 16, G);
         mbar_wait(pv_go + gb, gph);
-        if (lane == 0) trace_at(p, 17, G);
         tc_fence_after();
         const uint32_t aV = aV0 + vs * Cfg::kKVBytes;
         const uint32_t aP = aP0 + pb * Cfg::kPBytes;
         if (elect_one()) {
-          trace_at(p, 4, G);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            if (kk < 4 || full) {  // a 64-row key block has 4 valid K=16 steps
+            if (kk < 4 || full) {  // a 64-row tile has 4 valid K=16 steps
               const uint64_t da = umma_desc_sw128(aV + kk * 2048, D == 128 ? 16384u : 0u, 1024u);
               const uint64_t db = umma_desc_sw128(aP + kk * 2048, 16384u, 1024u);
               // the first tile of each group in the unit overwrites its O^T buffer
               tc_mma_f16(tO, da, db, idesc_pv, (t >= kGroups || kk > 0) ? 1u : 0u);
             }
           }
-          trace_at(p, 14, G);
           tc_commit(pv_done + gb);
-          if (t == n - 1) tc_commit(o_full + ob);
-          if (kQkLead > 0) mbar_arrive(pv_iss + G % 4);
-          trace_at(p, 15, G);
+          if (t == ut.nt - 1) tc_commit(o_full + ob);
+          mbar_arrive(pv_iss + G % 4);
         }
         __syncwarp();
         if (++gb == kPB) { gb = 0; gph ^= 1u; }
         if (++vs == kNV) vs = 0;
         if (++pb == kNP) pb = 0;
       }
-      ++U;
     }
   } else {
     epilogue_warps();
@@ -872,8 +789,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
   } else {
     reg_alloc<Cfg::kRegSoftmax>();
     // ===================================== softmax warps ================================
-    // Group grp handles the tiles G with G % kGroups == grp (ping-pong: the two groups'
-    // latencies overlap) with its own running references and O^T accumulator.
+    // Group grp handles the tiles t of a unit with t % kGroups == grp (ping-pong: the two
+    // groups' latencies overlap) with its own running references and O^T accumulator.
     const int grp = warp / WG, wl = warp % WG;
     const int quarter = warp & 3, cg = wl >> 2;
     const int j = quarter * 32 + lane;  // key row == TMEM lane
@@ -887,28 +804,24 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     if (lane == 0)
       for (int i = grp; i < kNS; i += kGroups) mbar_arrive(qk_go + i);  // S buffers start free
     int T = 0;
-    // Units with work, in the producer's order, from its per-unit tables (slot U & 1); an
-    // entry with n < 0 ends the stream.  Empty units are the epilogue warps' alone.
+    // Units with work, from the per-unit tables (slot U & 1); an entry with tiles < 0 ends the
+    // stream.  Empty units are the epilogue warps' alone.
     for (int U = 0;; ++U) {
       const int tsl = U & 1;
-      if (threadIdx.x == 0) trace_at(p, 33, U);
-      mbar_wait(tab_full + tsl, (uint32_t)(U >> 1) & 1);
-      if (threadIdx.x == 0) trace_at(p, 34, U);
-      const int n = utab[tsl * 4];
+      const UnitTab ut = wait_unit(U);
+      const int n = ut.nt;
       if (n < 0) break;
-      const int head = utab[tsl * 4 + 1], qtr = utab[tsl * 4 + 2], qtile = utab[tsl * 4 + 3];
-      const int* sel = p.sel + ((long long)head * g.bnq + qtr * g.n_tiles + qtile) * p.cap;
+      const int qtr = ut.qtr, qtile = ut.qtile;
       const int qf0 = g.q_tr_first[qtr];
       const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
-      const uint32_t* info = info2 + tsl * kInfoCap;
       const float* kn2_s = kn2_2 + tsl * kInfoCap;
       const float* qn2_s = qn2_2 + tsl;
       const int* win = win2 + tsl * 32;
       // this group's references (and their word minima) start at the unit's initial value;
       // the epilogue of unit U - 2 (same slot) released them with the tables
       float* cg_c = c_s + (tsl * 2 + grp) * 128;
-      // references 0 for the whole unit (every tile of it then fits the bound: see the producer)
-      const bool fixed_unit = c0_2[tsl] == 0.0f && !(kInstrument && (p.debug & 1)) && !(kExp & 4);
+      // references 0 for the whole unit (every tile of it then fits the bound)
+      const bool fixed_unit = c0_2[tsl] == 0.0f;
       {
         const float c0v = c0_2[tsl];
         for (int i = wl * 32 + lane; i < NQ; i += WG * 32) cg_c[i] = c0v;
@@ -936,8 +849,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       const int t_first = grp;
       bool any = false;  // this group processed a tile of the unit (its O^T is defined)
 
-      auto info_at = [&](int tt) { return tt < kInfoCap ? info[tt] : tile_info(g, sel_at(sel, tt)); };
-      uint32_t inf_next = t_first < n ? info_at(t_first) : 0u;  // prefetched a tile ahead
+      uint32_t inf_next = t_first < n ? desc_at(tsl, t_first) : 0u;  // prefetched a tile ahead
       // The tile loop, compiled twice: for fixed-reference units (references 0, every tile on
       // the fast path: no vote, no rescale, no reference loads -- a compact hot loop) and for
       // the general case.
@@ -948,28 +860,29 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           const int sb = G % kNS, pb = G % kNP;
           // ---- key row j: validity and allowed-query mask over this thread's columns ----
           const uint32_t inf = inf_next;
-          if (t + kGroups < n) inf_next = info_at(t + kGroups);
-          const int kcnt = inf & 3, kf0 = (inf >> 2) & 63;
-          const int kh = (int)((inf >> 8) & 0xfff) + ((j & 63) >> 3);
-          const int kw = (int)(inf >> 20) + (j & 7);
-          const bool kvalid = (j < 64 || kcnt == 2) && kh < g.rows && kw < g.cols;
+          if (t + kGroups < n) inf_next = desc_at(tsl, t + kGroups);
+          const uint32_t hd = j < 64 ? (inf & 0xffffu) : (inf >> 16);  // warp-uniform half
+          const int kf = (int)((hd >> 11) & 31u);
+          const int kh = (int)((hd >> 6) & 31u) * 8 + ((j & 63) >> 3);
+          const int kw = (int)(hd & 63u) * 8 + (j & 7);
+          const bool kvalid = kf != 31 && kh < g.rows && kw < g.cols;
           uint32_t mk[kW];  // bit i of word w: (key j, column col0 + 32w + i) allowed
-  #pragma unroll
+#pragma unroll
           for (int w = 0; w < kW; ++w) mk[w] = 0;
           if (kvalid) {
             if (MK == 0) {
-  #pragma unroll
+#pragma unroll
               for (int w = 0; w < kW; ++w) mk[w] = qvalid[w];
             } else if (MK == 1) {
               uint32_t wb = 0, hb = 0;  // allowed query cols / rows of the 8x8 query tile
-  #pragma unroll
+#pragma unroll
               for (int i = 0; i < 8; ++i) {
                 wb |= (kw >= win[16 + i] && kw < win[24 + i]) ? (1u << i) : 0u;
                 hb |= (kh >= win[i] && kh < win[8 + i]) ? (1u << i) : 0u;
               }
-  #pragma unroll
+#pragma unroll
               for (int w = 0; w < kW; ++w) {
-  #pragma unroll
+#pragma unroll
                 for (int i = 0; i < 32; ++i) {
                   const int qc = (col0 + 32 * w + i) & 63;
                   if (((hb >> (qc >> 3)) & (wb >> (qc & 7)) & 1u) != 0u) mk[w] |= 1u << i;
@@ -977,10 +890,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
                 mk[w] &= qvalid[w];
               }
             } else {
-              const long long tk = g.k_frame_tok0[kf0 + (j >> 6)] + (long long)kh * g.cols + kw;
-  #pragma unroll
+              const long long tk = g.k_frame_tok0[kf] + (long long)kh * g.cols + kw;
+#pragma unroll
               for (int w = 0; w < kW; ++w) {
-  #pragma unroll 4
+#pragma unroll 4
                 for (int i = 0; i < 32; ++i) {
                   if (!((qvalid[w] >> i) & 1u)) continue;
                   const int col = col0 + 32 * w + i, qc = col & 63;
@@ -991,7 +904,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
               }
             }
           }
-  #pragma unroll
+#pragma unroll
           for (int w = 0; w < kW; ++w) my_pairs += __popc(mk[w]);
           any = true;
 
@@ -1003,10 +916,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           // memory-clobbering asm between the words, so their loads and math interleave.  The
           // decision uses only shared inputs: all 4 warps of a column group take the same path.
           // (Fixed-reference units: always.)
-          bool fast = kFixed || (!(kExp & 4) && !(kInstrument && (p.debug & 1)) && t < kInfoCap);
+          bool fast = kFixed || t < kInfoCap;
           if (!kFixed && fast) {
             const float b2 = qn2_s[0] * kn2_s[t] * (sl2 * sl2) * 1.0002f;
-  #pragma unroll
+#pragma unroll
             for (int w = 0; w < kW; ++w) {
               const float lim = kBoundSlack + cmin_s[(grp * Cfg::kCGg + cg) * kW + w];
               fast = fast && lim > 0.0f && b2 <= lim * lim;
@@ -1014,10 +927,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           }
           // S(G) ready: the Q/K producer publishes the QKs it saw complete (it waits on them to
           // recycle K stages, normally well before this tile), else wait on the barrier itself
-          if (threadIdx.x == 0) trace_at(p, 6, G);
           if (ld_acquire_shared(prog + 0) <= (uint32_t)G) mbar_wait(s_full + sb, (uint32_t)(G / kNS) & 1);
           tc_fence_after();
-          if (threadIdx.x == 0) trace_at(p, 2, G);
           if (fast) {
             // P buffer pb was last read by PV(G - NP) (kNP tiles back: normally long done, and
             // published by the V producer, which waits on PVs to recycle V stages), so each
@@ -1028,53 +939,43 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
             if constexpr (kEarlyP) {
               if (G >= kNP && ld_acquire_shared(prog + 1) <= (uint32_t)(G - kNP))
                 mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
-              if (threadIdx.x == 0) trace_at(p, 9, G);
             }
             uint32_t pk[CPT / 2];
-  #pragma unroll
+#pragma unroll
             for (int w = 0; w < kW; ++w) {
               const uint32_t mw = mk[w];
               const float* cw = cg_c + col0 + 32 * w;
               float d[32];
-              if (kExp & 2) {
-  #pragma unroll
-                for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
-              } else {
-                tmem_ld<32>(tS0 + sb * NQ + col0 + 32 * w + lane_off, reinterpret_cast<uint32_t*>(d));
-                tc_wait_ld();
-              }
-              if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
+              tmem_ld<32>(tS0 + sb * NQ + col0 + 32 * w + lane_off, reinterpret_cast<uint32_t*>(d));
+              tc_wait_ld();
               if (mw == 0u) {
-  #pragma unroll
+#pragma unroll
                 for (int i = 0; i < 16; ++i) pk[16 * w + i] = 0u;
               } else {
                 if (kFixed && mw == 0xffffffffu) {
                   // references fixed at 0, every key allowed: d = s * scale * log2(e)
-  #pragma unroll
+#pragma unroll
                   for (int i = 0; i < 16; ++i) fmul2(d[2 * i], d[2 * i + 1], sl2);
                 } else {
-  #pragma unroll
+#pragma unroll
                   for (int i = 0; i < 32; i += 4) {
                     const float4 c4 = kFixed ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                                 : *reinterpret_cast<const float4*>(cw + i);
+                                             : *reinterpret_cast<const float4*>(cw + i);
                     d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
                     d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
                     d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
                     d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
                   }
                 }
-  #pragma unroll
+#pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                  // kPolyN of every 8 pairs of an unmasked word on the FMA pipe (MUFU relief)
-                  const bool poly = (i & 7) < kPolyN && mw == 0xffffffffu;
-                  const float p0 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i]) : ex2(d[2 * i]));
-                  const float p1 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i + 1]) : ex2(d[2 * i + 1]));
+                  const float p0 = ex2(d[2 * i]);
+                  const float p1 = ex2(d[2 * i + 1]);
                   fadd2(lp[32 * w + 2 * i], lp[32 * w + 2 * i + 1], p0, p1);
                   const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                   pk[16 * w + i] = *reinterpret_cast<const uint32_t*>(&h2);
                 }
               }
-              if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
               if constexpr (kEarlyP) {
                 const int cwi = col0 + 32 * w;
                 uint8_t* pw = prow + (cwi >> 6) * 16384;
@@ -1089,7 +990,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
             if constexpr (!kEarlyP) {
               if (G >= kNP && ld_acquire_shared(prog + 1) <= (uint32_t)(G - kNP))
                 mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
-              if (threadIdx.x == 0) trace_at(p, 9, G);
 #pragma unroll
               for (int w = 0; w < kW; ++w) {
                 const int cwi = col0 + 32 * w;
@@ -1105,151 +1005,123 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           } else {
             // Columns in 32-wide words: each word is loaded, exponentiated and stored on its own
             // (32 live scores per thread); its columns have their own references and vote.
-    #pragma unroll
+#pragma unroll
             for (int w = 0; w < kW; ++w) {
               const int cw = col0 + 32 * w;                // first column of the word
               const uint32_t tS = tS0 + sb * NQ + cw + lane_off;
               float d[32];  // scores -> exponents -> probabilities
-              if (kExp & 2) {
-    #pragma unroll
-                for (int i = 0; i < 32; ++i) d[i] = 0.25f * (i & 3);
+              tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+              tc_wait_ld();
+              uint32_t pk[16];
+              // d = s*scale*log2(e) - c (one FFMA; c = -inf before a column's first key gives
+              // +inf, which forces the exact path); masked entries -> -inf (ex2 -> 0).  The mask
+              // word is warp-uniform except on ragged edge tiles: all-allowed / none / mixed.
+              const uint32_t mw = mk[w];
+              if (mw == 0xffffffffu) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
+                  d[i] = fmaf(d[i], sl2, -c4.x);
+                  d[i + 1] = fmaf(d[i + 1], sl2, -c4.y);
+                  d[i + 2] = fmaf(d[i + 2], sl2, -c4.z);
+                  d[i + 3] = fmaf(d[i + 3], sl2, -c4.w);
+                }
+              } else if (mw == 0u) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) d[i] = -INFINITY;
               } else {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
+                  d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
+                  d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
+                  d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
+                  d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
+                }
+              }
+              const bool need = bar_red_or(bar_id, 128, mw != 0u && tree_max<32>(d) > kRescaleThreshold);
+              if (need) {
+                // exact column max of this tile over the group's 128 key rows, from the raw scores
                 tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
                 tc_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) d[i] = ((mk[w] >> i) & 1u) ? d[i] * sl2 : -INFINITY;
+                warp_colreduce<32, true>(d, lane);
+                cg_red[quarter * 32 + lane] = d[0];
+                named_bar_sync(bar_id, 128);
+                if (quarter == 0) {
+                  const float mx = fmaxf(fmaxf(cg_red[lane], cg_red[32 + lane]), fmaxf(cg_red[64 + lane], cg_red[96 + lane]));
+                  const float cold = cg_c[cw + lane];
+                  const float nw = fmaxf(cold, mx);
+                  cg_c[cw + lane] = nw;
+                  cg_a[cw + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
+                  float mn = nw;
+#pragma unroll
+                  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                  if (lane == 0) cmin_s[(grp * Cfg::kCGg + cg) * kW + w] = mn;
+                }
+                named_bar_sync(bar_id, 128);
+                tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
+                tc_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  lp[32 * w + i] *= cg_a[cw + i];
+                  d[i] = ((mk[w] >> i) & 1u) ? fmaf(d[i], sl2, -cg_c[cw + i]) : -INFINITY;
+                }
+                if (t >= kGroups) {
+                  // O^T holds this group's PVs of the unit: wait for its last one, rescale columns
+                  const int Gp = G - kGroups;
+                  mbar_wait(pv_done + Gp % kPB, (uint32_t)(Gp / kPB) & 1);
+                  tc_fence_after();
+                  if (j < D) {
+                    uint32_t o[32];
+                    tmem_ld<32>(tO + cw + lane_off, o);
+                    tc_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * cg_a[cw + i]);
+                    tmem_st<32>(tO + cw + lane_off, o);
+                    tc_wait_st();
+                  }
+                }
               }
-              if (threadIdx.x == 0) trace_at(p, 20 + 4 * w, G);
-              uint32_t pk[16];
-              if (kInstrument && (p.debug & 1)) {  // experiment: no softmax math
-    #pragma unroll
-                for (int i = 0; i < 16; ++i) pk[i] = 0x3f803f80u;  // bf16 pair (1, 1)
-    #pragma unroll
-                for (int i = 0; i < 32; ++i) lp[32 * w + i] += 1.0f;
+              // ---- P^T row j (bf16) and partial denominators (fp32) -------------------------
+              if (mw == 0u) {  // key row j of this tile is padding / masked for every column
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pk[i] = 0u;
               } else {
-                // d = s*scale*log2(e) - c (one FFMA; c = -inf before a column's first key gives
-                // +inf, which forces the exact path); masked entries -> -inf (ex2 -> 0).  The mask
-                // word is warp-uniform except on ragged edge tiles: all-allowed / none / mixed.
-                const uint32_t mw = mk[w];
-                if (mw == 0xffffffffu) {
-    #pragma unroll
-                  for (int i = 0; i < 32; i += 4) {
-                    const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
-                    d[i] = fmaf(d[i], sl2, -c4.x);
-                    d[i + 1] = fmaf(d[i + 1], sl2, -c4.y);
-                    d[i + 2] = fmaf(d[i + 2], sl2, -c4.z);
-                    d[i + 3] = fmaf(d[i + 3], sl2, -c4.w);
-                  }
-                } else if (mw == 0u) {
-    #pragma unroll
-                  for (int i = 0; i < 32; ++i) d[i] = -INFINITY;
-                } else {
-    #pragma unroll
-                  for (int i = 0; i < 32; i += 4) {
-                    const float4 c4 = *reinterpret_cast<const float4*>(cg_c + cw + i);
-                    d[i] = ((mw >> i) & 1u) ? fmaf(d[i], sl2, -c4.x) : -INFINITY;
-                    d[i + 1] = ((mw >> (i + 1)) & 1u) ? fmaf(d[i + 1], sl2, -c4.y) : -INFINITY;
-                    d[i + 2] = ((mw >> (i + 2)) & 1u) ? fmaf(d[i + 2], sl2, -c4.z) : -INFINITY;
-                    d[i + 3] = ((mw >> (i + 3)) & 1u) ? fmaf(d[i + 3], sl2, -c4.w) : -INFINITY;
-                  }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const float p0 = ex2(d[2 * i]);
+                  const float p1 = ex2(d[2 * i + 1]);
+                  lp[32 * w + 2 * i] += p0;
+                  lp[32 * w + 2 * i + 1] += p1;
+                  const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                  pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
                 }
-                const bool need = (kExp & 4) ? (t < kGroups)
-                                             : bar_red_or(bar_id, 128, mw != 0u && tree_max<32>(d) > kRescaleThreshold);
-                if (threadIdx.x == 0) trace_at(p, 21 + 4 * w, G);
-                if (need) {
-                  // exact column max of this tile over the group's 128 key rows, from the raw scores
-                  tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
-                  tc_wait_ld();
-    #pragma unroll
-                  for (int i = 0; i < 32; ++i) d[i] = ((mk[w] >> i) & 1u) ? d[i] * sl2 : -INFINITY;
-                  warp_colreduce<32, true>(d, lane);
-                  cg_red[quarter * 32 + lane] = d[0];
-                  named_bar_sync(bar_id, 128);
-                  if (quarter == 0) {
-                    const float mx = fmaxf(fmaxf(cg_red[lane], cg_red[32 + lane]), fmaxf(cg_red[64 + lane], cg_red[96 + lane]));
-                    const float cold = cg_c[cw + lane];
-                    const float nw = fmaxf(cold, mx);
-                    cg_c[cw + lane] = nw;
-                    cg_a[cw + lane] = (nw == -INFINITY) ? 1.0f : ex2(cold - nw);
-                    float mn = nw;
-    #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                    if (lane == 0) cmin_s[(grp * Cfg::kCGg + cg) * kW + w] = mn;
-                  }
-                  named_bar_sync(bar_id, 128);
-                  tmem_ld<32>(tS, reinterpret_cast<uint32_t*>(d));
-                  tc_wait_ld();
-    #pragma unroll
-                  for (int i = 0; i < 32; ++i) {
-                    lp[32 * w + i] *= cg_a[cw + i];
-                    d[i] = ((mk[w] >> i) & 1u) ? fmaf(d[i], sl2, -cg_c[cw + i]) : -INFINITY;
-                  }
-                  if (t >= kGroups) {
-                    // O^T holds this group's PVs of the unit: wait for its last one, rescale columns
-                    const int Gp = G - kGroups;
-                    mbar_wait(pv_done + Gp % kPB, (uint32_t)(Gp / kPB) & 1);
-                    tc_fence_after();
-                    if (j < D) {
-                      uint32_t o[32];
-                      tmem_ld<32>(tO + cw + lane_off, o);
-                      tc_wait_ld();
-    #pragma unroll
-                      for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * cg_a[cw + i]);
-                      tmem_st<32>(tO + cw + lane_off, o);
-                      tc_wait_st();
-                    }
-                  }
-                }
-                if (threadIdx.x == 0) trace_at(p, 7, G);
-                // ---- P^T row j (bf16) and partial denominators (fp32) -------------------------
-                if (mw == 0u) {  // key row j of this tile is padding / masked for every column
-    #pragma unroll
-                  for (int i = 0; i < 16; ++i) pk[i] = 0u;
-                } else {
-    #pragma unroll
-                  for (int i = 0; i < 16; ++i) {
-                    // every 4th pair of an unmasked word on the FMA pipe (balances MUFU and issue)
-                    const bool poly = (i & 7) < kPolyN && mw == 0xffffffffu;
-                    const float p0 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i]) : ex2(d[2 * i]));
-                    const float p1 = (kExp & 1) ? 1.0f : (poly ? ex2_poly(d[2 * i + 1]) : ex2(d[2 * i + 1]));
-                    lp[32 * w + 2 * i] += p0;
-                    lp[32 * w + 2 * i + 1] += p1;
-                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                    pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
-                  }
-                }
-                if (threadIdx.x == 0) trace_at(p, 22 + 4 * w, G);
               }
-              if (w == 0) {
-                if (threadIdx.x == 0) trace_at(p, 8, G);
-                // P buffer pb was last read by PV(G - NP)
-                if (G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
-                if (threadIdx.x == 0) trace_at(p, 9, G);
-              }
+              // P buffer pb was last read by PV(G - NP)
+              if (w == 0 && G >= kNP) mbar_wait(pv_done + (G - kNP) % kPB, (uint32_t)((G - kNP) / kPB) & 1);
               uint8_t* pw = prow + (cw >> 6) * 16384;
               const int ch0 = (cw & 63) >> 3;
-    #pragma unroll
+#pragma unroll
               for (int c8 = 0; c8 < 4; ++c8)
                 *reinterpret_cast<uint4*>(pw + (((ch0 + c8) ^ (j & 7)) << 4)) =
                     make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
-              if (threadIdx.x == 0) trace_at(p, 23 + 4 * w, G);
             }
           }
           // S buffer free for QK(G + NS); P(G) visible to the tensor core
           tc_fence_before();
-          if (threadIdx.x == 0) trace_at(p, 10, G);
           fence_proxy_async_smem();
-          if (threadIdx.x == 0) trace_at(p, 11, G);
           __syncwarp();
           if (lane == 0) {
             mbar_arrive(qk_go + sb);
             mbar_arrive(pv_go + G % kPB);
           }
-          if (threadIdx.x == 0) trace_at(p, 3, G);
         }
       };
       if (fixed_unit) tile_loop(std::true_type{}); else tile_loop(std::false_type{});
 
       // ---- end of unit: this group's denominators -> the epilogue warpgroup -------------
-      if (threadIdx.x == 0) trace_at(p, 28, U);
       if (p.pairs) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
@@ -1268,7 +1140,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         }
         named_bar_arrive(kStatBar0 + tsl, kStatCount);  // references (written by quarter 0) and l final
       }
-      if (threadIdx.x == 0) trace_at(p, 29, U);
       T += n;
     }
   }

@@ -171,6 +171,12 @@ class Context:
         check(self.lib.fvsr_ctx_read_pairs(self.h, C.byref(v)))
         return v.value
 
+    def read_tiles(self):
+        """(key tiles issued, of them with 128 key rows) since the last read; resets."""
+        t, f = C.c_uint64(), C.c_uint64()
+        check(self.lib.fvsr_ctx_read_tiles(self.h, C.byref(t), C.byref(f)))
+        return t.value, f.value
+
     def __del__(self):
         try:
             if getattr(self, "h", None):
