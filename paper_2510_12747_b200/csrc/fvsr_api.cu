@@ -507,7 +507,14 @@ int launch_attn_dqm(const DevGeom& g, const DevMask& dm, const AttnParams& p, in
   FVSR_TRY(ensure_smem(sparse_attn_kernel<D, NQ, MK>, Cfg::kBytes));
   const long long units = p.unit_end - p.unit_begin;
   if (units <= 0) return FVSR_OK;
-  const unsigned grid = (unsigned)std::min<long long>(units, sms);  // persistent CTAs
+  // persistent CTAs: as many as the waves need (792 units on 148 SMs -> 6 waves -> 132 CTAs),
+  // so no SM holds one unit more than the others (FVSR_GRID_BALANCE=0: one CTA per SM)
+  static const int balance = [] {
+    const char* e = std::getenv("FVSR_GRID_BALANCE");
+    return e ? std::atoi(e) : 1;
+  }();
+  const long long waves = (units + sms - 1) / sms;
+  const unsigned grid = (unsigned)(balance ? (units + waves - 1) / waves : std::min<long long>(units, sms));
   FVSR_CUDA(launch_kp(true, sparse_attn_kernel<D, NQ, MK>, dim3(grid), dim3(Cfg::kThreads), Cfg::kBytes, s, g, dm, p));
   return FVSR_OK;
 }
