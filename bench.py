@@ -255,16 +255,17 @@ def run_b200(args):
         l = s % LAYERS
         t = T0 + s // LAYERS
         q, k, v = pool_local[(t + l) % POOL]
-        _abi.check(lib.fvsr_ring_append(ctx.h, rings.h, l, t, k.data_ptr(), v.data_ptr(), C.c_void_p(sptr)))
         ids = (C.c_int32 * 1)(t)
+        # one C-ABI call: ring append + mask builder (one launch) + sparse attention
         if gather is None:
-            _abi.check(lib.fvsr_ring_attention(ctx.h, rings.h, l, q.data_ptr(), ids, 1, C.byref(md), TOPK, scale,
-                                               0, -1, out_tok.data_ptr(), 0, 0, None, None, C.c_void_p(sptr)))
+            _abi.check(lib.fvsr_ring_step(ctx.h, rings.h, l, t, k.data_ptr(), v.data_ptr(), q.data_ptr(), ids, 1,
+                                          C.byref(md), TOPK, scale, 0, -1, out_tok.data_ptr(), 0, 0, None, None,
+                                          C.c_void_p(sptr)))
         else:
             buf = gather.next_shard()
-            _abi.check(lib.fvsr_ring_attention(ctx.h, rings.h, l, q.data_ptr(), ids, 1, C.byref(md), TOPK, scale,
-                                               sh.local_unit_begin, sh.local_unit_end, buf.data_ptr(), 1, 0, None,
-                                               None, C.c_void_p(sptr)))
+            _abi.check(lib.fvsr_ring_step(ctx.h, rings.h, l, t, k.data_ptr(), v.data_ptr(), q.data_ptr(), ids, 1,
+                                          C.byref(md), TOPK, scale, sh.local_unit_begin, sh.local_unit_end,
+                                          buf.data_ptr(), 1, 0, None, None, C.c_void_p(sptr)))
             gather.launch()
         _abi.check(lib.fvsr_ring_evict_sliding(rings.h, l))
 
@@ -321,8 +322,7 @@ def run_b200(args):
     pairs_span = ctx.read_pairs()
     tiles_span, full_span = ctx.read_tiles()
     attn_ms, attn_n = ctx.timing_read(_abi.TIME_ATTENTION)
-    mb_ms, mb_n = ctx.timing_read(_abi.TIME_MASK_BUILDER)
-    ap_ms, ap_n = ctx.timing_read(_abi.TIME_APPEND, clear=True)
+    fr_ms, fr_n = ctx.timing_read(_abi.TIME_FRONT, clear=True)
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -379,10 +379,9 @@ def run_b200(args):
                                                C.c_void_p(streams[j].cuda_stream)))
         else:
             qd, kd, vd = (x.to(dev, non_blocking=True) for x in (q, k, v))
-            rings.append(l, t, kd, vd)
             buf = gather.next_shard()
-            rings.attention(l, qd, [t], mask, TOPK, unit_begin=sh.local_unit_begin, unit_end=sh.local_unit_end,
-                            out=buf, tile_major=True, check_errors=False)
+            rings.step(l, t, kd, vd, qd, [t], mask, TOPK, unit_begin=sh.local_unit_begin, unit_end=sh.local_unit_end,
+                       out=buf[: sh.u1 - sh.u0], tile_major=True, check_errors=False)
             gather.launch()
             full = gather.result()
             ho.view(-1)[: full.numel()].copy_(full.reshape(-1)[: ho.numel()], non_blocking=True)
@@ -439,15 +438,17 @@ def run_b200(args):
     roofline["full_tiles_per_launch"] = nf_l
     roofline["tile_tflops"] = tile_flops / (attn_avg_ms / 1e3) / 1e12
     roofline["tile_flops_per_launch"] = tile_flops
-    mb_avg = mb_ms / max(1, mb_n)
+    fr_avg = fr_ms / max(1, fr_n)
     bnk = 3 * tiles  # context {28..32}: t_rows 14, 15, 16
-    mb_bytes = nh * N * D * 2 + nh * bnk * D * 4 + nh * tiles * TOPK * 4  # Q once, pooled K, indices
-    mask_builder = {"avg_us": mb_avg * 1e3, "algorithmic_bytes": mb_bytes,
-                    "gbs": mb_bytes / (mb_avg / 1e3) / 1e9 if mb_avg > 0 else None, "peak_gbs": pk["hbm_gbs"]}
-    ap_avg = ap_ms / max(1, ap_n)
+    # front kernel (ring append + mask builder, one launch): K/V read + written once, their
+    # pooled partials written, Q read once and its packed tiles written, the ring's pooled
+    # keys read, indices written
     ap_bytes = 2 * 2 * nh * N * D * 2 + nh * tiles * D * 4 * 2
-    append = {"avg_us": ap_avg * 1e3, "algorithmic_bytes": ap_bytes,
-              "gbs": ap_bytes / (ap_avg / 1e3) / 1e9 if ap_avg > 0 else None}
+    mb_bytes = nh * N * D * 2 * 2 + nh * bnk * D * 4 + nh * tiles * TOPK * 4
+    front = {"kernel": "ring_front_kernel (append + Q pack/pool + coarse scores + top-k)", "avg_us": fr_avg * 1e3,
+             "algorithmic_bytes": ap_bytes + mb_bytes,
+             "gbs": (ap_bytes + mb_bytes) / (fr_avg / 1e3) / 1e9 if fr_avg > 0 else None, "peak_gbs": pk["hbm_gbs"],
+             "frac": (ap_bytes + mb_bytes) / (fr_avg / 1e3) / 1e9 / pk["hbm_gbs"] if fr_avg > 0 else None}
 
     # ---- CPU baseline (reference on host cores, rank 0, N=1 only) ----------------------------
     cpu = None
@@ -469,8 +470,7 @@ def run_b200(args):
                    "parallelism": f"head-parallel x{world}" if world > 1 else "single GPU"},
         "eff_tflops": eff_tflops,
         "roofline": roofline,
-        "mask_builder": mask_builder,
-        "kv_append": append,
+        "front": front,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clocks.summary(),

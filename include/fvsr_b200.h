@@ -98,6 +98,7 @@ typedef struct {
   int64_t words_per_row; /* FVSR_MASK_BITMASK only: (Lk + 63) / 64 */
 } fvsr_mask;
 
+/* FVSR_FLAG_SYNC_CHECK: synchronize and check the device error word after every call. */
 enum { FVSR_FLAG_SYNC_CHECK = 1 };
 
 /* Output layouts of fvsr_ring_attention. */
@@ -111,7 +112,7 @@ enum {
 enum { FVSR_EVICT_SLIDING = 0, FVSR_EVICT_UNIFORM = 1, FVSR_EVICT_HEAD_WISE = 2 };
 
 /* Kernel classes timed by fvsr_ctx_timing_enable. */
-enum { FVSR_TIME_APPEND = 0, FVSR_TIME_MASK_BUILDER = 1, FVSR_TIME_ATTENTION = 2 };
+enum { FVSR_TIME_APPEND = 0, FVSR_TIME_MASK_BUILDER = 1, FVSR_TIME_ATTENTION = 2, FVSR_TIME_FRONT = 3 };
 
 typedef struct fvsr_ctx fvsr_ctx;
 typedef struct fvsr_ring fvsr_ring;
@@ -238,6 +239,18 @@ FVSR_API int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* ring, int32_t lay
                             int64_t topk, float scale, int64_t unit_begin, int64_t unit_end,
                             uint16_t* out, int32_t out_layout, int32_t sel_cap, int32_t* sel,
                             int32_t* sel_count, fvsr_stream_t stream);
+
+/* One streaming layer-step of step() (P/src/stream.cpp:228-256) on device: KVCache::append of
+ * frame `frame_id`'s K/V (k, v: [heads][rows*cols][d] bf16, as fvsr_ring_append) followed by
+ * head_attention for the query frames (as fvsr_ring_attention, whose arguments these are).
+ * The append and the query pack + pool share one kernel launch (independent inputs, one pass
+ * over HBM), coarse scores + top-k a second, then the sparse attention kernel: three launches
+ * per layer-step.  The ring keeps the new frame; evict afterwards as with fvsr_ring_append. */
+FVSR_API int32_t fvsr_ring_step(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer, int32_t frame_id, const uint16_t* k,
+                                const uint16_t* v, const uint16_t* q, const int32_t* q_frame_ids, int32_t nq,
+                                const fvsr_mask* mask, int64_t topk, float scale, int64_t unit_begin,
+                                int64_t unit_end, uint16_t* out, int32_t out_layout, int32_t sel_cap, int32_t* sel,
+                                int32_t* sel_count, fvsr_stream_t stream);
 
 /* ---- scored eviction ------------------------------------------------- */
 /* frame_attention_mass (P/src/kv_cache.cpp:170-206; declared P/include/vsr/kv_cache.hpp:79):

@@ -27,7 +27,7 @@ MASK_ALL, MASK_LOCALITY, MASK_BITMASK = 0, 1, 2
 LOCALITY_PRESERVED, LOCALITY_TRUNCATED = 0, 1
 FLAG_SYNC_CHECK = 1
 OUT_TOKEN_MAJOR, OUT_TILE_MAJOR = 0, 1
-TIME_APPEND, TIME_MASK_BUILDER, TIME_ATTENTION = 0, 1, 2
+TIME_APPEND, TIME_MASK_BUILDER, TIME_ATTENTION, TIME_FRONT = 0, 1, 2, 3
 
 
 class Error(RuntimeError):
@@ -109,6 +109,8 @@ SIGNATURES = {
     "fvsr_ring_frame_mass": (I32, [P, P, I32, C.POINTER(I32), I32, MP, P, P]),
     "fvsr_ring_evict": (I32, [P, I32, I32, P]),
     "fvsr_build_flags": (C.c_char_p, []),
+    "fvsr_ring_step": (I32, [P, P, I32, I32, P, P, P, C.POINTER(I32), I32, MP, I64, F32, I64, I64, P, I32, I32, P,
+                             P, P]),
     "fvsr_ctx_read_tiles": (I32, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "fvsr_ring_step_host": (I32, [P, P, I32, I32, P, P, P, MP, I64, F32, P, P]),
 }

@@ -507,14 +507,11 @@ int launch_attn_dqm(const DevGeom& g, const DevMask& dm, const AttnParams& p, in
   FVSR_TRY(ensure_smem(sparse_attn_kernel<D, NQ, MK>, Cfg::kBytes));
   const long long units = p.unit_end - p.unit_begin;
   if (units <= 0) return FVSR_OK;
-  // persistent CTAs: as many as the waves need (792 units on 148 SMs -> 6 waves -> 132 CTAs),
-  // so no SM holds one unit more than the others (FVSR_GRID_BALANCE=0: one CTA per SM)
-  static const int balance = [] {
-    const char* e = std::getenv("FVSR_GRID_BALANCE");
-    return e ? std::atoi(e) : 1;
-  }();
+  // persistent CTAs, round robin over whole units: as many as the waves need (792 units on 148
+  // SMs -> 6 waves -> 132 CTAs), so no SM holds one unit more than the others.  Every unit is
+  // processed whole by one CTA: its output does not depend on the launch's other units.
   const long long waves = (units + sms - 1) / sms;
-  const unsigned grid = (unsigned)(balance ? (units + waves - 1) / waves : std::min<long long>(units, sms));
+  const unsigned grid = (unsigned)((units + waves - 1) / waves);
   FVSR_CUDA(launch_kp(true, sparse_attn_kernel<D, NQ, MK>, dim3(grid), dim3(Cfg::kThreads), Cfg::kBytes, s, g, dm, p));
   return FVSR_OK;
 }
@@ -1063,20 +1060,46 @@ int32_t fvsr_ring_frame_ids(const fvsr_ring* r, int32_t layer, int32_t* ids, int
   return FVSR_OK;
 }
 
-int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const uint16_t* q,
-                            const int32_t* q_frame_ids, int32_t nq, const fvsr_mask* mask, int64_t topk, float scale,
-                            int64_t unit_begin, int64_t unit_end, uint16_t* out, int32_t out_layout,
-                            int32_t sel_cap, int32_t* sel, int32_t* sel_count, fvsr_stream_t stream) {
-  FVSR_TRY(check_ctx(ctx));
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+}  // extern "C"
+
+namespace {
+// The new frame of a fused step (KVCache::append, P/src/kv_cache.cpp:39-47).
+struct AppendSpec {
+  const uint16_t* k;
+  const uint16_t* v;
+  int frame_id;
+};
+
+// Ring attention of one layer-step: mask builder (one launch: optional ring append of the
+// new frame, Q pack + pool, coarse scores, top-k) then the sparse attention kernel.
+int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, const int32_t* q_frame_ids, int nq,
+                   const fvsr_mask* mask, int64_t topk, float scale, int64_t unit_begin, int64_t unit_end,
+                   uint16_t* out, int out_layout, int sel_cap, int32_t* sel, int32_t* sel_count,
+                   const AppendSpec* app, cudaStream_t s) {
   if (!r || !q || !out || !q_frame_ids) return fail(FVSR_E_SHAPE, "ring_attention: null argument");
   if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
-  const auto& c = r->ctx[layer];
-  if (c.empty()) return fail(FVSR_E_CONFIG, "ring_attention: empty context");
+  auto& c = r->ctx[layer];
+  int app_slot = -1, partner = -1;
+  if (app) {  // fvsr_ring_append's contract (kv_cache.cpp:39-47)
+    if (!app->k || !app->v) return fail(FVSR_E_SHAPE, "ring_append: null argument");
+    if (app->frame_id < 0) return fail(FVSR_E_CONFIG, "TokenGrid: negative frame id");
+    if (!c.empty() && app->frame_id <= c.back().first)
+      return fail(FVSR_E_INVARIANT, "KVCache: frame ids must increase");  // kv_cache.cpp:42
+    for (int i = 0; i < r->slots; ++i)
+      if (!r->used[layer][i]) { app_slot = i; break; }
+    if (app_slot < 0)
+      return fail(FVSR_E_INVARIANT, "KVCache: head retains more than window + current (evict before append)");
+    if ((app->frame_id & 1) && !c.empty() && c.back().first == app->frame_id - 1) partner = c.back().second;
+  }
+  if (c.empty() && !app) return fail(FVSR_E_CONFIG, "ring_attention: empty context");
   std::vector<int> kids, kslots;
   for (auto& fs : c) {
     kids.push_back(fs.first);
     kslots.push_back(fs.second);
+  }
+  if (app) {
+    kids.push_back(app->frame_id);
+    kslots.push_back(app_slot);
   }
   fvsr_grid gq{q_frame_ids, nq, r->rows, r->cols};
   fvsr_grid gk{kids.data(), (int)kids.size(), r->rows, r->cols};
@@ -1085,6 +1108,8 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   DevMask dm;
   FVSR_TRY(build_mask(mask, g, grid_tokens(&gk), dm));
   if (topk < 1) return fail(FVSR_E_CONFIG, "plan_sparse: topk must be >= 1");
+  if (g.bnk > 32 * 128) return fail(FVSR_E_CONFIG, "too many key blocks (%d > 4096) for the selector", g.bnk);
+  if (g.d % 8 != 0) return fail(FVSR_E_CONFIG, "pack_pool: head_dim must be a multiple of 8 (got %d)", g.d);
   const int cap_need = (int)std::min<long long>(topk, g.bnk);
   if (sel && sel_cap < cap_need) return fail(FVSR_E_SHAPE, "ring_attention: sel_cap < min(topk, bnk)");
   const int cap = sel ? sel_cap : cap_need;
@@ -1094,8 +1119,8 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   const size_t qbytes = (size_t)r->heads * g.nqf * g.n_tiles * tb;
   const size_t qpart = (size_t)r->heads * g.nqf * g.n_tiles * d;
   const size_t nsel = (size_t)r->heads * g.bnq;
-  int st;
   const size_t qn = (size_t)r->heads * g.nqf * g.n_tiles;
+  int st;
   void* ws = ws_get(ctx, Carve::need({qbytes, qpart * 4, qpart * 4, nsel * cap * 4, nsel * 4, qn * 4}), &st);
   if (!ws) return st;
   Carve cv(ws);
@@ -1107,11 +1132,41 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   float* qn2 = cv.take<float>(qn);
   int* use_sel = sel ? sel : wsel;
   int* use_cnt = sel_count ? sel_count : wcnt;
-
+  const size_t n_scores = (size_t)r->heads * g.bnq * g.bnk;
+  if (ctx_reserve_scores(ctx, n_scores) != FVSR_OK) return FVSR_E_CUDA;
   {
-    SpanGuard sg(ctx, s, FVSR_TIME_MASK_BUILDER);
+    SpanGuard sg(ctx, s, app ? FVSR_TIME_FRONT : FVSR_TIME_MASK_BUILDER);
+    FrontArgs fa{};
+    // append: K -> swizzled ring slot + pooled partials (S1 continues the even partner), V -> slot
+    if (app) {
+      PackPoolArgs& a = fa.kv;
+      a.src = app->k;
+      a.src2 = app->v;
+      a.src_head_stride = (long long)r->rows * r->cols * d;
+      a.dst = r->k_layer(layer);
+      a.dst2 = r->v_layer(layer);
+      a.dst_head_stride = r->kv_head_stride();
+      a.s0 = r->s0_layer(layer);
+      a.s1 = r->s1_layer(layer);
+      a.part_head_stride = r->part_head_stride();
+      a.ext_s0 = r->s0_layer(layer);
+      a.norm2 = r->kn2_layer(layer);
+      a.norm2_head_stride = r->kn2_head_stride();
+      a.rows = r->rows;
+      a.cols = r->cols;
+      a.tiles_w = r->tiles_w;
+      a.n_tiles = r->n_tiles;
+      a.d = d;
+      FVSR_TRY(rope_args(r, &app->frame_id, 1, a));
+      fa.kv_pg.first[0] = 0;
+      fa.kv_pg.count[0] = 1;
+      fa.kv_pg.ext_slot[0] = partner;
+      fa.kv_sl.s[0] = app_slot;
+      if ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.src2)) % 16 != 0)
+        return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
+    }
     // one pass over Q: swizzled query tiles for the tensor cores + pooled partials for the plan
-    PackPoolArgs a{};
+    PackPoolArgs& a = fa.q;
     a.src = q;
     a.src_head_stride = Lq * d;
     a.dst = qp;
@@ -1126,28 +1181,81 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
     a.tiles_w = g.tiles_w;
     a.n_tiles = g.n_tiles;
     a.d = d;
+    if (reinterpret_cast<uintptr_t>(q) % 16 != 0)
+      return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
     FVSR_TRY(rope_args(r, q_frame_ids, nq, a));
-    PoolGroups pg{};
-    SlotList sl{};
-    for (int t = 0; t < g.nq_trows; ++t) {
-      pg.first[t] = g.q_tr_first[t];
-      pg.count[t] = g.q_tr_count[t];
-      pg.ext_slot[t] = -1;
-    }
-    for (int i = 0; i < g.nqf; ++i) sl.s[i] = i;
     int max_cnt = 1;
-    for (int t = 0; t < g.nq_trows; ++t) max_cnt = std::max(max_cnt, g.q_tr_count[t]);
-    FVSR_TRY(launch_pack_pool(a, pg, sl, dim3(g.n_tiles, g.nq_trows, r->heads), max_cnt, s));
-    const float cscale = 1.0f / std::sqrt(static_cast<float>(d));
-    FVSR_TRY(launch_select(ctx, g, dm, r->heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, r->s0_layer(layer),
-                           r->s1_layer(layer), r->part_head_stride(), cscale, topk, cap, use_sel, use_cnt, nullptr,
-                           nullptr, nullptr, s));
-    ctx->stamp.ring = r;
-    ctx->stamp.layer = layer;
-    ctx->stamp.gen = r->gen[layer];
-    ctx->stamp.qids.assign(q_frame_ids, q_frame_ids + nq);
-    ctx->stamp.mask = mask ? *mask : fvsr_mask{};
+    for (int t = 0; t < g.nq_trows; ++t) {
+      fa.q_pg.first[t] = g.q_tr_first[t];
+      fa.q_pg.count[t] = g.q_tr_count[t];
+      fa.q_pg.ext_slot[t] = -1;
+      max_cnt = std::max(max_cnt, g.q_tr_count[t]);
+    }
+    for (int i = 0; i < g.nqf; ++i) fa.q_sl.s[i] = i;
+    fa.heads = r->heads;
+    fa.n_tiles = g.n_tiles;
+    fa.q_trows = g.nq_trows;
+    SelectParams p{};
+    p.q_s0 = qs0;
+    p.q_s1 = qs1;
+    p.q_head_stride = (long long)g.nqf * g.n_tiles * d;
+    p.k_s0 = r->s0_layer(layer);
+    p.k_s1 = r->s1_layer(layer);
+    p.k_head_stride = r->part_head_stride();
+    p.scale = 1.0f / std::sqrt(static_cast<float>(d));  // sparse.cpp:97
+    p.topk = topk;
+    p.cap = cap;
+    p.npow2 = npow2(g.bnk);
+    p.sel = use_sel;
+    p.sel_count = use_cnt;
+    p.coarse = ctx->d_scores;  // kept for fvsr_ring_frame_mass
+    p.err = ctx->d_err;
+    const size_t rope_bytes =
+        r->rope ? (size_t)(2 * (r->rope_split[0] / 2) + 8 * (r->rope_split[1] / 2) + 8 * (r->rope_split[2] / 2)) *
+                      sizeof(float2)
+                : 0;
+    // launch 1: ring append + Q pack/pool (independent inputs, one pass)
+    const size_t smem_p = ring_pack_smem(d, max_cnt, rope_bytes);
+    const unsigned grid_p = (unsigned)((app ? r->heads * g.n_tiles : 0) + r->heads * g.nq_trows * g.n_tiles);
+    auto kp = r->rope ? ring_pack_kernel<true> : ring_pack_kernel<false>;
+    FVSR_TRY(ensure_smem(kp, smem_p));
+    FVSR_CUDA(launch_k(kp, dim3(grid_p), dim3(kPPThreads), smem_p, s, fa));
+    // launch 2: coarse scores + top-k (programmatic launch: its prologue overlaps launch 1's tail)
+    const size_t smem_s = mask_select_smem(d, g.bnk);
+    const unsigned grid_s = (unsigned)(r->heads * ((g.bnq + kFrontQB - 1) / kFrontQB));
+    auto launch_s = [&](auto kern) -> int {
+      FVSR_TRY(ensure_smem(kern, smem_s));
+      FVSR_CUDA(launch_kp(true, kern, dim3(grid_s), dim3(kFrontThreads), smem_s, s, g, dm, p));
+      return FVSR_OK;
+    };
+    if (smem_s <= 200 * 1024) {
+      st = g.bnk <= 256 ? launch_s(mask_select_kernel<8>)
+                        : (g.bnk <= 1024 ? launch_s(mask_select_kernel<32>) : launch_s(mask_select_kernel<128>));
+      FVSR_TRY(st);
+      ctx->launches += 2;
+    } else {  // score rows too long for shared memory: scores through L2, then the row selector
+      FVSR_TRY(launch_select(ctx, g, dm, r->heads, qs0, qs1, p.q_head_stride, p.k_s0, p.k_s1, p.k_head_stride, p.scale,
+                             topk, cap, use_sel, use_cnt, nullptr, ctx->d_scores, nullptr, s));
+      ctx->launches += 3;
+    }
+    if (ctx->flags & FVSR_FLAG_SYNC_CHECK) {  // debugging: attribute a fault to the front launches
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return fail(FVSR_E_CUDA, "ring front kernels: %s", cudaGetErrorString(e));
+    }
+    ctx->scores_heads = r->heads;
+    ctx->scores_bnq = g.bnq;
+    ctx->scores_bnk = g.bnk;
   }
+  if (app) {  // the new frame is in the ring from here on
+    r->used[layer][app_slot] = 1;
+    c.emplace_back(app->frame_id, app_slot);
+    ++r->gen[layer];
+  }
+  ctx->stamp.ring = r;
+  ctx->stamp.layer = layer;
+  ctx->stamp.gen = r->gen[layer];
+  ctx->stamp.qids.assign(q_frame_ids, q_frame_ids + nq);
+  ctx->stamp.mask = mask ? *mask : fvsr_mask{};
   const long long units_total = (long long)r->heads * g.nq_trows * g.n_tiles;
   if (unit_end < 0 || unit_end > units_total) unit_end = units_total;
   if (unit_begin < 0 || unit_begin > unit_end) return fail(FVSR_E_CONFIG, "ring_attention: bad unit range");
@@ -1176,7 +1284,30 @@ int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const ui
   p.qn2 = qn2;
   p.qn2_head_stride = (long long)g.nqf * g.n_tiles;
   FVSR_TRY(launch_attention(ctx, g, dm, p, r->heads, unit_begin, unit_end, s));
-  return after_launch(ctx, s, 4);
+  return after_launch(ctx, s, 0);
+}
+}  // namespace
+
+extern "C" {
+
+int32_t fvsr_ring_attention(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const uint16_t* q,
+                            const int32_t* q_frame_ids, int32_t nq, const fvsr_mask* mask, int64_t topk, float scale,
+                            int64_t unit_begin, int64_t unit_end, uint16_t* out, int32_t out_layout,
+                            int32_t sel_cap, int32_t* sel, int32_t* sel_count, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  return ring_step_impl(ctx, r, layer, q, q_frame_ids, nq, mask, topk, scale, unit_begin, unit_end, out, out_layout,
+                        sel_cap, sel, sel_count, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int32_t fvsr_ring_step(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* k,
+                       const uint16_t* v, const uint16_t* q, const int32_t* q_frame_ids, int32_t nq,
+                       const fvsr_mask* mask, int64_t topk, float scale, int64_t unit_begin, int64_t unit_end,
+                       uint16_t* out, int32_t out_layout, int32_t sel_cap, int32_t* sel, int32_t* sel_count,
+                       fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  const AppendSpec app{k, v, frame_id};
+  return ring_step_impl(ctx, r, layer, q, q_frame_ids, nq, mask, topk, scale, unit_begin, unit_end, out, out_layout,
+                        sel_cap, sel, sel_count, &app, reinterpret_cast<cudaStream_t>(stream));
 }
 
 // ---- scored eviction ------------------------------------------------------
@@ -1396,10 +1527,9 @@ int32_t fvsr_ring_step_host(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t 
   FVSR_CUDA(cudaMemcpyAsync(dq, q_host, bytes, cudaMemcpyHostToDevice, s));
   FVSR_CUDA(cudaMemcpyAsync(dk, k_host, bytes, cudaMemcpyHostToDevice, s));
   FVSR_CUDA(cudaMemcpyAsync(dv, v_host, bytes, cudaMemcpyHostToDevice, s));
-  FVSR_TRY(fvsr_ring_append(ctx, r, layer, frame_id, dk, dv, stream));
   const int32_t qids[1] = {frame_id};
-  FVSR_TRY(fvsr_ring_attention(ctx, r, layer, dq, qids, 1, mask, topk, scale, 0, -1, dout, FVSR_OUT_TOKEN_MAJOR, 0,
-                               nullptr, nullptr, stream));
+  FVSR_TRY(fvsr_ring_step(ctx, r, layer, frame_id, dk, dv, dq, qids, 1, mask, topk, scale, 0, -1, dout,
+                          FVSR_OUT_TOKEN_MAJOR, 0, nullptr, nullptr, stream));
   FVSR_TRY(fvsr_ring_evict_sliding(r, layer));
   FVSR_CUDA(cudaMemcpyAsync(out_host, dout, bytes, cudaMemcpyDeviceToHost, s));
   return FVSR_OK;

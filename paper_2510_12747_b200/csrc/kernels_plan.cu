@@ -181,14 +181,16 @@ __device__ __forceinline__ uint32_t rope_word(uint32_t v, float2 cs) {
   return *reinterpret_cast<const uint32_t*>(&b);
 }
 
+// One (tile, t_row group, head) of the fused pack + pool pass by the whole CTA (kPPThreads
+// threads), staging through `sm_pp` (pack_pool_smem bytes + RoPE tables).  A CTA that runs
+// several passes calls it with use = 0, 1, 2, ...: the staging barrier is initialised once
+// (use 0) and waited on with parity use & 1 (an mbarrier is not re-initialised while live),
+// with a __syncthreads between passes.  `aux` (if given) holds the staging barrier and the
+// RoPE tables apart from the tile staging area, which the caller may then reuse.
 template <bool ROPE>
-__global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_constant__ PackPoolArgs a,
-                                                               const __grid_constant__ PoolGroups groups,
-                                                               const __grid_constant__ SlotList slots) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ __align__(128) uint8_t sm_pp[];
-  const int tile = blockIdx.x, grp = blockIdx.y, head = blockIdx.z;
+__device__ __forceinline__ void pack_pool_body(const PackPoolArgs& a, const PoolGroups& groups,
+                                               const SlotList& slots, int tile, int grp, int head,
+                                               uint8_t* sm_pp, int use = 0, uint8_t* aux = nullptr) {
   const int tid = threadIdx.x;
   const int d = a.d;
   const int th = tile / a.tiles_w, tw = tile - th * a.tiles_w;
@@ -197,7 +199,8 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
   const uint32_t tile_bytes = (uint32_t)d * 128u;
   const int f0 = groups.first[grp], cnt = groups.count[grp], es = groups.ext_slot[grp];
   const int nt = a.src2 ? 2 : 1;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm_pp + (size_t)cnt * nt * tile_bytes);
+  uint8_t* aux_p = aux ? aux : sm_pp + (size_t)cnt * nt * tile_bytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(aux_p);
   auto stage = [&](int fi, int t) -> uint8_t* { return sm_pp + (size_t)(fi * nt + t) * tile_bytes; };
   const bool full = hc == 8 && wc == 8;
   if (!full) {  // edge tile: rows / columns past the frame are zero
@@ -206,8 +209,10 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
     __syncthreads();
   }
   if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_barrier_init();
+    if (use == 0) {
+      mbar_init(bar, 1);
+      fence_barrier_init();
+    }
     fence_proxy_async_smem();
     const uint32_t row_bytes = (uint32_t)wc * d * 2;
     mbar_arrive_expect_tx(bar, row_bytes * hc * cnt * nt);
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
   }
   // RoPE tables of this tile -> shared memory while the bulk copies are in flight:
   // t: [cnt][dt/2], h: [8 tile rows][dh/2], w: [8 tile cols][dw/2]
-  float2* rtab = reinterpret_cast<float2*>(sm_pp + (size_t)cnt * nt * tile_bytes + 16);
+  float2* rtab = reinterpret_cast<float2*>(aux_p + 16);
   if constexpr (ROPE) {
     const int ht = a.rope_dt >> 1, hh = a.rope_dh >> 1, hw = a.rope_dw >> 1;
     for (int i = tid; i < cnt * ht; i += kPPThreads) {
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
     }
   }
   __syncthreads();
-  mbar_wait(bar, 0);
+  mbar_wait(bar, (uint32_t)use & 1u);
   // RoPE (ROPE): applied on the fly where the pooling and packing phases read the staged
   // src rows (both round the rotated pair to bf16 the same way, so the pooled sums, the |k|
   // bound and the stored tile agree); no serial rotate phase, no write-back
@@ -369,6 +374,16 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
       }
     }
   }
+}
+
+template <bool ROPE>
+__global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_constant__ PackPoolArgs a,
+                                                               const __grid_constant__ PoolGroups groups,
+                                                               const __grid_constant__ SlotList slots) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(128) uint8_t sm_pp[];
+  pack_pool_body<ROPE>(a, groups, slots, blockIdx.x, blockIdx.y, blockIdx.z, sm_pp);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -845,6 +860,164 @@ __global__ void __launch_bounds__(kFThreads) score_topk_kernel(const __grid_cons
   // ---- top-k: warp w -> q-block qb0 + w ----------------------------------------------
   const int qb = qb0 + warp;
   if (qb < g.bnq) topk_row<NPER>(g, m, p, qb, head, sc + (size_t)warp * bnk);
+}
+
+// ---------------------------------------------------------------------------------------
+// Streaming front end of one layer-step (ring append + mask builder) in two launches:
+//   ring_pack_kernel   blocks [0, heads*n_tiles): KVCache::append of the new frame's tile
+//                      (swizzled K/V ring slot, pooled partials, |k| bounds); the blocks after
+//                      that: the query frames' tiles (packed for the tensor cores, pooled
+//                      partials, |q| bounds).  Independent inputs, one pass over HBM.
+//   mask_select_kernel kFrontQB q-blocks of one head per block: pooled queries, coarse scores
+//                      against the ring's pooled keys streamed through shared memory in
+//                      kFrontKC-block chunks (exact sequential chains, P/src/tensor.cpp:121-151,
+//                      sparse.cpp:97-99), top-k with the forced diagonal (topk_row).
+// ---------------------------------------------------------------------------------------
+constexpr int kFrontQB = 8;     // q-blocks per mask-select block (one warp each for top-k)
+constexpr int kFrontThreads = kFrontQB * 32;
+constexpr int kFrontKC = kFrontThreads;  // pooled key blocks staged per chunk: one per thread
+
+struct FrontArgs {
+  PackPoolArgs kv;   // append: src = k, src2 = v, dst/dst2 = ring slots (src null: no append)
+  PoolGroups kv_pg;
+  SlotList kv_sl;
+  PackPoolArgs q;    // query frames: packed tiles + pooled partials into the workspace
+  PoolGroups q_pg;
+  SlotList q_sl;
+  int heads, n_tiles, q_trows;
+};
+
+inline size_t ring_pack_smem(int d, int max_q_cnt, size_t rope_bytes) {
+  return std::max(pack_pool_smem(d, 1, true), pack_pool_smem(d, max_q_cnt, false)) + rope_bytes;
+}
+
+template <bool ROPE>
+__global__ void __launch_bounds__(kPPThreads) ring_pack_kernel(const __grid_constant__ FrontArgs fa) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(128) uint8_t sm_rp[];
+  const int n_append = fa.kv.src != nullptr ? fa.heads * fa.n_tiles : 0;
+  int b = blockIdx.x;
+  if (b < n_append) {
+    const int head = b / fa.n_tiles;
+    pack_pool_body<ROPE>(fa.kv, fa.kv_pg, fa.kv_sl, b - head * fa.n_tiles, 0, head, sm_rp);
+    return;
+  }
+  b -= n_append;
+  const int per_head = fa.q_trows * fa.n_tiles;
+  const int head = b / per_head, rem = b - head * per_head, qtr = rem / fa.n_tiles;
+  pack_pool_body<ROPE>(fa.q, fa.q_pg, fa.q_sl, rem - qtr * fa.n_tiles, qtr, head, sm_rp);
+}
+
+inline size_t mask_select_smem(int d, int bnk) {
+  return ((size_t)(kFrontQB + kFrontKC) * (d + 4) + (size_t)kFrontQB * bnk) * 4;
+}
+
+template <int NPER>
+__global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid_constant__ DevGeom g,
+                                                                    const __grid_constant__ DevMask m,
+                                                                    const __grid_constant__ SelectParams p) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) float sm_ms[];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int per_head = (g.bnq + kFrontQB - 1) / kFrontQB;
+  const int head = blockIdx.x / per_head;
+  const int qb0 = (blockIdx.x - head * per_head) * kFrontQB;
+  const int nqb = min(kFrontQB, g.bnq - qb0);
+  const int d = g.d, ld = d + 4, d4 = d >> 2, bnk = g.bnk;
+  float* pq = sm_ms;                 // [kFrontQB][d+4]
+  float* pk = pq + kFrontQB * ld;    // [kFrontKC][d+4]
+  float* sc = pk + kFrontKC * ld;    // [kFrontQB][bnk]
+  bool fin = true;
+  // pooled keys, kFrontKC blocks per chunk; each chunk's row sources and 1/count come from
+  // one thread per row (shared), then every thread has its loads of the chunk in flight at once
+  constexpr int kPer = kFrontKC * 32 / kFrontThreads;  // float4 per thread per chunk (d <= 128)
+  __shared__ const float* rsrc[kFrontKC];
+  __shared__ float rinv[kFrontKC];
+  const int lg4 = d4 == 32 ? 5 : 4;  // d in {64, 128}
+  // pooled queries: S1 (two-frame rows) or S0, times 1/count (avg_pool_blocks' final scale)
+  for (int idx = tid; idx < kFrontQB * d4; idx += kFrontThreads) {
+    const int r = idx >> lg4, c4 = idx & (d4 - 1);
+    float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < nqb) {
+      const int qb = qb0 + r, qtr = qb / g.n_tiles, qtile = qb - qtr * g.n_tiles;
+      const int qcnt = g.q_tr_count[qtr], qf = g.q_tr_first[qtr] + qcnt - 1;
+      const float* src = (qcnt == 2 ? p.q_s1 : p.q_s0) + head * p.q_head_stride + ((long long)qf * g.n_tiles + qtile) * d;
+      const float inv = __fdiv_rn(1.0f, (float)(qcnt * tile_h_count(g, qtile) * tile_w_count(g, qtile)));
+      w = __ldg(reinterpret_cast<const float4*>(src) + c4);
+      w.x = __fmul_rn(w.x, inv);
+      w.y = __fmul_rn(w.y, inv);
+      w.z = __fmul_rn(w.z, inv);
+      w.w = __fmul_rn(w.w, inv);
+      fin = fin && isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w);
+    }
+    *reinterpret_cast<float4*>(pq + r * ld + c4 * 4) = w;
+  }
+  for (int kc0 = 0; kc0 < bnk; kc0 += kFrontKC) {
+    const int nk = min(kFrontKC, bnk - kc0);
+    if (tid < kFrontKC) {
+      const int kb = kc0 + tid;
+      const float* src = nullptr;
+      float inv = 0.0f;
+      if (tid < nk) {
+        const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+        const int kcnt = g.k_tr_count[ktr], kf = g.k_tr_first[ktr] + kcnt - 1;
+        src = (kcnt == 2 ? p.k_s1 : p.k_s0) + head * p.k_head_stride + ((long long)g.k_slot[kf] * g.n_tiles + ktile) * d;
+        inv = __fdiv_rn(1.0f, (float)(kcnt * tile_h_count(g, ktile) * tile_w_count(g, ktile)));
+      }
+      rsrc[tid] = src;
+      rinv[tid] = inv;
+    }
+    __syncthreads();  // row sources ready; the previous chunk's scores have read pk
+    {
+      float4 kv4[kPer];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int idx = tid + j * kFrontThreads, r = idx >> lg4, c4 = idx & (d4 - 1);
+        const float* src = r < kFrontKC ? rsrc[r] : nullptr;
+        kv4[j] = src ? __ldg(reinterpret_cast<const float4*>(src) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int idx = tid + j * kFrontThreads, r = idx >> lg4, c4 = idx & (d4 - 1);
+        if (r < nk) {
+          const float inv = rinv[r];
+          float4 w = kv4[j];
+          w.x = __fmul_rn(w.x, inv);
+          w.y = __fmul_rn(w.y, inv);
+          w.z = __fmul_rn(w.z, inv);
+          w.w = __fmul_rn(w.w, inv);
+          fin = fin && isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w);
+          *reinterpret_cast<float4*>(pk + r * ld + c4 * 4) = w;
+        }
+      }
+    }
+    __syncthreads();
+    // thread t scores key block kc0 + t against the kFrontQB pooled queries: kFrontQB
+    // independent exact chains (channels ascending, separate multiply and add from 0.0f, then
+    // the 1/sqrt(d) multiply); query rows are warp-broadcast loads, the key row stays put
+    if (tid < nk) {
+      float acc[kFrontQB];
+#pragma unroll
+      for (int k = 0; k < kFrontQB; ++k) acc[k] = 0.0f;
+      const float* kr = pk + tid * ld;
+#pragma unroll 2
+      for (int c = 0; c < d; c += 4) {
+        const float4 b = *reinterpret_cast<const float4*>(kr + c);
+#pragma unroll
+        for (int k = 0; k < kFrontQB; ++k) {
+          const float4 a = *reinterpret_cast<const float4*>(pq + k * ld + c);
+          chain4(acc[k], a, b);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kFrontQB; ++k) sc[k * bnk + kc0 + tid] = __fmul_rn(acc[k], p.scale);
+    }
+    __syncthreads();
+  }
+  if (!fin) atomicOr(p.err, kErrShape);
+  if (warp < nqb) topk_row<NPER>(g, m, p, qb0 + warp, head, sc + warp * bnk);
 }
 
 // ---------------------------------------------------------------------------------------

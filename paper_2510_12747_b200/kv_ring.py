@@ -119,7 +119,7 @@ class KVRing:
                   topk: int = 1, scale: Optional[float] = None, *, unit_begin: int = 0, unit_end: int = -1,
                   out: Optional[torch.Tensor] = None, tile_major: bool = False,
                   sel: Optional[torch.Tensor] = None, sel_count: Optional[torch.Tensor] = None,
-                  check_errors: bool = True) -> torch.Tensor:
+                  check_errors: bool = True, _append=None) -> torch.Tensor:
         mask = mask or Mask.all_allowed()
         self._last_mask[layer] = mask
         q3 = _heads3(q, "ring attention q")
@@ -141,13 +141,34 @@ class KVRing:
         ids = (C.c_int32 * nq)(*[int(f) for f in q_frame_ids])
         md = mask.c()
         cap = sel.shape[-1] if sel is not None else 0
-        check(self.ctx.lib.fvsr_ring_attention(self.ctx.h, self.h, layer, q3.data_ptr(), ids, nq, C.byref(md),
-                                               int(topk), float(scale), int(unit_begin), int(unit_end),
-                                               out.data_ptr(), 1 if tile_major else 0, cap, sel.data_ptr() if sel is not None else None,
-                                               sel_count.data_ptr() if sel_count is not None else None, _stream()))
+        sp = sel.data_ptr() if sel is not None else None
+        cp = sel_count.data_ptr() if sel_count is not None else None
+        if _append is None:
+            check(self.ctx.lib.fvsr_ring_attention(self.ctx.h, self.h, layer, q3.data_ptr(), ids, nq, C.byref(md),
+                                                   int(topk), float(scale), int(unit_begin), int(unit_end),
+                                                   out.data_ptr(), 1 if tile_major else 0, cap, sp, cp, _stream()))
+        else:
+            fid, k3, v3 = _append
+            check(self.ctx.lib.fvsr_ring_step(self.ctx.h, self.h, layer, fid, k3.data_ptr(), v3.data_ptr(),
+                                              q3.data_ptr(), ids, nq, C.byref(md), int(topk), float(scale),
+                                              int(unit_begin), int(unit_end), out.data_ptr(), 1 if tile_major else 0,
+                                              cap, sp, cp, _stream()))
         if check_errors:
             self.ctx.check_errors()
         return out
+
+    def step(self, layer: int, frame_id: int, k: torch.Tensor, v: torch.Tensor, q: torch.Tensor,
+             q_frame_ids: Optional[Sequence[int]] = None, mask: Optional[Mask] = None, topk: int = 1,
+             scale: Optional[float] = None, *, unit_begin: int = 0, unit_end: int = -1,
+             out: Optional[torch.Tensor] = None, tile_major: bool = False, sel: Optional[torch.Tensor] = None,
+             sel_count: Optional[torch.Tensor] = None, check_errors: bool = True) -> torch.Tensor:
+        """append(layer, frame_id, k, v) + attention(layer, q, q_frame_ids, ...) as ONE C-ABI call
+        (fvsr_ring_step): the append and the mask builder share one kernel launch."""
+        k3, v3 = self._frame(k, "append k"), self._frame(v, "append v")
+        q_frame_ids = [int(frame_id)] if q_frame_ids is None else [int(f) for f in q_frame_ids]
+        return self.attention(layer, q, q_frame_ids, mask, topk, scale, unit_begin=unit_begin, unit_end=unit_end,
+                              out=out, tile_major=tile_major, sel=sel, sel_count=sel_count,
+                              check_errors=check_errors, _append=(int(frame_id), k3, v3))
 
     def step_host(self, layer: int, frame_id: int, q_host: torch.Tensor, k_host: torch.Tensor,
                   v_host: torch.Tensor, out_host: torch.Tensor, mask: Optional[Mask] = None, topk: int = 1,

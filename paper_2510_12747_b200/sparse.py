@@ -158,6 +158,11 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.fvsr_ctx_launch_count(self.h))
 
+    def set_flags(self, flags: int) -> None:
+        """fvsr_ctx_set_flags: FLAG_SYNC_CHECK (see include/fvsr_b200.h)."""
+        self.flags = int(flags)
+        check(self.lib.fvsr_ctx_set_flags(self.h, int(flags)))
+
     def timing(self, enable: bool) -> None:
         check(self.lib.fvsr_ctx_timing_enable(self.h, 1 if enable else 0))
 
