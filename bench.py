@@ -131,48 +131,54 @@ def cpu_model():
     return "unknown"
 
 
-def reference_case(seed: int = 1234, head: int = 0):
-    """One head of the step at t=32 over {28..32}, fp32 values that are bf16-representable."""
+def reference_cases():
+    """The 12 heads of the step at t=32 over {28..32}: per-head q/k/v drawn from
+    vsr::Rng(1234 + head) (fp32 values that are bf16-representable), as compiled-reference
+    cases (oracle/_ref; None when it is not built)."""
     import oracle
     N = ROWS * COLS
-    q, k, v = oracle.synthetic_qkv(seed + head, N, 5 * N, D)
-    return q, k, v
-
-
-def time_reference_heads(n_heads: int, threads: int, warmup: int = 1):
-    """Median seconds for one head of the reference head_attention (partition, mask,
-    plan_sparse, sparse_attention_exec; P/src/stream.cpp:175-194)."""
-    import numpy as np
-    import oracle
-    kind = "reference"
     try:
         ref = oracle.Ref()
     except Exception:
-        ref = None
-        kind = "port"
+        return None
+    cases = []
+    for h in range(HEADS):
+        q, k, v = oracle.synthetic_qkv(1234 + h, N, 5 * N, D)
+        cases.append(ref.case(q, k, v, [T0], list(range(T0 - WINDOW, T0 + 1)), ROWS, COLS, oracle.Mask.all()))
+    return cases
+
+
+def time_reference_steps(n_steps: int, threads: int, warmup: int = 1):
+    """Wall seconds of whole layer-steps of the reference hot path: head_attention (partition,
+    mask, plan_sparse, sparse_attention_exec; P/src/stream.cpp:175-194) for each of the 12
+    heads, distinct per-head inputs, `threads` worker threads per call.  Plus one head at
+    threads=1 (reported separately, x12 extrapolated and labelled so)."""
+    import oracle
     scale = oracle.head_scale(D)
-    times = []
-    q, k, v = reference_case()
-    if ref is not None:
-        case = ref.case(q, k, v, [T0], list(range(T0 - WINDOW, T0 + 1)), ROWS, COLS, oracle.Mask.all())
-        for i in range(warmup + n_heads):
-            t = time.perf_counter()
-            case.head_attention(TOPK, scale, threads)
-            dt = time.perf_counter() - t
-            if i >= warmup:
-                times.append(dt)
-    else:
+    cases = reference_cases()
+    if cases is None:  # no compiled reference: the C port, one head per step, x12
         port = oracle.Port()
-        threads = 1
+        q, k, v = oracle.synthetic_qkv(1234, ROWS * COLS, 5 * ROWS * COLS, D)
         kf = list(range(T0 - WINDOW, T0 + 1))
-        for i in range(warmup + n_heads):
+        times = []
+        for i in range(warmup + n_steps):
             t = time.perf_counter()
             plan = port.plan(q, k, [T0], kf, ROWS, COLS, oracle.Mask.all(), TOPK)
             port.exec(q, k, v, [T0], kf, ROWS, COLS, oracle.Mask.all(), plan, scale)
-            dt = time.perf_counter() - t
             if i >= warmup:
-                times.append(dt)
-    return statistics.median(times), kind, threads, times
+                times.append((time.perf_counter() - t) * HEADS)
+        return statistics.median(times), "port", 1, times, None
+    times = []
+    for i in range(warmup + n_steps):
+        t = time.perf_counter()
+        for c in cases:
+            c.head_attention(TOPK, scale, threads)
+        if i >= warmup:
+            times.append(time.perf_counter() - t)
+    t = time.perf_counter()
+    cases[0].head_attention(TOPK, scale, 1)
+    t1_head = time.perf_counter() - t
+    return statistics.median(times), "reference", threads, times, t1_head
 
 
 def run_reference_arm(args):
@@ -180,22 +186,28 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = cpu_threads()
-    # each step = one head of the layer-step (a bounded sample); value scales to 12 heads.
-    # At most 20 timed samples (+2 warm-up) so the arm ends within minutes for any --steps.
-    n_timed, n_warm = max(1, min(args.steps, 20)), min(args.warmup, 2)
-    med, kind, threads_used, times = time_reference_heads(n_timed, threads, warmup=n_warm)
-    tokens_per_s = ROWS * COLS / (HEADS * med)
+    # each step = one whole 12-head layer-step of the reference; at most 8 timed steps (+1
+    # warm-up) so the arm ends within a couple of minutes for any --steps
+    n_timed = max(1, min(args.steps, 8))
+    med, kind, threads_used, times, t1_head = time_reference_steps(n_timed, threads, warmup=1)
+    tokens_per_s = ROWS * COLS / med
+    sample = (f"{n_timed} whole layer-steps (12 head_attention calls each, distinct per-head inputs), median "
+              f"{med*1e3:.1f} ms/step, threads={threads_used}, {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": med * HEADS * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (vsr::Rng N(0,1), bf16-rounded)",
+        "steps": n_timed, "steps_requested": args.steps, "warmup": 1, "ms_per_step": med * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (vsr::Rng N(0,1), bf16-representable), per-head seeds 1234+h",
         "config": {"workload": WORKLOAD, "heads": HEADS, "d": D, "latent": [ROWS, COLS], "window": WINDOW,
                    "topk": TOPK, "mask": "all"},
         "cpu_baseline": {"value": tokens_per_s, "unit": "tokens/s", "cores": threads_used, "kind": kind,
-                         "sample": f"{n_timed} single-head head_attention calls (1/12 of a layer-step each), "
-                                   f"median {med*1e3:.1f} ms, threads={threads_used}, {cpu_model()}"},
+                         "sample": sample},
         "e2e": {"value": tokens_per_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if t1_head is not None:
+        line["cpu_threads1"] = {"value": ROWS * COLS / (t1_head * HEADS), "unit": "tokens/s", "cores": 1,
+                                "sample": f"one head_attention call at threads=1 ({t1_head*1e3:.0f} ms), x12 heads "
+                                          "(extrapolated)"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -249,7 +261,7 @@ def run_b200(args):
 
     state = {"s": 0}
 
-    def step():
+    def step(md=md):
         s = state["s"]
         state["s"] += 1
         l = s % LAYERS
@@ -323,6 +335,35 @@ def run_b200(args):
     tiles_span, full_span = ctx.read_tiles()
     attn_ms, attn_n = ctx.timing_read(_abi.TIME_ATTENTION)
     fr_ms, fr_n = ctx.timing_read(_abi.TIME_FRONT, clear=True)
+    # the same step with the paper's locality window at 768x1408 (48x72 latent tokens, truncated;
+    # SURVEY 8(d)), measured the same way (spans + kernel-counted pairs)
+    variants = {}
+    if world == 1:
+        mloc = fv.Mask.locality(48, 72, truncated=True).c()
+        for _ in range(10):
+            step(mloc)
+        barrier()
+        ctx.read_pairs()
+        ctx.timing(True)
+        ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev_a.record(stream)
+        nv = min(args.steps, 100)
+        for _ in range(nv):
+            step(mloc)
+        ev_b.record(stream)
+        barrier()
+        ctx.timing(False)
+        ctx.check_errors()
+        vp = ctx.read_pairs()
+        va_ms, va_n = ctx.timing_read(_abi.TIME_ATTENTION)
+        ctx.timing_read(_abi.TIME_FRONT, clear=True)
+        v_step = ev_a.elapsed_time(ev_b) / nv  # includes the span events (serialises the PDL overlap)
+        v_attn = va_ms / max(1, va_n)
+        v_eff = 4.0 * D * vp / max(1, va_n) / (v_attn / 1e3) / 1e12
+        variants["locality_48x72_truncated"] = {
+            "mask": "locality 48x72 truncated", "attention_us": v_attn * 1e3, "eff_tflops": v_eff,
+            "frac": v_eff / peaks()["bf16_tflops"], "executed_pairs_per_launch": vp / max(1, va_n),
+            "step_us_with_span_events": v_step * 1e3, "tokens_per_s_with_span_events": N / (v_step / 1e3)}
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -415,18 +456,22 @@ def run_b200(args):
     attn_avg_ms = attn_ms / max(1, attn_n)
     pairs_per_launch = pairs_span / max(1, attn_n)
     achieved = 4.0 * D * pairs_per_launch / (attn_avg_ms / 1e3) / 1e12
-    traffic = None
-    prof = os.path.join(HERE, "profiles", "ncu_attention_summary.json")
+    traffic, traffic_src = None, None
+    prof = os.path.join(HERE, "profiles", "ncu_attention_r2.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                pj = json.load(f)
+            traffic = pj.get("dram_bytes_per_launch")
+            traffic_src = ("ncu --set full of this kernel at this workload (not measured in this run): "
+                           f"profiles/ncu_attention_r2.json, {pj.get('source', '')}")
         except Exception:
             traffic = None
     roofline = {"kernel": "sparse_attn_kernel<128>", "bound": "tensor", "achieved": achieved,
                 "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"],
                 "frac_sustained": achieved / pk["bf16_tflops_sustained"] if pk["bf16_tflops_sustained"] else None,
                 "peak_source": pk["source"] + " burst bf16 (MEASURED_PEAKS.json)", "traffic": traffic,
+                "traffic_source": traffic_src,
                 "flops_per_launch": 4.0 * D * pairs_per_launch,
                 "flop_def": "4*d per executed (mask-allowed, selected-block) token pair, counted by the kernel",
                 "avg_launch_us": attn_avg_ms * 1e3, "launches": attn_n}
@@ -438,6 +483,23 @@ def run_b200(args):
     roofline["full_tiles_per_launch"] = nf_l
     roofline["tile_tflops"] = tile_flops / (attn_avg_ms / 1e3) / 1e12
     roofline["tile_flops_per_launch"] = tile_flops
+    # the K/V gather (L2 -> shared memory, cp.async.bulk): the attention kernel's binding
+    # resource: bytes each launch moves into shared memory per key tile
+    # (16 KB frame-tile halves of K and V) plus each unit's Q tile, against the measured
+    # per-SM bulk-copy ingest cap (tools/l2bench, profiles/l2bench_r2.json)
+    tile_b = 128 * D
+    gather_bytes = (nf_l * 2 + (nt_l - nf_l)) * tile_b * 2 + HEADS * tiles * tile_b
+    l2cap = None
+    try:
+        with open(os.path.join(HERE, "profiles", "l2bench_r2.json")) as f:
+            rows = json.load(f)["rows"]
+        l2cap = max(r["GBps"] for r in rows if r["buffer_mb"] == 64 and r["grid"] == 148)
+    except Exception:
+        pass
+    roofline["gather"] = {"bytes_per_launch": gather_bytes, "achieved_gbs": gather_bytes / (attn_avg_ms / 1e3) / 1e9,
+                          "peak_gbs": l2cap, "frac": (gather_bytes / (attn_avg_ms / 1e3) / 1e9 / l2cap) if l2cap else None,
+                          "peak_source": "L2->SMEM cp.async.bulk ingest, 148 CTAs x 32 KB stages, L2-resident 64 MB "
+                                         "(tools/l2bench.cu, profiles/l2bench_r2.json)"}
     fr_avg = fr_ms / max(1, fr_n)
     bnk = 3 * tiles  # context {28..32}: t_rows 14, 15, 16
     # front kernel (ring append + mask builder, one launch): K/V read + written once, their
@@ -454,11 +516,14 @@ def run_b200(args):
     cpu = None
     if world == 1 and not args.no_cpu:
         threads = cpu_threads()
-        med, kind, threads_used, times = time_reference_heads(args.cpu_heads, threads)
-        cpu = {"value": N / (HEADS * med), "unit": "tokens/s", "cores": threads_used, "kind": kind,
-               "sample": f"{args.cpu_heads} single-head head_attention calls of the same step (partition, mask, "
-                         f"plan_sparse, sparse_attention_exec), median {med*1e3:.1f} ms/head x 12 heads, "
+        med, kind, threads_used, times, t1_head = time_reference_steps(args.cpu_steps, threads, warmup=0)
+        cpu = {"value": N / med, "unit": "tokens/s", "cores": threads_used, "kind": kind,
+               "sample": f"{args.cpu_steps} whole layer-steps of the reference (12 head_attention calls each: "
+                         f"partition, mask, plan_sparse, sparse_attention_exec), median {med*1e3:.1f} ms/step, "
                          f"threads={threads_used}, {cpu_model()}"}
+        if t1_head is not None:
+            cpu["threads1"] = {"value": N / (t1_head * HEADS), "unit": "tokens/s", "cores": 1,
+                               "sample": f"one head at threads=1 ({t1_head*1e3:.0f} ms), x12 heads (extrapolated)"}
 
     line = {
         "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -471,6 +536,7 @@ def run_b200(args):
         "eff_tflops": eff_tflops,
         "roofline": roofline,
         "front": front,
+        "variants": variants,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clocks.summary(),
@@ -492,7 +558,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=30)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=120)
-    ap.add_argument("--cpu-heads", type=int, default=3)
+    ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":

@@ -263,6 +263,8 @@ class Ref:
             lib.vsrref_report.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                           C.POINTER(C.c_uint64), C.c_char_p, C.c_int]
             lib.vsrref_dense.argtypes = [C.c_void_p, C.c_float, C.POINTER(C.c_float), C.c_char_p, C.c_int]
+            lib.vsrref_dense_stream.argtypes = [C.c_void_p, C.c_float, C.c_long, C.POINTER(C.c_float), C.c_char_p,
+                                                C.c_int]
             lib.vsrref_apply_rope.argtypes = [C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                               C.POINTER(C.c_int), C.POINTER(C.c_float), C.c_char_p, C.c_int]
             lib.vsrref_segment_mask.argtypes = [C.POINTER(C.c_int), C.c_long, C.POINTER(C.c_uint64), C.c_char_p,
@@ -365,6 +367,16 @@ class Ref:
             out = np.zeros(len(self.kf), np.float64)
             err = C.create_string_buffer(512)
             st = self.lib.vsrref_frame_mass(self.h, _ptr(out, C.c_double), err, 512)
+            if st:
+                raise OracleError(st, err.value.decode())
+            return out
+
+        def dense_stream(self, scale: float, rows: int) -> np.ndarray:
+            """dense_attention_stream (P/src/attention.cpp:58-99) on the first `rows` query rows."""
+            rows = min(int(rows), self.lq)
+            out = np.zeros((rows, self.q.shape[1]), np.float32)
+            err = C.create_string_buffer(512)
+            st = self.lib.vsrref_dense_stream(self.h, C.c_float(scale), C.c_long(rows), _ptr(out, C.c_float), err, 512)
             if st:
                 raise OracleError(st, err.value.decode())
             return out

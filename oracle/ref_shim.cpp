@@ -237,6 +237,21 @@ int vsrref_dense(const vsrref_case* c, float scale, float* out, char* err, int e
   });
 }
 
+// dense_attention_stream (P/src/attention.cpp:58-99), the reference's dense baseline, on the
+// first `rows` query rows of the case (timed CPU sample for the dense-causal comparison).
+int vsrref_dense_stream(const vsrref_case* c, float scale, long rows, float* out, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const std::size_t m = std::min<std::size_t>(static_cast<std::size_t>(rows), c->q.shape[0]);
+    const std::size_t d = c->q.shape[1];
+    vsr::TensorF32 qs({m, d}, std::vector<float>(c->q.data.begin(), c->q.data.begin() + m * d));
+    vsr::MaskMatrix ms(m, c->mask.cols(), false);
+    for (std::size_t i = 0; i < m; ++i)
+      std::memcpy(ms.row_words(i), c->mask.row_words(i), ms.words_per_row() * sizeof(std::uint64_t));
+    vsr::TensorF32 o = vsr::dense_attention_stream(qs, c->k, c->v, ms, scale);
+    if (out) std::memcpy(out, o.data.data(), o.data.size() * sizeof(float));
+  });
+}
+
 // One head of the reference streaming hot path as head_attention runs it
 // (P/src/stream.cpp:175-194): partitions, mask, plan_sparse, sparse_attention_exec.
 // Used only as the timed CPU baseline.  Returns the executed plan's density.

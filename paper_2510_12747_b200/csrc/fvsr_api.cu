@@ -451,27 +451,6 @@ int launch_select(fvsr_ctx* ctx, const DevGeom& g, const DevMask& dm, int heads,
   p.allowed = allowed;
   p.err = ctx->d_err;
   if (g.d % 4 != 0) return fail(FVSR_E_CONFIG, "plan_sparse: head_dim must be a multiple of 4 (got %d)", g.d);
-  // fused scores + top-k when every pooled key of a head fits in shared memory (opt-in:
-  // FVSR_FUSED_SELECT=1; measured slower than the two-kernel path at 768x1408: 108 CTAs of
-  // serial staging vs 240 + 108 wider ones)
-  const size_t smem_f = score_topk_smem(g.bnk, g.d);
-  static const bool fused_select = [] {
-    const char* e = std::getenv("FVSR_FUSED_SELECT");
-    return e && std::atoi(e) != 0;
-  }();
-  if (fused_select && smem_f <= 200 * 1024 && g.bnk <= 32 * 16) {
-    ctx->scores_heads = ctx->scores_bnq = ctx->scores_bnk = 0;
-    p.coarse = coarse;
-    dim3 gf((g.bnq + kFQB - 1) / kFQB, heads);
-    if (g.bnk <= 32 * 8) {
-      FVSR_TRY(ensure_smem(score_topk_kernel<8>, smem_f));
-      FVSR_CUDA(launch_k(score_topk_kernel<8>, dim3(gf), dim3(kFThreads), smem_f, s, g, dm, p));
-    } else {
-      FVSR_TRY(ensure_smem(score_topk_kernel<16>, smem_f));
-      FVSR_CUDA(launch_k(score_topk_kernel<16>, dim3(gf), dim3(kFThreads), smem_f, s, g, dm, p));
-    }
-    return FVSR_OK;
-  }
   // coarse scores -> workspace (L2-resident, heads*bnq*bnk floats), then per-row top-k
   const size_t n_scores = (size_t)heads * g.bnq * g.bnk;
   float* scores = coarse;

@@ -746,122 +746,6 @@ __global__ void __launch_bounds__(kTopkWarps * 32) topk_select_kernel(const __gr
   topk_row<NPER>(g, m, p, qb, head, scores + ((long long)head * g.bnq + qb) * g.bnk);
 }
 
-// Fused coarse scores + top-k for grids whose pooled keys fit in shared memory: one CTA per
-// (head, kFQB q-blocks) stages every pooled key and its pooled queries once (exact
-// 1/count scaling, finite check), computes the kFQB x bnk scores with the same exact
-// sequential chains as coarse_score_kernel (4 independent chains per thread), then one
-// warp per q-block runs topk_row on the scores in shared memory.  One launch, no score
-// round trip through L2.
-constexpr int kFQB = 8, kFThreads = kFQB * 32;
-
-inline size_t score_topk_smem(int bnk, int d) {
-  return ((size_t)(bnk + kFQB) * (d + 4) + (size_t)kFQB * bnk) * 4 + 16;
-}
-
-template <int NPER>
-__global__ void __launch_bounds__(kFThreads) score_topk_kernel(const __grid_constant__ DevGeom g,
-                                                              const __grid_constant__ DevMask m,
-                                                              const __grid_constant__ SelectParams p) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ __align__(16) float smf[];
-  const int d = g.d, ld = d + 4, d4 = d >> 2, bnk = g.bnk;
-  const int rows = bnk + kFQB;                      // pooled keys, then pooled queries
-  float* pk = smf;                                  // [bnk][d+4]
-  float* pq = smf + (size_t)bnk * ld;               // [kFQB][d+4]
-  float* sc = pq + (size_t)kFQB * ld;               // [kFQB][bnk]
-  const int qb0 = blockIdx.x * kFQB, head = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kWarps = kFThreads / 32;
-  // ---- stage: warp w copies rows w, w + kWarps, ...; lane = float4 column --------------
-  bool fin = true;
-  auto row_src = [&](int r, float& inv) -> const float* {
-    int cnt_tok;
-    const float* src;
-    if (r < bnk) {
-      const int kb = r, ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
-      const int kcnt = g.k_tr_count[ktr], kf = g.k_tr_first[ktr] + kcnt - 1;
-      src = (kcnt == 2 ? p.k_s1 : p.k_s0) + head * p.k_head_stride + ((long long)g.k_slot[kf] * g.n_tiles + ktile) * d;
-      cnt_tok = kcnt * tile_h_count(g, ktile) * tile_w_count(g, ktile);
-    } else {
-      const int qb = qb0 + (r - bnk);
-      if (qb >= g.bnq) { inv = 0.0f; return nullptr; }
-      const int qtr = qb / g.n_tiles, qtile = qb - qtr * g.n_tiles;
-      const int qcnt = g.q_tr_count[qtr], qf = g.q_tr_first[qtr] + qcnt - 1;
-      src = (qcnt == 2 ? p.q_s1 : p.q_s0) + head * p.q_head_stride + ((long long)qf * g.n_tiles + qtile) * d;
-      cnt_tok = qcnt * tile_h_count(g, qtile) * tile_w_count(g, qtile);
-    }
-    inv = __fdiv_rn(1.0f, (float)cnt_tok);
-    return src;
-  };
-  constexpr int kB = 8;
-  for (int c4 = lane; c4 < d4; c4 += 32) {
-    for (int r0 = warp; r0 < rows; r0 += kB * kWarps) {
-      float4 v[kB];
-      float inv[kB];
-#pragma unroll
-      for (int k = 0; k < kB; ++k) {
-        const int r = r0 + k * kWarps;
-        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        inv[k] = 0.0f;
-        if (r < rows) {
-          const float* src = row_src(r, inv[k]);
-          if (src) v[k] = __ldg(reinterpret_cast<const float4*>(src) + c4);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kB; ++k) {
-        const int r = r0 + k * kWarps;
-        if (r < rows) {
-          float4 w = v[k];
-          w.x = __fmul_rn(w.x, inv[k]);
-          w.y = __fmul_rn(w.y, inv[k]);
-          w.z = __fmul_rn(w.z, inv[k]);
-          w.w = __fmul_rn(w.w, inv[k]);
-          fin = fin && isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w);
-          *reinterpret_cast<float4*>(smf + (size_t)r * ld + c4 * 4) = w;
-        }
-      }
-    }
-  }
-  if (!fin) atomicOr(p.err, kErrShape);
-  __syncthreads();
-  // ---- scores: 4 independent exact chains per thread (channels ascending, mul then add) ----
-  const int n_sc = kFQB * bnk;
-  for (int s0 = tid; s0 < n_sc; s0 += 4 * kFThreads) {
-    const float* qr[4];
-    const float* kr[4];
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int sidx = min(s0 + k * kFThreads, n_sc - 1);
-      qr[k] = pq + (size_t)(sidx / bnk) * ld;
-      kr[k] = pk + (size_t)(sidx % bnk) * ld;
-    }
-#pragma unroll 2
-    for (int c = 0; c < d; c += 4) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float4 a = *reinterpret_cast<const float4*>(qr[k] + c);
-        const float4 b = *reinterpret_cast<const float4*>(kr[k] + c);
-        acc[k] = __fadd_rn(acc[k], __fmul_rn(a.x, b.x));
-        acc[k] = __fadd_rn(acc[k], __fmul_rn(a.y, b.y));
-        acc[k] = __fadd_rn(acc[k], __fmul_rn(a.z, b.z));
-        acc[k] = __fadd_rn(acc[k], __fmul_rn(a.w, b.w));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int sidx = s0 + k * kFThreads;
-      if (sidx < n_sc) sc[sidx] = __fmul_rn(acc[k], p.scale);
-    }
-  }
-  __syncthreads();
-  // ---- top-k: warp w -> q-block qb0 + w ----------------------------------------------
-  const int qb = qb0 + warp;
-  if (qb < g.bnq) topk_row<NPER>(g, m, p, qb, head, sc + (size_t)warp * bnk);
-}
-
 // ---------------------------------------------------------------------------------------
 // Streaming front end of one layer-step (ring append + mask builder) in two launches:
 //   ring_pack_kernel   blocks [0, heads*n_tiles): KVCache::append of the new frame's tile

@@ -96,3 +96,14 @@ def test_error_taxonomy_matches_reference():
         with pytest.raises(exc):
             _abi.check(code)
         assert oracle.ERRORS[code] == exc.__name__
+
+
+def test_sparsity_csv_format_is_the_reference_one():
+    """sparsity-csv-v1 header/row layout (P/src/bench.cpp:49-60; P/tests/test_config.cpp:80-87)."""
+    from paper_2510_12747_b200.bench_sparsity import (SparsityRow, sparsity_csv_header, sparsity_csv_row,
+                                                      topk_for_density)
+    r = SparsityRow(4, 0.125, 0.1234567, 1.5, 12.0, 8.0, 0.001)
+    assert sparsity_csv_header() == "k,density,flop_ratio,wall_ms_sparse,wall_ms_dense,speedup,max_abs_err_vs_dense"
+    assert sparsity_csv_header().count(",") == sparsity_csv_row(r).count(",")
+    assert sparsity_csv_row(r) == "4,0.125,0.123457,1.5,12,8,0.001"
+    assert topk_for_density(0.136, 198) == 27 and topk_for_density(1.0, 7) == 7 and topk_for_density(0.001, 5) == 1
