@@ -256,6 +256,25 @@ __device__ __forceinline__ long long half_offset(const DevGeom& g, uint32_t h) {
   return ((long long)g.k_slot[(h >> 11) & 31u] * g.n_tiles + kt) * kUnit;
 }
 
+// Locality window (build_locality_mask, P/src/mask.cpp:109-147) from the key side: bit r of the
+// result is set when query coordinate p0 + r (r < 8) sees key coordinate k along an axis of
+// length F with extent e.  Truncated: |k - p| <= e/2.  Preserved: the window start
+// a(p) = clamp(p - e/2, 0, F - e) is monotone in p, so the p with a(p) <= k < a(p) + e are
+// (p < e/2 and k < e) | (e/2 <= p <= F - e + e/2 and k - e + e/2 < p <= k + e/2) |
+// (p > F - e + e/2 and k >= F - e): at most three intervals.
+__device__ __forceinline__ uint32_t bit_interval(int a, int b, int p0) {  // bits of p in [a, b] n [p0, p0+7]
+  const int lo = max(a, p0) - p0, hi = min(b, p0 + 7) - p0;
+  return lo > hi ? 0u : ((2u << hi) - (1u << lo));
+}
+__device__ __forceinline__ uint32_t window_bits(int mode, int k, int p0, int e, int F) {
+  const int r = e / 2;
+  if (mode == 1) return bit_interval(k - r, k + r, p0);
+  uint32_t bits = bit_interval(r - e + k + 1, k + r, p0) & bit_interval(r, F - e + r, p0);
+  if (k < e) bits |= bit_interval(p0, r - 1, p0);
+  if (k >= F - e) bits |= bit_interval(F - e + r + 1, p0 + 7, p0);
+  return bits;
+}
+
 // MK: token-mask kind (0 all-allowed, 1 locality window, 2 explicit bitmask), fixed at
 // compile time so the per-tile mask logic of the other kinds costs nothing.
 template <int D, int NQ, int MK>
@@ -424,17 +443,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
     } else {
       for (int i = et; i < kInfoCap; i += 128) info[i] = block_desc(g, sel_at(sel, i));
       if (et == 0) utab[sl * 8] = n;
-    }
-    if (MK == 1 && et >= 32 && et < 40) {
-      const int e = et - 32;
-      const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
-      int lo, hi;
-      locality_range(m.mode, qh0 + e, m.extent_h, g.rows, lo, hi);
-      win2[sl * 32 + e] = lo;
-      win2[sl * 32 + 8 + e] = hi;
-      locality_range(m.mode, qw0 + e, m.extent_w, g.cols, lo, hi);
-      win2[sl * 32 + 16 + e] = lo;
-      win2[sl * 32 + 24 + e] = hi;
     }
     named_bar_sync(kEpiBar, 128);
     const int nt = utab[sl * 8];
@@ -816,7 +824,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
       const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
       const float* kn2_s = kn2_2 + tsl * kInfoCap;
       const float* qn2_s = qn2_2 + tsl;
-      const int* win = win2 + tsl * 32;
       // this group's references (and their word minima) start at the unit's initial value;
       // the epilogue of unit U - 2 (same slot) released them with the tables
       float* cg_c = c_s + (tsl * 2 + grp) * 128;
@@ -874,21 +881,16 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
 #pragma unroll
               for (int w = 0; w < kW; ++w) mk[w] = qvalid[w];
             } else if (MK == 1) {
-              uint32_t wb = 0, hb = 0;  // allowed query cols / rows of the 8x8 query tile
+              // allowed query cols / rows of the 8x8 query tile, closed form (window_bits)
+              const uint32_t hb = window_bits(m.mode, kh, qh0, m.extent_h, g.rows);
+              const uint32_t wb = window_bits(m.mode, kw, qw0, m.extent_w, g.cols);
+              // 64-bit tile mask: byte r (query tile row r) = wb where hb has bit r
+              unsigned long long rows64 = 0;
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                wb |= (kw >= win[16 + i] && kw < win[24 + i]) ? (1u << i) : 0u;
-                hb |= (kh >= win[i] && kh < win[8 + i]) ? (1u << i) : 0u;
-              }
+              for (int r = 0; r < 8; ++r) rows64 |= ((hb >> r) & 1u) ? (0xffull << (8 * r)) : 0ull;
+              const unsigned long long m64 = rows64 & ((unsigned long long)wb * 0x0101010101010101ull);
 #pragma unroll
-              for (int w = 0; w < kW; ++w) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const int qc = (col0 + 32 * w + i) & 63;
-                  if (((hb >> (qc >> 3)) & (wb >> (qc & 7)) & 1u) != 0u) mk[w] |= 1u << i;
-                }
-                mk[w] &= qvalid[w];
-              }
+              for (int w = 0; w < kW; ++w) mk[w] = (uint32_t)(m64 >> ((col0 + 32 * w) & 63)) & qvalid[w];
             } else {
               const long long tk = g.k_frame_tok0[kf] + (long long)kh * g.cols + kw;
 #pragma unroll
