@@ -166,6 +166,15 @@ FVSR_API int32_t fvsr_plan_sparse(fvsr_ctx* ctx, const uint16_t* q, const uint16
                          int32_t* sel_count, int32_t* diag, float* coarse, uint8_t* allowed,
                          fvsr_stream_t stream);
 
+/* fvsr_plan_sparse on fp32 inputs (q, k: DEVICE fp32 [heads][L][d]): the reference's own
+ * inputs, pooled exactly as avg_pool_blocks does, so the plan (indices, coarse scores) is
+ * bit-exact with vsr::plan_sparse on ANY fp32 data (the C++ drop-in layer plans this way). */
+FVSR_API int32_t fvsr_plan_sparse_f32(fvsr_ctx* ctx, const float* q, const float* k, int32_t heads,
+                         int32_t d, const fvsr_grid* grid_q, const fvsr_grid* grid_k,
+                         const fvsr_mask* mask, int64_t topk, int32_t cap, int32_t* sel,
+                         int32_t* sel_count, int32_t* diag, float* coarse, uint8_t* allowed,
+                         fvsr_stream_t stream);
+
 /* sparse_attention_exec: exact softmax attention restricted to each query block's
  * selected key blocks and the token mask, tcgen05 tensor cores, fp32 online softmax,
  * bf16 out [heads][Lq][d].  Rows outside [row_begin, row_end) are written as zeros

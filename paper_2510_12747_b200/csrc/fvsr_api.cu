@@ -410,7 +410,8 @@ void launch_pack(const uint16_t* src, long long src_head_stride, int heads, int 
 }
 
 // Pooled partials for the t_rows of a frame list.
-void launch_pool_trows(const uint16_t* src, long long src_head_stride, int heads, const int* tr_first,
+template <typename T>
+void launch_pool_trows(const T* src, long long src_head_stride, int heads, const int* tr_first,
                        const int* tr_count, int ntr, const DevGeom& g, const int* slots, float* s0, float* s1,
                        long long part_head_stride, cudaStream_t s) {
   PoolGroups pg{};
@@ -425,7 +426,7 @@ void launch_pool_trows(const uint16_t* src, long long src_head_stride, int heads
   for (int i = 0; i < nf; ++i) sl.s[i] = slots ? slots[i] : i;
   dim3 grid(g.n_tiles, ntr, heads);
   const int threads = std::min(256, ((g.d + 31) / 32) * 32);
-  (void)launch_k(pool_partials_kernel, grid, dim3(threads), 0, s, src, src_head_stride, g.rows, g.cols, g.tiles_w,
+  (void)launch_k(pool_partials_kernel<T>, grid, dim3(threads), 0, s, src, src_head_stride, g.rows, g.cols, g.tiles_w,
                  g.n_tiles, g.d, pg, sl, s0, s1, part_head_stride, nullptr);
 }
 
@@ -686,7 +687,10 @@ int32_t fvsr_block_counts(const fvsr_grid* grid_q, const fvsr_grid* grid_k, int3
   return FVSR_OK;
 }
 
-int32_t fvsr_plan_sparse(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k, int32_t heads, int32_t d,
+}  // extern "C"
+namespace {
+template <typename T>
+int plan_sparse_impl(fvsr_ctx* ctx, const T* q, const T* k, int32_t heads, int32_t d,
                          const fvsr_grid* grid_q, const fvsr_grid* grid_k, const fvsr_mask* mask, int64_t topk,
                          int32_t cap, int32_t* sel, int32_t* sel_count, int32_t* diag, float* coarse,
                          uint8_t* allowed, fvsr_stream_t stream) {
@@ -719,6 +723,24 @@ int32_t fvsr_plan_sparse(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k, in
   FVSR_TRY(launch_select(ctx, g, dm, heads, qs0, qs1, (long long)g.nqf * g.n_tiles * d, ks0, ks1,
                          (long long)g.nkf * g.n_tiles * d, scale, topk, cap, sel, sel_count, diag, coarse, allowed, s));
   return after_launch(ctx, s, 4);
+}
+}  // namespace
+extern "C" {
+
+int32_t fvsr_plan_sparse(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k, int32_t heads, int32_t d,
+                         const fvsr_grid* grid_q, const fvsr_grid* grid_k, const fvsr_mask* mask, int64_t topk,
+                         int32_t cap, int32_t* sel, int32_t* sel_count, int32_t* diag, float* coarse,
+                         uint8_t* allowed, fvsr_stream_t stream) {
+  return plan_sparse_impl(ctx, q, k, heads, d, grid_q, grid_k, mask, topk, cap, sel, sel_count, diag, coarse, allowed,
+                          stream);
+}
+
+int32_t fvsr_plan_sparse_f32(fvsr_ctx* ctx, const float* q, const float* k, int32_t heads, int32_t d,
+                             const fvsr_grid* grid_q, const fvsr_grid* grid_k, const fvsr_mask* mask, int64_t topk,
+                             int32_t cap, int32_t* sel, int32_t* sel_count, int32_t* diag, float* coarse,
+                             uint8_t* allowed, fvsr_stream_t stream) {
+  return plan_sparse_impl(ctx, q, k, heads, d, grid_q, grid_k, mask, topk, cap, sel, sel_count, diag, coarse, allowed,
+                          stream);
 }
 
 int32_t fvsr_sparse_attention_exec(fvsr_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v,

@@ -71,7 +71,12 @@ struct PoolGroups {
   int ext_slot[kMaxFrames];  // count==1: slot of the partner frame's S0 in ext_s0, or -1
 };
 
-__global__ void __launch_bounds__(256) pool_partials_kernel(const uint16_t* __restrict__ src,
+// element loads of the pooling pass: bf16 bit patterns or fp32 (the reference's own inputs)
+__device__ __forceinline__ float load_elem(const uint16_t* p) { return __uint_as_float((uint32_t)*p << 16); }
+__device__ __forceinline__ float load_elem(const float* p) { return *p; }
+
+template <typename T>
+__global__ void __launch_bounds__(256) pool_partials_kernel(const T* __restrict__ src,
                                                             long long src_head_stride, int rows, int cols,
                                                             int tiles_w, int n_tiles, int d, PoolGroups groups,
                                                             SlotList slots, float* __restrict__ s0,
@@ -90,18 +95,17 @@ __global__ void __launch_bounds__(256) pool_partials_kernel(const uint16_t* __re
   const int es = groups.ext_slot[grp];
 
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    const uint16_t* base = src + head * src_head_stride + c;
+    const T* base = src + head * src_head_stride + c;
     // Sequential fp32 sum over one frame's tile rows in ascending token order, carried
     // in two accumulators: a0 (from 0.0f) and a1 (continued from `start`).
     auto frame_sum2 = [&](int f, float& a0, float& a1, bool two) {
-      const uint16_t* fb = base + (long long)f * N * d;
+      const T* fb = base + (long long)f * N * d;
 #pragma unroll 1
       for (int rh = 0; rh < hc; ++rh) {
-        const uint16_t* rowp = fb + ((long long)(8 * th + rh) * cols + 8 * tw) * d;
+        const T* rowp = fb + ((long long)(8 * th + rh) * cols + 8 * tw) * d;
         float v[8];
 #pragma unroll
-        for (int rw = 0; rw < 8; ++rw)
-          v[rw] = rw < wc ? __uint_as_float((uint32_t)rowp[(long long)rw * d] << 16) : 0.0f;
+        for (int rw = 0; rw < 8; ++rw) v[rw] = rw < wc ? load_elem(rowp + (long long)rw * d) : 0.0f;
 #pragma unroll
         for (int rw = 0; rw < 8; ++rw)
           if (rw < wc) {

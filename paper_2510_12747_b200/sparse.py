@@ -194,10 +194,10 @@ def _stream() -> C.c_void_p:
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _heads3(x: torch.Tensor, name: str) -> torch.Tensor:
+def _heads3(x: torch.Tensor, name: str, fp32_ok: bool = False) -> torch.Tensor:
     if not isinstance(x, torch.Tensor) or not x.is_cuda:
         raise ShapeError(f"{name}: CUDA tensor required")
-    if x.dtype != torch.bfloat16:
+    if x.dtype != torch.bfloat16 and not (fp32_ok and x.dtype == torch.float32):
         raise ShapeError(f"{name}: bf16 tensor required (got {x.dtype})")
     if x.dim() == 2:
         x = x.unsqueeze(0)
@@ -226,7 +226,7 @@ def plan_sparse(q: torch.Tensor, k: torch.Tensor, grid_q: TokenGrid, grid_k: Opt
     ctx = ctx or Context.default()
     grid_k = grid_k or grid_q
     mask = mask or Mask.all_allowed()
-    q3, k3 = _heads3(q, "plan_sparse q"), _heads3(k, "plan_sparse k")
+    q3, k3 = _heads3(q, "plan_sparse q", fp32_ok=True), _heads3(k, "plan_sparse k", fp32_ok=True)
     if q3.shape[0] != k3.shape[0] or q3.shape[2] != k3.shape[2]:
         raise ShapeError("plan_sparse: q/k dim mismatch")
     if q3.shape[1] != grid_q.token_count() or k3.shape[1] != grid_k.token_count():
@@ -247,10 +247,15 @@ def plan_sparse(q: torch.Tensor, k: torch.Tensor, grid_q: TokenGrid, grid_k: Opt
     gq, kq = grid_q.c()
     gk, kk = grid_k.c()
     md = mask.c()
-    check(ctx.lib.fvsr_plan_sparse(ctx.h, q3.data_ptr(), k3.data_ptr(), heads, d, C.byref(gq), C.byref(gk),
-                                   C.byref(md), int(topk), cap, sel.data_ptr(), cnt.data_ptr(), diag.data_ptr(),
-                                   coarse.data_ptr() if coarse is not None else None,
-                                   allowed.data_ptr() if allowed is not None else None, _stream()))
+    if q3.dtype != k3.dtype:
+        raise ShapeError("plan_sparse: q and k must have the same dtype")
+    # fp32 inputs (the reference's own) are pooled as they are: the plan is bit-exact with
+    # vsr::plan_sparse on any data; bf16 inputs are the streaming path's
+    fn = ctx.lib.fvsr_plan_sparse_f32 if q3.dtype == torch.float32 else ctx.lib.fvsr_plan_sparse
+    check(fn(ctx.h, q3.data_ptr(), k3.data_ptr(), heads, d, C.byref(gq), C.byref(gk),
+             C.byref(md), int(topk), cap, sel.data_ptr(), cnt.data_ptr(), diag.data_ptr(),
+             coarse.data_ptr() if coarse is not None else None,
+             allowed.data_ptr() if allowed is not None else None, _stream()))
     if check_errors:
         ctx.check_errors()
     return SparsePlan(int(topk), d, grid_q, grid_k, sel, cnt, diag, coarse, allowed, mask)

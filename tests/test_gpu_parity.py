@@ -194,3 +194,20 @@ def test_stream_768x1408_step_plan_and_exec():
     got = out[check_heads]
     assert rel_l2(got, ref) <= REL_L2_TOL, rel_l2(got, ref)
     assert max_abs(got, ref) <= MAX_ABS_TOL, max_abs(got, ref)
+
+
+def test_plan_from_fp32_inputs_bit_exact():
+    """fvsr_plan_sparse_f32: the reference's own fp32 inputs (not bf16-representable) pooled
+    as they are -> indices and coarse-score bits identical to the oracle on the same fp32."""
+    import torch
+    port = oracle.Port()
+    for (qf, kf, rows, cols, d, topk, mask) in [([1], [0, 1], 16, 16, 64, 2, M()),
+                                               ([5], [2, 3, 4, 5], 20, 28, 16, 3, M("loc", 7, 9, True)),
+                                               ([32], [28, 29, 30, 31, 32], 48, 88, 128, 27, M())]:
+        N = rows * cols
+        q = port.gaussian(91, len(qf) * N * d).reshape(1, len(qf) * N, d)
+        k = port.gaussian(92, len(kf) * N * d).reshape(1, len(kf) * N, d)
+        gq, gk = fv.TokenGrid(qf, rows, cols), fv.TokenGrid(kf, rows, cols)
+        plan = fv.plan_sparse(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), gq, gk, mask, topk)
+        refs = oracle_plans(q, k, qf, kf, rows, cols, to_oracle_mask(mask), topk)
+        _assert_plan_equal(plan, refs)
