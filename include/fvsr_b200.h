@@ -285,6 +285,13 @@ FVSR_API int32_t fvsr_ring_frame_mass(fvsr_ctx* ctx, fvsr_ring* ring, int32_t la
  * scored strategy: FVSR_E_CONFIG (kv_cache.cpp:112-113). */
 FVSR_API int32_t fvsr_ring_evict(fvsr_ring* ring, int32_t layer, int32_t strategy, const double* scores);
 
+/* Tile-major attention output -> token-major (the head-parallel gather's last step):
+ * tiles [units][64 * frames_per_unit][d] bf16 (FVSR_OUT_TILE_MAJOR, unit = head * (nq /
+ * frames_per_unit * tiles) + temporal row * tiles + tile) -> out [heads][nq * rows * cols][d];
+ * frames_per_unit 2 for paired query frames (2m, 2m+1).  DEVICE buffers, 16-byte aligned. */
+FVSR_API int32_t fvsr_untile(fvsr_ctx* ctx, const uint16_t* tiles, int64_t units, int32_t frames_per_unit, int32_t nq,
+                             int32_t rows, int32_t cols, int32_t d, uint16_t* out, fvsr_stream_t stream);
+
 /* One streaming layer-step from HOST buffers (the end-to-end path): H2D copy of the new
  * frame's q/k/v ([heads][rows*cols][d] bf16; pinned memory recommended), ring append,
  * sliding evict, attention, D2H copy of out.  Returns after enqueueing; the host output is

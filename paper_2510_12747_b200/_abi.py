@@ -109,6 +109,7 @@ SIGNATURES = {
     "fvsr_ring_frame_mass": (I32, [P, P, I32, C.POINTER(I32), I32, MP, P, P]),
     "fvsr_ring_evict": (I32, [P, I32, I32, P]),
     "fvsr_build_flags": (C.c_char_p, []),
+    "fvsr_untile": (I32, [P, P, I64, I32, I32, I32, I32, I32, P, P]),
     "fvsr_plan_sparse_f32": (I32, [P, P, P, I32, I32, GP, GP, MP, I64, I32, P, P, P, P, P, P]),
     "fvsr_ring_step": (I32, [P, P, I32, I32, P, P, P, C.POINTER(I32), I32, MP, I64, F32, I64, I64, P, I32, I32, P,
                              P, P]),

@@ -1506,6 +1506,24 @@ int32_t fvsr_build_causal_mask(fvsr_ctx* ctx, const int32_t* frame, int64_t L, i
   return launch_token_mask(ctx, frame, L, 1, lookahead, bits, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int32_t fvsr_untile(fvsr_ctx* ctx, const uint16_t* tiles, int64_t units, int32_t frames_per_unit, int32_t nq,
+                    int32_t rows, int32_t cols, int32_t d, uint16_t* out, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  if (!tiles || !out) return fail(FVSR_E_SHAPE, "untile: null tensor");
+  if (units < 0 || rows < 1 || cols < 1 || d < 8 || d % 8 || (frames_per_unit != 1 && frames_per_unit != 2) ||
+      nq < 1 || nq % frames_per_unit)
+    return fail(FVSR_E_CONFIG, "untile: bad geometry");
+  if ((reinterpret_cast<uintptr_t>(tiles) | reinterpret_cast<uintptr_t>(out)) % 16)
+    return fail(FVSR_E_CONFIG, "untile: buffers must be 16-byte aligned");
+  if (units == 0) return FVSR_OK;
+  int sms = 148;
+  (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  FVSR_CUDA(launch_k(untile_kernel, dim3(4 * sms), dim3(256), 0, s, tiles, (long long)units, (int)frames_per_unit,
+                     (int)nq, (int)rows, (int)cols, (int)d, out));
+  return after_launch(ctx, s, 1);
+}
+
 int32_t fvsr_ring_step_host(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* q_host,
                             const uint16_t* k_host, const uint16_t* v_host, const fvsr_mask* mask, int64_t topk,
                             float scale, uint16_t* out_host, fvsr_stream_t stream) {

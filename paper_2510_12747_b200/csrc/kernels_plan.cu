@@ -1126,3 +1126,35 @@ __global__ void __launch_bounds__(kMaskThreads) token_rows_copy_kernel(const int
 }
 
 }  // namespace fvsr
+
+namespace fvsr {
+// ---------------------------------------------------------------------------------------
+// Tile-major attention output ([unit][64 * fpu rows][d], the head-parallel shard layout) ->
+// token-major [heads][nq * rows * cols][d].  Unit u = head * (ntr * tiles) + trow * tiles +
+// tile; row r of a unit is frame trow * fpu + r / 64, tile row (r % 64) / 8, column r % 8.
+// One thread per 16-byte chunk; padding rows of ragged tiles are skipped.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) untile_kernel(const uint16_t* __restrict__ tiles, long long units, int fpu,
+                                                     int nq, int rows, int cols, int d,
+                                                     uint16_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int tw = (cols + 7) / 8, n_tiles = tw * ((rows + 7) / 8), ntr = nq / fpu;
+  const int chunks = d / 8, urows = 64 * fpu;
+  const long long total = units * urows * chunks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / chunks;
+    const int ch = (int)(i - row * chunks);
+    const long long u = row / urows;
+    const int r = (int)(row - u * urows);
+    const int head = (int)(u / (ntr * n_tiles));
+    const int rem = (int)(u - (long long)head * ntr * n_tiles);
+    const int trow = rem / n_tiles, tile = rem - trow * n_tiles;
+    const int f = trow * fpu + r / 64, rr = r % 64;
+    const int h = (tile / tw) * 8 + rr / 8, w = (tile % tw) * 8 + rr % 8;
+    if (h >= rows || w >= cols) continue;
+    const long long dst = ((long long)(head * nq + f) * rows * cols + (long long)h * cols + w) * d + ch * 8;
+    *reinterpret_cast<uint4*>(out + dst) = *reinterpret_cast<const uint4*>(tiles + row * d + ch * 8);
+  }
+}
+}  // namespace fvsr

@@ -133,3 +133,36 @@ def test_nccl_gather_world2():
     for p in procs:
         p.join(timeout=60)
     assert all(r[1] is True for r in res), res
+
+
+def test_cpp_head_parallel_layer_step():
+    """The host-stays-C++ head-parallel layer-step (integration/vsr_b200_parallel.hpp): world 1
+    through a real NCCL all-gather and simulated worlds 2, 4, 8 (one object per rank, shards
+    concatenated in rank order, fvsr_untile), six streaming steps with a locality window, each
+    bitwise equal to the unsharded fvsr_ring_step (integration/hp_main.cpp)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration", "_build",
+                       "hp_main")
+    if not os.path.exists(exe):
+        pytest.skip("integration/_build/hp_main not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("OK") == 4, r.stdout
+
+
+@pytest.mark.parametrize("qf", [[32], [32, 33]])
+def test_device_untile_matches_index_untile(qf):
+    """fvsr_untile (device) == head_parallel.untile (index gather) for single and paired query frames."""
+    import ctypes as C
+    heads, rows, cols, d = 3, 20, 28, 64
+    ntr, fpu = unit_space(qf)
+    tiles = ((rows + 7) // 8) * ((cols + 7) // 8)
+    units = heads * ntr * tiles
+    t = torch.randn(units, 64 * fpu, d, device="cuda").to(torch.bfloat16)
+    want = untile(t, heads, len(qf), rows, cols, frames_per_unit=fpu)
+    got = torch.zeros_like(want)
+    ctx = fv.Context.default()
+    fv._abi.check(ctx.lib.fvsr_untile(ctx.h, t.data_ptr(), units, fpu, len(qf), rows, cols, d, got.data_ptr(),
+                                      C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
