@@ -261,6 +261,26 @@ FVSR_API int32_t fvsr_ring_step(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer, i
                                 int64_t unit_end, uint16_t* out, int32_t out_layout, int32_t sel_cap, int32_t* sel,
                                 int32_t* sel_count, fvsr_stream_t stream);
 
+/* Strided tensor layout in elements: head h, token t of a tensor starts at
+ * h * head_stride + t * token_stride.  {0, 0} = [heads][tokens][d] (head_stride = tokens * d,
+ * token_stride = d); {d, heads * d} reads / writes a projection GEMM's [tokens][heads * d]
+ * matrix in place (no per-head split or transpose pass).  Strides are multiples of 8. */
+typedef struct {
+  int64_t head_stride;
+  int64_t token_stride;
+} fvsr_layout;
+
+/* fvsr_ring_step with strided K/V, Q and output layouts (token-major output, all units):
+ * the DiT block's K/V projection [tokens][2 * heads * d] feeds the ring append directly
+ * (make_frame_kv's per-head slice_cols + apply_rope, P/src/stream.cpp:134-152, fused into
+ * the append's gather), Q likewise, and the attention writes [tokens][heads * d] for the
+ * output projection (P/src/stream.cpp:252-259). */
+FVSR_API int32_t fvsr_ring_step_layout(fvsr_ctx* ctx, fvsr_ring* ring, int32_t layer, int32_t frame_id,
+                                       const uint16_t* k, const uint16_t* v, fvsr_layout kv_layout, const uint16_t* q,
+                                       fvsr_layout q_layout, const int32_t* q_frame_ids, int32_t nq,
+                                       const fvsr_mask* mask, int64_t topk, float scale, uint16_t* out,
+                                       fvsr_layout out_layout, fvsr_stream_t stream);
+
 /* ---- scored eviction ------------------------------------------------- */
 /* frame_attention_mass (P/src/kv_cache.cpp:170-206; declared P/include/vsr/kv_cache.hpp:79):
  * per head and key frame (grid_k order), the coarse-score softmax mass of every q-block
@@ -284,6 +304,11 @@ FVSR_API int32_t fvsr_ring_frame_mass(fvsr_ctx* ctx, fvsr_ring* ring, int32_t la
  * ring keeps head-identical sets), else FVSR_E_CONFIG.  NULL scores while over budget on a
  * scored strategy: FVSR_E_CONFIG (kv_cache.cpp:112-113). */
 FVSR_API int32_t fvsr_ring_evict(fvsr_ring* ring, int32_t layer, int32_t strategy, const double* scores);
+
+/* rms_norm (P/src/stream.cpp:86-99) of the DiT block: x fp32 [n][D] (DEVICE), gain fp32 [D],
+ * y = x / sqrt(mean(x^2) + 1e-6) * gain as bf16 [n][D] (the projection GEMMs' operand). */
+FVSR_API int32_t fvsr_rms_norm(fvsr_ctx* ctx, const float* x, const float* gain, int64_t n, int32_t D, uint16_t* y,
+                               fvsr_stream_t stream);
 
 /* Tile-major attention output -> token-major (the head-parallel gather's last step):
  * tiles [units][64 * frames_per_unit][d] bf16 (FVSR_OUT_TILE_MAJOR, unit = head * (nq /

@@ -78,6 +78,14 @@ I32, I64, F32 = C.c_int32, C.c_int64, C.c_float
 GP = C.POINTER(Grid)
 MP = C.POINTER(MaskDesc)
 
+
+class Layout(C.Structure):
+    """fvsr_layout: element strides of head h / token t (include/fvsr_b200.h); {0, 0} = [heads][L][d]."""
+    _fields_ = [("head_stride", C.c_int64), ("token_stride", C.c_int64)]
+
+
+LAYOUT = Layout
+
 # name -> (restype, argtypes); must list every symbol include/fvsr_b200.h declares
 SIGNATURES = {
     "fvsr_abi_version": (I32, []),
@@ -109,6 +117,9 @@ SIGNATURES = {
     "fvsr_ring_frame_mass": (I32, [P, P, I32, C.POINTER(I32), I32, MP, P, P]),
     "fvsr_ring_evict": (I32, [P, I32, I32, P]),
     "fvsr_build_flags": (C.c_char_p, []),
+    "fvsr_rms_norm": (I32, [P, P, P, I64, I32, P, P]),
+    "fvsr_ring_step_layout": (I32, [P, P, I32, I32, P, P, LAYOUT, P, LAYOUT, C.POINTER(I32), I32, MP, I64, F32, P,
+                                    LAYOUT, P]),
     "fvsr_untile": (I32, [P, P, I64, I32, I32, I32, I32, I32, P, P]),
     "fvsr_plan_sparse_f32": (I32, [P, P, P, I32, I32, GP, GP, MP, I64, I32, P, P, P, P, P, P]),
     "fvsr_ring_step": (I32, [P, P, I32, I32, P, P, P, C.POINTER(I32), I32, MP, I64, F32, I64, I64, P, I32, I32, P,

@@ -1069,6 +1069,7 @@ struct AppendSpec {
   const uint16_t* k;
   const uint16_t* v;
   int frame_id;
+  fvsr_layout kv;  // {0, 0}: [heads][rows * cols][d]
 };
 
 // Ring attention of one layer-step: mask builder (one launch: optional ring append of the
@@ -1076,7 +1077,8 @@ struct AppendSpec {
 int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, const int32_t* q_frame_ids, int nq,
                    const fvsr_mask* mask, int64_t topk, float scale, int64_t unit_begin, int64_t unit_end,
                    uint16_t* out, int out_layout, int sel_cap, int32_t* sel, int32_t* sel_count,
-                   const AppendSpec* app, cudaStream_t s) {
+                   const AppendSpec* app, cudaStream_t s, fvsr_layout q_lay = {0, 0},
+                   fvsr_layout out_lay = {0, 0}) {
   if (!r || !q || !out || !q_frame_ids) return fail(FVSR_E_SHAPE, "ring_attention: null argument");
   if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
   auto& c = r->ctx[layer];
@@ -1143,7 +1145,8 @@ int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
       PackPoolArgs& a = fa.kv;
       a.src = app->k;
       a.src2 = app->v;
-      a.src_head_stride = (long long)r->rows * r->cols * d;
+      a.src_head_stride = app->kv.head_stride ? app->kv.head_stride : (long long)r->rows * r->cols * d;
+      a.src_token_stride = app->kv.token_stride;
       a.dst = r->k_layer(layer);
       a.dst2 = r->v_layer(layer);
       a.dst_head_stride = r->kv_head_stride();
@@ -1169,7 +1172,8 @@ int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
     // one pass over Q: swizzled query tiles for the tensor cores + pooled partials for the plan
     PackPoolArgs& a = fa.q;
     a.src = q;
-    a.src_head_stride = Lq * d;
+    a.src_head_stride = q_lay.head_stride ? q_lay.head_stride : Lq * d;
+    a.src_token_stride = q_lay.token_stride;
     a.dst = qp;
     a.dst_head_stride = (long long)g.nqf * g.n_tiles * tb;
     a.s0 = qs0;
@@ -1272,7 +1276,8 @@ int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
   p.sel_count = use_cnt;
   p.cap = cap;
   p.out = out;
-  p.out_head_stride = Lq * d;
+  p.out_head_stride = out_lay.head_stride ? out_lay.head_stride : Lq * d;
+  p.out_token_stride = out_lay.token_stride;
   p.row_begin = 0;
   p.row_end = Lq;
   p.scale_log2 = scale * 1.4426950408889634f;
@@ -1306,9 +1311,24 @@ int32_t fvsr_ring_step(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame
                        uint16_t* out, int32_t out_layout, int32_t sel_cap, int32_t* sel, int32_t* sel_count,
                        fvsr_stream_t stream) {
   FVSR_TRY(check_ctx(ctx));
-  const AppendSpec app{k, v, frame_id};
+  const AppendSpec app{k, v, frame_id, {0, 0}};
   return ring_step_impl(ctx, r, layer, q, q_frame_ids, nq, mask, topk, scale, unit_begin, unit_end, out, out_layout,
                         sel_cap, sel, sel_count, &app, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int32_t fvsr_ring_step_layout(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* k,
+                              const uint16_t* v, fvsr_layout kv_layout, const uint16_t* q, fvsr_layout q_layout,
+                              const int32_t* q_frame_ids, int32_t nq, const fvsr_mask* mask, int64_t topk, float scale,
+                              uint16_t* out, fvsr_layout out_layout, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  if (!r) return fail(FVSR_E_SHAPE, "ring_step: null ring");
+  for (const fvsr_layout* l : {&kv_layout, &q_layout, &out_layout})
+    if (l->head_stride < 0 || l->token_stride < 0 || (l->token_stride && l->token_stride < r->d) ||
+        (l->token_stride * 2) % 16 || (l->head_stride * 2) % 16)
+      return fail(FVSR_E_CONFIG, "ring_step: layout strides must be >= d elements and 16-byte multiples");
+  const AppendSpec app{k, v, frame_id, kv_layout};
+  return ring_step_impl(ctx, r, layer, q, q_frame_ids, nq, mask, topk, scale, 0, -1, out, FVSR_OUT_TOKEN_MAJOR, 0,
+                        nullptr, nullptr, &app, reinterpret_cast<cudaStream_t>(stream), q_layout, out_layout);
 }
 
 // ---- scored eviction ------------------------------------------------------
@@ -1504,6 +1524,19 @@ int32_t fvsr_build_causal_mask(fvsr_ctx* ctx, const int32_t* frame, int64_t L, i
   for (long long i = 1; i < L; ++i)
     if (frame[i] < frame[i - 1]) return fail(FVSR_E_CONFIG, "build_causal_mask: frame indices must be non-decreasing");
   return launch_token_mask(ctx, frame, L, 1, lookahead, bits, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int32_t fvsr_rms_norm(fvsr_ctx* ctx, const float* x, const float* gain, int64_t n, int32_t D, uint16_t* y,
+                      fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  if (!x || !gain || !y) return fail(FVSR_E_SHAPE, "rms_norm: null tensor");
+  if (n < 0 || D < 4 || D % 4) return fail(FVSR_E_SHAPE, "rms_norm: D must be a positive multiple of 4");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(gain)) % 16 || reinterpret_cast<uintptr_t>(y) % 8)
+    return fail(FVSR_E_CONFIG, "rms_norm: misaligned buffers");
+  if (n == 0) return FVSR_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  FVSR_CUDA(launch_k(rms_norm_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, s, x, gain, (long long)n, (int)D, y));
+  return after_launch(ctx, s, 1);
 }
 
 int32_t fvsr_untile(fvsr_ctx* ctx, const uint16_t* tiles, int64_t units, int32_t frames_per_unit, int32_t nq,

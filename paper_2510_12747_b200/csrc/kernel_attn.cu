@@ -56,6 +56,7 @@ struct AttnParams {
   int cap;
   uint16_t* out;             // bf16 [heads][Lq][d] (token major) or [unit][NQ][d] (tile major)
   long long out_head_stride; // elements
+  long long out_token_stride;// elements between consecutive tokens of a head (token major; 0: D)
   long long row_begin, row_end;
   float scale_log2;          // scale * log2(e)
   int n_trows;               // q temporal rows handled by this launch
@@ -557,8 +558,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
         for (int idx = et; idx < NQ * kChunks; idx += 128) {
           const int col = idx / kChunks, ch = idx % kChunks, qc = col & 63;
           if (qh0 + (qc >> 3) >= g.rows || (qc & 7) >= cv) continue;
-          uint16_t* row = p.out_tile_major ? p.out + (u * NQ + col) * D
-                                           : p.out + head * p.out_head_stride + (row_tok(col >> 6, qc >> 3) + (qc & 7)) * D;
+          uint16_t* row = p.out_tile_major
+                              ? p.out + (u * NQ + col) * D
+                              : p.out + head * p.out_head_stride +
+                                    (row_tok(col >> 6, qc >> 3) + (qc & 7)) * (p.out_token_stride ? p.out_token_stride : D);
           *reinterpret_cast<uint4*>(row + ch * 8) = make_uint4(0, 0, 0, 0);
         }
         continue;
@@ -628,13 +631,19 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
           if (p.out_tile_major) {
             bulk_s2g(p.out + (u * NQ + c0) * D, stage, kEC * D * 2);
           } else {
-            // the chunk's tile rows: cv consecutive tokens each
+            // the chunk's tile rows: cv consecutive tokens each (one copy per row when the
+            // tokens are contiguous, else one per token)
+            const long long ots = p.out_token_stride ? p.out_token_stride : D;
 #pragma unroll 1
             for (int r0 = c0; r0 < c0 + kEC; r0 += 8) {
               const int qc = r0 & 63;
-              if (qh0 + (qc >> 3) < g.rows)
-                bulk_s2g(p.out + head * p.out_head_stride + row_tok(r0 >> 6, qc >> 3) * D, stage + (r0 - c0) * D,
-                         cv * D * 2);
+              if (qh0 + (qc >> 3) >= g.rows) continue;
+              uint16_t* dst = p.out + head * p.out_head_stride + row_tok(r0 >> 6, qc >> 3) * ots;
+              if (ots == D) {
+                bulk_s2g(dst, stage + (r0 - c0) * D, cv * D * 2);
+              } else {
+                for (int w = 0; w < cv; ++w) bulk_s2g(dst + w * ots, stage + (r0 - c0 + w) * D, D * 2);
+              }
             }
           }
           bulk_commit();

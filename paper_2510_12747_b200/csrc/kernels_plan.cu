@@ -149,6 +149,8 @@ struct PackPoolArgs {
   const uint16_t* src;   // pooled + packed, [heads][frames * rows * cols][d]
   const uint16_t* src2;  // packed only (may be null)
   long long src_head_stride;  // elements (both sources)
+  long long src_token_stride; // elements between consecutive tokens (0: d, i.e. [heads][L][d]);
+                              // D = heads * d reads a projection GEMM's [L][D] output in place
   uint8_t* dst;
   uint8_t* dst2;
   long long dst_head_stride;  // bytes
@@ -220,12 +222,18 @@ __device__ __forceinline__ void pack_pool_body(const PackPoolArgs& a, const Pool
     fence_proxy_async_smem();
     const uint32_t row_bytes = (uint32_t)wc * d * 2;
     mbar_arrive_expect_tx(bar, row_bytes * hc * cnt * nt);
+    const long long ts = a.src_token_stride ? a.src_token_stride : d;
     for (int fi = 0; fi < cnt; ++fi)
       for (int t = 0; t < nt; ++t) {
-        const uint16_t* src = (t == 0 ? a.src : a.src2) + head * a.src_head_stride + (long long)(f0 + fi) * N * d;
+        const uint16_t* src = (t == 0 ? a.src : a.src2) + head * a.src_head_stride + (long long)(f0 + fi) * N * ts;
         for (int rh = 0; rh < hc; ++rh) {
           const long long tok = (long long)(8 * th + rh) * a.cols + 8 * tw;
-          bulk_g2s(stage(fi, t) + rh * 8 * d * 2, src + tok * d, row_bytes, bar);
+          if (ts == d) {  // a tile row is contiguous
+            bulk_g2s(stage(fi, t) + rh * 8 * d * 2, src + tok * d, row_bytes, bar);
+          } else {        // one copy per token (its d channels are contiguous)
+            for (int rw = 0; rw < wc; ++rw)
+              bulk_g2s(stage(fi, t) + (rh * 8 + rw) * d * 2, src + (tok + rw) * ts, (uint32_t)d * 2, bar);
+          }
         }
       }
   }
@@ -1155,6 +1163,43 @@ __global__ void __launch_bounds__(256) untile_kernel(const uint16_t* __restrict_
     if (h >= rows || w >= cols) continue;
     const long long dst = ((long long)(head * nq + f) * rows * cols + (long long)h * cols + w) * d + ch * 8;
     *reinterpret_cast<uint4*>(out + dst) = *reinterpret_cast<const uint4*>(tiles + row * d + ch * 8);
+  }
+}
+}  // namespace fvsr
+
+namespace fvsr {
+// ---------------------------------------------------------------------------------------
+// rms_norm (P/src/stream.cpp:86-99): y = x * 1/sqrt(mean(x^2) + 1e-6) * gain, one warp per
+// token row: fp32 residual stream in, bf16 out (the projection GEMMs' operand).  The sum of
+// squares is an fp32 warp tree (the reference sums in double; the difference is far below
+// the bf16 rounding of y).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) rms_norm_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                                                       long long n, int D, uint16_t* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const long long row = blockIdx.x * 8ll + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * D);
+  float acc = 0.0f;
+  for (int c = lane; c < D / 4; c += 32) {
+    const float4 v = xr[c];
+    acc = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, acc))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  const float inv = (float)(1.0 / sqrt((double)acc / (double)D + 1e-6));
+  const float4* gr = reinterpret_cast<const float4*>(gain);
+  uint2* yr = reinterpret_cast<uint2*>(y + row * D);
+  for (int c = lane; c < D / 4; c += 32) {
+    const float4 v = xr[c], g = gr[c];
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x * inv * g.x, v.y * inv * g.y);
+    const __nv_bfloat162 b = __floats2bfloat162_rn(v.z * inv * g.z, v.w * inv * g.w);
+    uint2 w;
+    w.x = *reinterpret_cast<const uint32_t*>(&a);
+    w.y = *reinterpret_cast<const uint32_t*>(&b);
+    yr[c] = w;
   }
 }
 }  // namespace fvsr
