@@ -236,6 +236,10 @@ FVSR_API int32_t fvsr_ring_evict_keep(fvsr_ring* ring, int32_t layer, int32_t ke
 /* KVCache::frame_ids (identical for every head under sliding eviction). */
 FVSR_API int32_t fvsr_ring_frame_ids(const fvsr_ring* ring, int32_t layer, int32_t* ids, int32_t cap,
                             int32_t* n);
+/* The frame ids head `head` of `layer` retains (head-wise eviction lets heads diverge;
+ * fvsr_ring_frame_ids reports head 0). */
+FVSR_API int32_t fvsr_ring_frame_ids_head(const fvsr_ring* ring, int32_t layer, int32_t head, int32_t* ids,
+                                          int32_t cap, int32_t* n);
 
 /* head_attention for heads [0, heads) of `layer`: queries of frames q_frame_ids (usually
  * the current frame) against the ring's context.  q is [heads][nq*rows*cols][d] (DEVICE),
@@ -300,9 +304,11 @@ FVSR_API int32_t fvsr_ring_frame_mass(fvsr_ctx* ctx, fvsr_ring* ring, int32_t la
 /* KVCache::evict (P/src/kv_cache.cpp:97-137): FVSR_EVICT_SLIDING ignores scores;
  * FVSR_EVICT_UNIFORM sums HOST scores [heads][n] (aligned with fvsr_ring_frame_ids) over heads
  * and drops the lowest-scored non-newest frames (older first on ties) from every head.
- * FVSR_EVICT_HEAD_WISE is accepted only when every head picks the same victims (the device
- * ring keeps head-identical sets), else FVSR_E_CONFIG.  NULL scores while over budget on a
- * scored strategy: FVSR_E_CONFIG (kv_cache.cpp:112-113). */
+ * FVSR_EVICT_HEAD_WISE drops each head's own lowest-scored frames, so the heads' retained sets
+ * may diverge (each (layer, head) has its own frame table; later steps run one launch per run
+ * of heads with identical sets).  FVSR_EVICT_UNIFORM on diverged sets: FVSR_E_INVARIANT
+ * (kv_cache.cpp:119-122).  NULL scores while over budget on a scored strategy: FVSR_E_CONFIG
+ * (kv_cache.cpp:112-113). */
 FVSR_API int32_t fvsr_ring_evict(fvsr_ring* ring, int32_t layer, int32_t strategy, const double* scores);
 
 /* rms_norm (P/src/stream.cpp:86-99) of the DiT block: x fp32 [n][D] (DEVICE), gain fp32 [D],

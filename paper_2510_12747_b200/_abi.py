@@ -117,6 +117,7 @@ SIGNATURES = {
     "fvsr_ring_frame_mass": (I32, [P, P, I32, C.POINTER(I32), I32, MP, P, P]),
     "fvsr_ring_evict": (I32, [P, I32, I32, P]),
     "fvsr_build_flags": (C.c_char_p, []),
+    "fvsr_ring_frame_ids_head": (I32, [P, I32, I32, C.POINTER(I32), I32, C.POINTER(I32)]),
     "fvsr_rms_norm": (I32, [P, P, P, I64, I32, P, P]),
     "fvsr_ring_step_layout": (I32, [P, P, I32, I32, P, P, LAYOUT, P, LAYOUT, C.POINTER(I32), I32, MP, I64, F32, P,
                                     LAYOUT, P]),

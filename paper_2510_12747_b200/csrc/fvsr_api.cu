@@ -92,6 +92,12 @@ struct fvsr_ctx {
   size_t scores_cap = 0;
   // shape of the scores the last two-kernel selection left in d_scores (fvsr_ring_frame_mass)
   int scores_heads = 0, scores_bnq = 0, scores_bnk = 0;
+  // the last ring step's runs of heads with identical frame tables and their score slices
+  struct ScoreRun {
+    int h0, h1, bnq, bnk;
+    size_t off;  // floats into d_scores
+  };
+  std::vector<ScoreRun> score_runs;
   // which ring attention call produced d_scores (fvsr_ring_frame_mass refuses any other):
   // ring, layer, the layer's frame-set generation, query frame ids and the mask descriptor
   struct ScoreStamp {
@@ -128,18 +134,87 @@ struct fvsr_ring {
   float2* rope_h = nullptr;  // [rows][split1/2]
   float2* rope_w = nullptr;  // [cols][split2/2]
   int rope_t_cap = 0;
-  std::vector<std::vector<std::pair<int, int>>> ctx;  // per layer: (frame_id, slot), ascending
-  std::vector<std::vector<char>> used;                // per layer: slot occupancy
+  // Frame tables.  KVCache keeps one list of frames per (layer, head) (P/include/vsr/
+  // kv_cache.hpp:72); head-wise eviction lets the heads of a layer diverge.  The owning ring
+  // keeps htab/hused per (layer, head); every operation runs on VIEWS, one per run of
+  // consecutive heads with identical tables (one view for all heads unless they diverged):
+  // a view is a shallow copy whose heads are [head0, head0 + heads) of the heads_total
+  // stored heads and whose ctx[layer] / used[layer] are the run's table.
+  using Table = std::vector<std::pair<int, int>>;     // (frame_id, slot), ascending ids
+  std::vector<std::vector<Table>> htab;               // owning ring: [layer][head]
+  std::vector<std::vector<std::vector<char>>> hused;  // owning ring: [layer][head][slot] occupancy
+  std::vector<Table> ctx;                             // view: [layer] the run's table
+  std::vector<std::vector<char>> used;                // view: [layer] the run's slot occupancy
   std::vector<unsigned long long> gen;                // per layer: bumped on every append / evict
+  int head0 = 0, heads_total = 0;
   long long kv_head_stride() const { return (long long)slots * n_tiles * (long long)tile_bytes; }
   long long part_head_stride() const { return (long long)slots * n_tiles * d; }
-  uint8_t* k_layer(int l) const { return k + (long long)l * heads * kv_head_stride(); }
-  uint8_t* v_layer(int l) const { return v + (long long)l * heads * kv_head_stride(); }
-  float* s0_layer(int l) const { return s0 + (long long)l * heads * part_head_stride(); }
-  float* s1_layer(int l) const { return s1 + (long long)l * heads * part_head_stride(); }
+  long long hbase(int l) const { return (long long)l * heads_total + head0; }
+  uint8_t* k_layer(int l) const { return k + hbase(l) * kv_head_stride(); }
+  uint8_t* v_layer(int l) const { return v + hbase(l) * kv_head_stride(); }
+  float* s0_layer(int l) const { return s0 + hbase(l) * part_head_stride(); }
+  float* s1_layer(int l) const { return s1 + hbase(l) * part_head_stride(); }
   long long kn2_head_stride() const { return (long long)slots * n_tiles; }
-  float* kn2_layer(int l) const { return kn2 + (long long)l * heads * kn2_head_stride(); }
+  float* kn2_layer(int l) const { return kn2 + hbase(l) * kn2_head_stride(); }
 };
+
+namespace {
+// runs [h0, h1) of consecutive heads of `layer` with identical frame tables
+std::vector<std::pair<int, int>> head_runs(const fvsr_ring* r, int layer) {
+  std::vector<std::pair<int, int>> out;
+  const auto& t = r->htab[layer];
+  int h0 = 0;
+  for (int h = 1; h <= r->heads; ++h)
+    if (h == r->heads || t[h] != t[h0]) {
+      out.emplace_back(h0, h);
+      h0 = h;
+    }
+  return out;
+}
+// view of heads [h0, h1) at `layer` (see fvsr_ring)
+fvsr_ring ring_view(const fvsr_ring* r, int layer, int h0, int h1) {
+  fvsr_ring v;
+  v.layers = r->layers;
+  v.heads = h1 - h0;
+  v.d = r->d;
+  v.rows = r->rows;
+  v.cols = r->cols;
+  v.window = r->window;
+  v.slots = r->slots;
+  v.tiles_w = r->tiles_w;
+  v.tiles_h = r->tiles_h;
+  v.n_tiles = r->n_tiles;
+  v.tile_bytes = r->tile_bytes;
+  v.k = r->k;
+  v.v = r->v;
+  v.s0 = r->s0;
+  v.s1 = r->s1;
+  v.kn2 = r->kn2;
+  v.rope = r->rope;
+  v.rope_theta0 = r->rope_theta0;
+  for (int i = 0; i < 3; ++i) v.rope_split[i] = r->rope_split[i];
+  v.rope_t = r->rope_t;
+  v.rope_h = r->rope_h;
+  v.rope_w = r->rope_w;
+  v.rope_t_cap = r->rope_t_cap;
+  v.ctx.assign(r->layers, {});
+  v.used.assign(r->layers, {});
+  v.ctx[layer] = r->htab[layer][h0];
+  v.used[layer] = r->hused[layer][h0];
+  v.gen = r->gen;
+  v.head0 = r->head0 + h0;
+  v.heads_total = r->heads_total;
+  return v;
+}
+// the view's table changes -> every head of its run
+void ring_commit(fvsr_ring* r, const fvsr_ring& v, int layer, int h0, int h1) {
+  for (int h = h0; h < h1; ++h) {
+    r->htab[layer][h] = v.ctx[layer];
+    r->hused[layer][h] = v.used[layer];
+  }
+  r->gen[layer] = std::max(r->gen[layer], v.gen[layer]);
+}
+}  // namespace
 
 namespace {
 
@@ -857,9 +932,10 @@ int32_t fvsr_ring_create(fvsr_ctx* ctx, int32_t layers, int32_t heads, int32_t d
     fvsr_ring_destroy(r);
     return fail(FVSR_E_NOMEM, "ring allocation of %zu bytes failed", 2 * kvb + 2 * pb);
   }
-  r->ctx.assign(layers, {});
-  r->used.assign(layers, std::vector<char>(r->slots, 0));
+  r->htab.assign(layers, std::vector<fvsr_ring::Table>(heads));
+  r->hused.assign(layers, std::vector<std::vector<char>>(heads, std::vector<char>(r->slots, 0)));
   r->gen.assign(layers, 0);
+  r->heads_total = heads;
   *out = r;
   return FVSR_OK;
 }
@@ -966,13 +1042,11 @@ int32_t fvsr_ring_set_rope(fvsr_ring* r, double theta0, const int32_t* axis_spli
   return rope_reserve_t(r, 1);
 }
 
-int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* k,
-                         const uint16_t* v, fvsr_stream_t stream) {
-  FVSR_TRY(check_ctx(ctx));
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (!r || !k || !v) return fail(FVSR_E_SHAPE, "ring_append: null argument");
-  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer/head out of range");
-  if (frame_id < 0) return fail(FVSR_E_CONFIG, "TokenGrid: negative frame id");
+}  // extern "C"
+namespace {
+// KVCache::append of one run of heads (a view; k, v point at its first head)
+int ring_append_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, int frame_id, const uint16_t* k, const uint16_t* v,
+                     cudaStream_t s) {
   auto& c = r->ctx[layer];
   if (!c.empty() && frame_id <= c.back().first)
     return fail(FVSR_E_INVARIANT, "KVCache: frame ids must increase");  // kv_cache.cpp:42
@@ -1023,17 +1097,40 @@ int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t fra
   r->used[layer][slot] = 1;
   c.emplace_back(frame_id, slot);
   ++r->gen[layer];
-  return after_launch(ctx, s, 1);
+  return FVSR_OK;
+}
+}  // namespace
+extern "C" {
+
+int32_t fvsr_ring_append(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, int32_t frame_id, const uint16_t* k,
+                         const uint16_t* v, fvsr_stream_t stream) {
+  FVSR_TRY(check_ctx(ctx));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!r || !k || !v) return fail(FVSR_E_SHAPE, "ring_append: null argument");
+  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer/head out of range");
+  if (frame_id < 0) return fail(FVSR_E_CONFIG, "TokenGrid: negative frame id");
+  if (r->rope) FVSR_TRY(rope_reserve_t(r, frame_id + 1));  // views never grow the shared table
+  const long long hs = (long long)r->rows * r->cols * r->d;
+  int launches = 0;
+  for (auto [h0, h1] : head_runs(r, layer)) {
+    fvsr_ring v_ = ring_view(r, layer, h0, h1);
+    FVSR_TRY(ring_append_view(ctx, &v_, layer, frame_id, k + h0 * hs, v + h0 * hs, s));
+    ring_commit(r, v_, layer, h0, h1);
+    ++launches;
+  }
+  return after_launch(ctx, s, launches);
 }
 
 int32_t fvsr_ring_evict_sliding(fvsr_ring* r, int32_t layer) {
   if (!r) return fail(FVSR_E_CONFIG, "null ring");
   if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
-  auto& c = r->ctx[layer];
-  while ((int)c.size() > r->window) {  // kv_cache.cpp:100-106
-    r->used[layer][c.front().second] = 0;
-    c.erase(c.begin());
-    ++r->gen[layer];
+  for (int h = 0; h < r->heads; ++h) {
+    auto& c = r->htab[layer][h];
+    while ((int)c.size() > r->window) {  // kv_cache.cpp:100-106
+      r->hused[layer][h][c.front().second] = 0;
+      c.erase(c.begin());
+      ++r->gen[layer];
+    }
   }
   return FVSR_OK;
 }
@@ -1042,19 +1139,27 @@ int32_t fvsr_ring_evict_keep(fvsr_ring* r, int32_t layer, int32_t keep) {
   if (!r) return fail(FVSR_E_CONFIG, "null ring");
   if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
   if (keep < 0) return fail(FVSR_E_CONFIG, "ring_evict_keep: keep must be >= 0");
-  auto& c = r->ctx[layer];
-  while ((int)c.size() > keep) {  // sliding: oldest first (kv_cache.cpp:100-106)
-    r->used[layer][c.front().second] = 0;
-    c.erase(c.begin());
-    ++r->gen[layer];
+  for (int h = 0; h < r->heads; ++h) {
+    auto& c = r->htab[layer][h];
+    while ((int)c.size() > keep) {  // sliding: oldest first (kv_cache.cpp:100-106)
+      r->hused[layer][h][c.front().second] = 0;
+      c.erase(c.begin());
+      ++r->gen[layer];
+    }
   }
   return FVSR_OK;
 }
 
 int32_t fvsr_ring_frame_ids(const fvsr_ring* r, int32_t layer, int32_t* ids, int32_t cap, int32_t* n) {
+  return fvsr_ring_frame_ids_head(r, layer, 0, ids, cap, n);
+}
+
+int32_t fvsr_ring_frame_ids_head(const fvsr_ring* r, int32_t layer, int32_t head, int32_t* ids, int32_t cap,
+                                 int32_t* n) {
   if (!r) return fail(FVSR_E_CONFIG, "null ring");
-  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
-  const auto& c = r->ctx[layer];
+  if (layer < 0 || layer >= r->layers || head < 0 || head >= r->heads)
+    return fail(FVSR_E_SHAPE, "KVCache: layer/head out of range");
+  const auto& c = r->htab[layer][head];
   if (n) *n = (int32_t)c.size();
   if ((int)c.size() > cap) return fail(FVSR_E_SHAPE, "frame id buffer too small");
   for (size_t i = 0; i < c.size(); ++i) ids[i] = c[i].first;
@@ -1074,11 +1179,10 @@ struct AppendSpec {
 
 // Ring attention of one layer-step: mask builder (one launch: optional ring append of the
 // new frame, Q pack + pool, coarse scores, top-k) then the sparse attention kernel.
-int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, const int32_t* q_frame_ids, int nq,
+int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, const int32_t* q_frame_ids, int nq,
                    const fvsr_mask* mask, int64_t topk, float scale, int64_t unit_begin, int64_t unit_end,
                    uint16_t* out, int out_layout, int sel_cap, int32_t* sel, int32_t* sel_count,
-                   const AppendSpec* app, cudaStream_t s, fvsr_layout q_lay = {0, 0},
-                   fvsr_layout out_lay = {0, 0}) {
+                   const AppendSpec* app, cudaStream_t s, fvsr_layout q_lay, fvsr_layout out_lay, float* coarse_out) {
   if (!r || !q || !out || !q_frame_ids) return fail(FVSR_E_SHAPE, "ring_attention: null argument");
   if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
   auto& c = r->ctx[layer];
@@ -1135,8 +1239,6 @@ int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
   float* qn2 = cv.take<float>(qn);
   int* use_sel = sel ? sel : wsel;
   int* use_cnt = sel_count ? sel_count : wcnt;
-  const size_t n_scores = (size_t)r->heads * g.bnq * g.bnk;
-  if (ctx_reserve_scores(ctx, n_scores) != FVSR_OK) return FVSR_E_CUDA;
   {
     SpanGuard sg(ctx, s, app ? FVSR_TIME_FRONT : FVSR_TIME_MASK_BUILDER);
     FrontArgs fa{};
@@ -1213,7 +1315,7 @@ int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
     p.npow2 = npow2(g.bnk);
     p.sel = use_sel;
     p.sel_count = use_cnt;
-    p.coarse = ctx->d_scores;  // kept for fvsr_ring_frame_mass
+    p.coarse = coarse_out;  // kept for fvsr_ring_frame_mass
     p.err = ctx->d_err;
     const size_t rope_bytes =
         r->rope ? (size_t)(2 * (r->rope_split[0] / 2) + 8 * (r->rope_split[1] / 2) + 8 * (r->rope_split[2] / 2)) *
@@ -1240,27 +1342,19 @@ int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
       ctx->launches += 2;
     } else {  // score rows too long for shared memory: scores through L2, then the row selector
       FVSR_TRY(launch_select(ctx, g, dm, r->heads, qs0, qs1, p.q_head_stride, p.k_s0, p.k_s1, p.k_head_stride, p.scale,
-                             topk, cap, use_sel, use_cnt, nullptr, ctx->d_scores, nullptr, s));
+                             topk, cap, use_sel, use_cnt, nullptr, coarse_out, nullptr, s));
       ctx->launches += 3;
     }
     if (ctx->flags & FVSR_FLAG_SYNC_CHECK) {  // debugging: attribute a fault to the front launches
       const cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) return fail(FVSR_E_CUDA, "ring front kernels: %s", cudaGetErrorString(e));
     }
-    ctx->scores_heads = r->heads;
-    ctx->scores_bnq = g.bnq;
-    ctx->scores_bnk = g.bnk;
   }
   if (app) {  // the new frame is in the ring from here on
     r->used[layer][app_slot] = 1;
     c.emplace_back(app->frame_id, app_slot);
     ++r->gen[layer];
   }
-  ctx->stamp.ring = r;
-  ctx->stamp.layer = layer;
-  ctx->stamp.gen = r->gen[layer];
-  ctx->stamp.qids.assign(q_frame_ids, q_frame_ids + nq);
-  ctx->stamp.mask = mask ? *mask : fvsr_mask{};
   const long long units_total = (long long)r->heads * g.nq_trows * g.n_tiles;
   if (unit_end < 0 || unit_end > units_total) unit_end = units_total;
   if (unit_begin < 0 || unit_begin > unit_end) return fail(FVSR_E_CONFIG, "ring_attention: bad unit range");
@@ -1291,6 +1385,79 @@ int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
   p.qn2_head_stride = (long long)g.nqf * g.n_tiles;
   FVSR_TRY(launch_attention(ctx, g, dm, p, r->heads, unit_begin, unit_end, s));
   return after_launch(ctx, s, 0);
+}
+
+// One layer-step over every run of heads with identical frame tables (one run unless
+// head-wise eviction made the heads diverge; unit ranges / tile-major output need one run).
+int ring_step_impl(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, const int32_t* q_frame_ids, int nq,
+                   const fvsr_mask* mask, int64_t topk, float scale, int64_t unit_begin, int64_t unit_end,
+                   uint16_t* out, int out_layout, int sel_cap, int32_t* sel, int32_t* sel_count,
+                   const AppendSpec* app, cudaStream_t s, fvsr_layout q_lay = {0, 0},
+                   fvsr_layout out_lay = {0, 0}) {
+  if (!r || !q || !out || !q_frame_ids || nq < 1) return fail(FVSR_E_SHAPE, "ring_attention: null argument");
+  if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
+  if (r->rope) {  // views never grow the shared RoPE table
+    int mx = app ? app->frame_id : 0;
+    for (int i = 0; i < nq; ++i) mx = std::max(mx, (int)q_frame_ids[i]);
+    if (mx >= 0) FVSR_TRY(rope_reserve_t(r, mx + 1));
+  }
+  const auto runs = head_runs(r, layer);
+  if (runs.size() > 1 && (unit_begin != 0 || unit_end >= 0 || out_layout == FVSR_OUT_TILE_MAJOR))
+    return fail(FVSR_E_CONFIG,
+                "ring_attention: the heads' frame sets diverge (head-wise eviction): unit ranges and tile-major "
+                "output (head-parallel shards) need head-identical sets");
+  // coarse-score slices of the runs (fvsr_ring_frame_mass reads them back)
+  std::vector<fvsr_ctx::ScoreRun> sr;
+  size_t total = 0;
+  for (auto [h0, h1] : runs) {
+    std::vector<int> kids;
+    for (auto& fs : r->htab[layer][h0]) kids.push_back(fs.first);
+    if (app) kids.push_back(app->frame_id);
+    int bnq = 0, bnk = 0;
+    if (!kids.empty()) {
+      fvsr_grid gq{q_frame_ids, nq, r->rows, r->cols};
+      fvsr_grid gk{kids.data(), (int)kids.size(), r->rows, r->cols};
+      DevGeom g;
+      if (build_geom(&gq, &gk, r->d, nullptr, g) == FVSR_OK) {
+        bnq = g.bnq;
+        bnk = g.bnk;
+      }
+    }
+    sr.push_back({h0, h1, bnq, bnk, total});
+    total += (size_t)(h1 - h0) * bnq * bnk;
+  }
+  if (ctx_reserve_scores(ctx, std::max<size_t>(1, total)) != FVSR_OK) return FVSR_E_CUDA;
+  ctx->score_runs.clear();
+  ctx->scores_heads = ctx->scores_bnq = ctx->scores_bnk = 0;
+  const long long Lq = (long long)nq * r->rows * r->cols;
+  const long long qhs = q_lay.head_stride ? q_lay.head_stride : Lq * r->d;
+  const long long ohs = out_lay.head_stride ? out_lay.head_stride : Lq * r->d;
+  for (const auto& run : sr) {
+    fvsr_ring v = ring_view(r, layer, run.h0, run.h1);
+    AppendSpec a{};
+    if (app) {
+      const long long khs = app->kv.head_stride ? app->kv.head_stride : (long long)r->rows * r->cols * r->d;
+      a = *app;
+      a.k += run.h0 * khs;
+      a.v += run.h0 * khs;
+    }
+    FVSR_TRY(ring_step_view(ctx, &v, layer, q + run.h0 * qhs, q_frame_ids, nq, mask, topk, scale, unit_begin,
+                            unit_end, out_layout == FVSR_OUT_TILE_MAJOR ? out : out + run.h0 * ohs, out_layout,
+                            sel_cap, sel ? sel + (long long)run.h0 * run.bnq * sel_cap : nullptr,
+                            sel_count ? sel_count + (long long)run.h0 * run.bnq : nullptr, app ? &a : nullptr, s,
+                            q_lay, out_lay, ctx->d_scores + run.off));
+    ring_commit(r, v, layer, run.h0, run.h1);
+  }
+  ctx->score_runs = sr;
+  ctx->scores_heads = r->heads;
+  ctx->scores_bnq = sr.empty() ? 0 : sr[0].bnq;
+  ctx->scores_bnk = sr.empty() ? 0 : sr[0].bnk;
+  ctx->stamp.ring = r;
+  ctx->stamp.layer = layer;
+  ctx->stamp.gen = r->gen[layer];
+  ctx->stamp.qids.assign(q_frame_ids, q_frame_ids + nq);
+  ctx->stamp.mask = mask ? *mask : fvsr_mask{};
+  return FVSR_OK;
 }
 }  // namespace
 
@@ -1392,31 +1559,37 @@ int32_t fvsr_ring_frame_mass(fvsr_ctx* ctx, fvsr_ring* r, int32_t layer, const i
   FVSR_TRY(check_ctx(ctx));
   if (!r || !q_frame_ids) return fail(FVSR_E_SHAPE, "ring_frame_mass: null argument");
   if (layer < 0 || layer >= r->layers) return fail(FVSR_E_SHAPE, "KVCache: layer out of range");
-  const auto& c = r->ctx[layer];
-  if (c.empty()) return fail(FVSR_E_CONFIG, "ring_frame_mass: empty context");
-  if (!mass) return fail(FVSR_E_SHAPE, "ring_frame_mass: null output");
-  std::vector<int> kids, kslots;
-  for (auto& fs : c) {
-    kids.push_back(fs.first);
-    kslots.push_back(fs.second);
-  }
-  fvsr_grid gq{q_frame_ids, nq, r->rows, r->cols};
-  fvsr_grid gk{kids.data(), (int)kids.size(), r->rows, r->cols};
-  DevGeom g;
-  FVSR_TRY(build_geom(&gq, &gk, r->d, kslots.data(), g));
-  DevMask dm;
-  FVSR_TRY(build_mask(mask, g, grid_tokens(&gk), dm));
   fvsr_ctx::ScoreStamp want;
   want.ring = r;
   want.layer = layer;
   want.gen = r->gen[layer];
   want.qids.assign(q_frame_ids, q_frame_ids + nq);
   want.mask = mask ? *mask : fvsr_mask{};
-  if (ctx->scores_heads != r->heads || ctx->scores_bnq != g.bnq || ctx->scores_bnk != g.bnk || !(ctx->stamp == want))
+  if (ctx->scores_heads != r->heads || ctx->score_runs.empty() || !(ctx->stamp == want))
     return fail(FVSR_E_CONFIG,
                 "ring_frame_mass: the coarse scores on the context are not those of this ring, layer, frame set, "
                 "query frames and mask (call right after fvsr_ring_attention of the same layer, before evicting)");
-  return launch_frame_mass(ctx, g, dm, r->heads, ctx->d_scores, mass, reinterpret_cast<cudaStream_t>(stream));
+  if (!mass) return fail(FVSR_E_SHAPE, "ring_frame_mass: null output");
+  // per run of heads with identical frame tables: its geometry, its score slice, its rows of mass
+  for (const auto& run : ctx->score_runs) {
+    const auto& c = r->htab[layer][run.h0];
+    if (c.empty()) return fail(FVSR_E_CONFIG, "ring_frame_mass: empty context");
+    std::vector<int> kids, kslots;
+    for (auto& fs : c) {
+      kids.push_back(fs.first);
+      kslots.push_back(fs.second);
+    }
+    fvsr_grid gq{q_frame_ids, nq, r->rows, r->cols};
+    fvsr_grid gk{kids.data(), (int)kids.size(), r->rows, r->cols};
+    DevGeom g;
+    FVSR_TRY(build_geom(&gq, &gk, r->d, kslots.data(), g));
+    DevMask dm;
+    FVSR_TRY(build_mask(mask, g, grid_tokens(&gk), dm));
+    if (g.bnq != run.bnq || g.bnk != run.bnk) return fail(FVSR_E_CONFIG, "ring_frame_mass: stale score slices");
+    FVSR_TRY(launch_frame_mass(ctx, g, dm, run.h1 - run.h0, ctx->d_scores + run.off,
+                               mass + (size_t)run.h0 * kids.size(), reinterpret_cast<cudaStream_t>(stream)));
+  }
+  return FVSR_OK;
 }
 
 int32_t fvsr_ring_evict(fvsr_ring* r, int32_t layer, int32_t strategy, const double* scores) {
@@ -1425,35 +1598,44 @@ int32_t fvsr_ring_evict(fvsr_ring* r, int32_t layer, int32_t strategy, const dou
   if (strategy < FVSR_EVICT_SLIDING || strategy > FVSR_EVICT_HEAD_WISE)
     return fail(FVSR_E_CONFIG, "unknown eviction strategy: %d", strategy);
   if (strategy == FVSR_EVICT_SLIDING) return fvsr_ring_evict_sliding(r, layer);  // kv_cache.cpp:100-106
-  auto& c = r->ctx[layer];
-  const size_t n = c.size();
-  if ((int)n <= r->window) return FVSR_OK;  // kv_cache.cpp:108-111
+  bool over = false;  // kv_cache.cpp:108-111
+  for (int h = 0; h < r->heads; ++h) over = over || (int)r->htab[layer][h].size() > r->window;
+  if (!over) return FVSR_OK;
   if (!scores) return fail(FVSR_E_CONFIG, "KVCache: importance scores required for scored eviction");
-  std::vector<int> ids;
-  for (auto& fs : c) ids.push_back(fs.first);
-  const size_t excess = n - (size_t)r->window;
-  std::vector<int> gone;
+  const size_t n = r->htab[layer][0].size();
+  for (int h = 1; h < r->heads; ++h)
+    if (r->htab[layer][h].size() != n) return fail(FVSR_E_SHAPE, "KVCache: score count must match retained frames");
+  auto ids_of = [&](int h) {
+    std::vector<int> ids;
+    for (auto& fs : r->htab[layer][h]) ids.push_back(fs.first);
+    return ids;
+  };
+  auto drop = [&](int h, int id) {
+    auto& c = r->htab[layer][h];
+    for (size_t i = 0; i < c.size(); ++i)
+      if (c[i].first == id) {
+        r->hused[layer][h][c[i].second] = 0;
+        c.erase(c.begin() + (long)i);
+        ++r->gen[layer];
+        return;
+      }
+  };
   if (strategy == FVSR_EVICT_UNIFORM) {  // kv_cache.cpp:118-128: head scores summed, one decision
+    const std::vector<int> ids = ids_of(0);
+    for (int h = 1; h < r->heads; ++h)
+      if (ids_of(h) != ids) return fail(FVSR_E_INVARIANT, "KVCache: uniform strategy requires head-identical sets");
     std::vector<double> total(n, 0.0);
     for (int h = 0; h < r->heads; ++h)
       for (size_t i = 0; i < n; ++i) total[i] += scores[(size_t)h * n + i];
-    gone = evict_victims(ids, total.data(), excess);
-  } else {  // head_wise (kv_cache.cpp:130-135): per-head decisions
-    gone = evict_victims(ids, scores, excess);
-    for (int h = 1; h < r->heads; ++h)
-      if (evict_victims(ids, scores + (size_t)h * n, excess) != gone)
-        return fail(FVSR_E_CONFIG,
-                    "ring_evict: head-wise victims differ across heads; the device ring keeps head-identical "
-                    "frame sets (use one ring per head for head-wise eviction)");
+    for (int id : evict_victims(ids, total.data(), n - (size_t)r->window))
+      for (int h = 0; h < r->heads; ++h) drop(h, id);
+    return FVSR_OK;
   }
-  for (int id : gone)
-    for (size_t i = 0; i < c.size(); ++i)
-      if (c[i].first == id) {
-        r->used[layer][c[i].second] = 0;
-        c.erase(c.begin() + (long)i);
-        ++r->gen[layer];
-        break;
-      }
+  for (int h = 0; h < r->heads; ++h) {  // head_wise (kv_cache.cpp:130-135): per-head decisions
+    const std::vector<int> ids = ids_of(h);
+    if ((int)ids.size() <= r->window) continue;
+    for (int id : evict_victims(ids, scores + (size_t)h * n, ids.size() - (size_t)r->window)) drop(h, id);
+  }
   return FVSR_OK;
 }
 

@@ -112,6 +112,13 @@ class KVRing:
         check(self.ctx.lib.fvsr_ring_frame_ids(self.h, layer, buf, 64, C.byref(n)))
         return [buf[i] for i in range(n.value)]
 
+    def frame_ids_head(self, layer: int, head: int):
+        """Frames head `head` of `layer` retains (head-wise eviction lets heads diverge)."""
+        buf = (C.c_int32 * 64)()
+        n = C.c_int32()
+        check(self.ctx.lib.fvsr_ring_frame_ids_head(self.h, layer, head, buf, 64, C.byref(n)))
+        return [buf[i] for i in range(n.value)]
+
     def retained(self, layer: int) -> int:
         return len(self.frame_ids(layer))
 

@@ -116,9 +116,63 @@ def test_ring_evict_errors():
         ring.evict_scored(0, fv.EVICT_UNIFORM, None)
     with pytest.raises(fv.ShapeError):
         ring.evict_scored(0, fv.EVICT_UNIFORM, np.zeros((2, 2)))
-    with pytest.raises(fv.ConfigError):  # head-wise victims that differ across heads
-        ring.evict_scored(0, fv.EVICT_HEAD_WISE, np.array([[0.0, 1.0, 2.0], [1.0, 0.0, 2.0]]))
     with pytest.raises(fv.ConfigError):  # no scores of this layer-step on the context
         fv.KVRing(1, 2, 64, 8, 16, 2).frame_mass(0, [0])
     ring.evict_scored(0, fv.EVICT_UNIFORM, np.array([[0.0, 1.0, 2.0], [0.5, 0.0, 2.0]]))
     assert ring.frame_ids(0) == [1, 2]
+    # head-wise victims that differ across heads: the sets diverge (kv_cache.cpp:130-136)
+    ring2 = fv.KVRing(1, 2, 64, 8, 16, 2)
+    for t in range(3):
+        ring2.append(0, t, to_dev(np.zeros((2, 128, 64), np.float32)), to_dev(np.zeros((2, 128, 64), np.float32)))
+    ring2.evict_scored(0, fv.EVICT_HEAD_WISE, np.array([[0.0, 1.0, 2.0], [1.0, 0.0, 2.0]]))
+    assert ring2.frame_ids_head(0, 0) == [1, 2] and ring2.frame_ids_head(0, 1) == [0, 2]
+
+
+@pytest.mark.parametrize("mask", [None, ("loc", 9, 13, True)])
+def test_headwise_eviction_diverging_heads(mask):
+    """KVCache::evict(head_wise) with heads that pick DIFFERENT victims (P/src/kv_cache.cpp:
+    130-136): each head keeps its own frame table, later steps run one launch per run of heads
+    with identical sets, and every head's selection, output and frame masses track the oracle
+    run on that head's own context; the retained sets diverge at least once."""
+    heads, rows, cols, d, topk, window = 4, 16, 40, 128, 4, 3
+    n = rows * cols
+    fmask, omask = _masks(mask or ("all",))
+    ring = fv.KVRing(1, heads, d, rows, cols, window)
+    port = oracle.Port()
+    store = {}
+    ids = [[] for _ in range(heads)]
+    diverged = False
+    for t in range(12):
+        x = oracle.bf16_round(np.stack([port.gaussian(1300 + 10 * t + h, 3 * n * d).reshape(3, n, d)
+                                        for h in range(heads)]))
+        q, k, v = x[:, 0], x[:, 1], x[:, 2]
+        store[t] = (k, v)
+        for h in range(heads):
+            ids[h].append(t)
+        bnq = (rows // 8) * (cols // 8)
+        sel = torch.empty((heads, bnq, topk), dtype=torch.int32, device="cuda")
+        cnt = torch.empty((heads, bnq), dtype=torch.int32, device="cuda")
+        out = ring.step(0, t, to_dev(k), to_dev(v), to_dev(q), [t], fmask, topk, sel=sel, sel_count=cnt)
+        out = out.float().cpu().numpy()
+        mass = ring.frame_mass(0, [t], fmask).cpu().numpy()
+        for h in range(heads):
+            assert ring.frame_ids_head(0, h) == ids[h], (t, h)
+            K = np.concatenate([store[i][0][h] for i in ids[h]], axis=0)
+            V = np.concatenate([store[i][1][h] for i in ids[h]], axis=0)
+            p = port.plan(q[h], K, [t], ids[h], rows, cols, omask, topk)
+            assert np.array_equal(sel[h].cpu().numpy()[:, : p.sel.shape[1]], p.sel), (t, h)
+            ref = port.exec(q[h], K, V, [t], ids[h], rows, cols, omask, p, oracle.head_scale(d))
+            assert rel_l2(out[h], ref) <= REL_L2_TOL and max_abs(out[h], ref) <= MAX_ABS_TOL, (t, h)
+            assert _close(mass[h], oracle.frame_attention_mass(p, ids[h], rows, cols)), (t, h)
+        ring.evict_scored(0, fv.EVICT_HEAD_WISE, mass)
+        for h in range(heads):
+            if len(ids[h]) > window:
+                gone = set(oracle.evict_victims(ids[h], list(mass[h]), len(ids[h]) - window))
+                ids[h] = [i for i in ids[h] if i not in gone]
+            assert ring.frame_ids_head(0, h) == ids[h], (t, h)
+        diverged |= any(ids[h] != ids[0] for h in range(heads))
+    assert diverged
+    if any(ids[h] != ids[0] for h in range(heads)):  # uniform needs head-identical sets (kv_cache.cpp:119-122)
+        ring.append(0, 12, to_dev(store[11][0]), to_dev(store[11][1]))
+        with pytest.raises(fv.InvariantError):
+            ring.evict_scored(0, fv.EVICT_UNIFORM, np.ones((heads, ring.retained(0))))
