@@ -507,7 +507,7 @@ def run_b200(args):
     # keys read, indices written
     ap_bytes = 2 * 2 * nh * N * D * 2 + nh * tiles * D * 4 * 2
     mb_bytes = nh * N * D * 2 * 2 + nh * bnk * D * 4 + nh * tiles * TOPK * 4
-    front = {"kernel": "ring_front_kernel (append + Q pack/pool + coarse scores + top-k)", "avg_us": fr_avg * 1e3,
+    front = {"kernel": "ring_pack_kernel (append K, V + Q pack/pool) + mask_select_kernel (coarse scores + top-k)", "avg_us": fr_avg * 1e3,
              "algorithmic_bytes": ap_bytes + mb_bytes,
              "gbs": (ap_bytes + mb_bytes) / (fr_avg / 1e3) / 1e9 if fr_avg > 0 else None, "peak_gbs": pk["hbm_gbs"],
              "frac": (ap_bytes + mb_bytes) / (fr_avg / 1e3) / 1e9 / pk["hbm_gbs"] if fr_avg > 0 else None}

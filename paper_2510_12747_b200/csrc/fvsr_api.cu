@@ -126,6 +126,9 @@ struct fvsr_ring {
   float* s0 = nullptr;
   float* s1 = nullptr;
   float* kn2 = nullptr;  // max squared key-row norm per (layer, head, slot, tile)
+  float* p0 = nullptr;   // block means S0 / count, S1 / count (the mask builder's pooled keys)
+  float* p1 = nullptr;
+  unsigned* kfl = nullptr;  // per (layer, head, slot, tile): non-finite bits of p0 / p1
   // fused RoPE (fvsr_ring_set_rope): device (cos, sin) tables per axis position
   bool rope = false;
   double rope_theta0 = 10000.0;
@@ -156,6 +159,21 @@ struct fvsr_ring {
   float* s1_layer(int l) const { return s1 + hbase(l) * part_head_stride(); }
   long long kn2_head_stride() const { return (long long)slots * n_tiles; }
   float* kn2_layer(int l) const { return kn2 + hbase(l) * kn2_head_stride(); }
+  float* p0_layer(int l) const { return p0 + hbase(l) * part_head_stride(); }
+  float* p1_layer(int l) const { return p1 + hbase(l) * part_head_stride(); }
+  unsigned* kfl_layer(int l) const { return kfl + hbase(l) * kn2_head_stride(); }
+  // the append pass's outputs besides the swizzled tiles
+  void append_outputs(int l, PackPoolArgs& a) const {
+    a.s0 = s0_layer(l);
+    a.s1 = s1_layer(l);
+    a.part_head_stride = part_head_stride();
+    a.ext_s0 = s0_layer(l);
+    a.norm2 = kn2_layer(l);
+    a.norm2_head_stride = kn2_head_stride();
+    a.p0 = p0_layer(l);
+    a.p1 = p1_layer(l);
+    a.pflag = kfl_layer(l);
+  }
 };
 
 namespace {
@@ -190,6 +208,9 @@ fvsr_ring ring_view(const fvsr_ring* r, int layer, int h0, int h1) {
   v.s0 = r->s0;
   v.s1 = r->s1;
   v.kn2 = r->kn2;
+  v.p0 = r->p0;
+  v.p1 = r->p1;
+  v.kfl = r->kfl;
   v.rope = r->rope;
   v.rope_theta0 = r->rope_theta0;
   for (int i = 0; i < 3; ++i) v.rope_split[i] = r->rope_split[i];
@@ -928,9 +949,10 @@ int32_t fvsr_ring_create(fvsr_ctx* ctx, int32_t layers, int32_t heads, int32_t d
   const size_t nb = (size_t)layers * heads * r->kn2_head_stride() * sizeof(float);
   if (cudaMalloc(&r->k, kvb) != cudaSuccess || cudaMalloc(&r->v, kvb) != cudaSuccess ||
       cudaMalloc(&r->s0, pb) != cudaSuccess || cudaMalloc(&r->s1, pb) != cudaSuccess ||
-      cudaMalloc(&r->kn2, nb) != cudaSuccess) {
+      cudaMalloc(&r->kn2, nb) != cudaSuccess || cudaMalloc(&r->p0, pb) != cudaSuccess ||
+      cudaMalloc(&r->p1, pb) != cudaSuccess || cudaMalloc(&r->kfl, nb) != cudaSuccess) {
     fvsr_ring_destroy(r);
-    return fail(FVSR_E_NOMEM, "ring allocation of %zu bytes failed", 2 * kvb + 2 * pb);
+    return fail(FVSR_E_NOMEM, "ring allocation of %zu bytes failed", 2 * kvb + 4 * pb + 2 * nb);
   }
   r->htab.assign(layers, std::vector<fvsr_ring::Table>(heads));
   r->hused.assign(layers, std::vector<std::vector<char>>(heads, std::vector<char>(r->slots, 0)));
@@ -947,6 +969,9 @@ void fvsr_ring_destroy(fvsr_ring* ring) {
   cudaFree(ring->s0);
   cudaFree(ring->s1);
   cudaFree(ring->kn2);
+  cudaFree(ring->p0);
+  cudaFree(ring->p1);
+  cudaFree(ring->kfl);
   cudaFree(ring->rope_t);
   cudaFree(ring->rope_h);
   cudaFree(ring->rope_w);
@@ -1075,12 +1100,7 @@ int ring_append_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, int frame_id, const
   a.dst = r->k_layer(layer);
   a.dst2 = r->v_layer(layer);
   a.dst_head_stride = r->kv_head_stride();
-  a.s0 = r->s0_layer(layer);
-  a.s1 = r->s1_layer(layer);
-  a.part_head_stride = r->part_head_stride();
-  a.ext_s0 = r->s0_layer(layer);
-  a.norm2 = r->kn2_layer(layer);
-  a.norm2_head_stride = r->kn2_head_stride();
+  r->append_outputs(layer, a);
   a.rows = r->rows;
   a.cols = r->cols;
   a.tiles_w = r->tiles_w;
@@ -1246,18 +1266,11 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
     if (app) {
       PackPoolArgs& a = fa.kv;
       a.src = app->k;
-      a.src2 = app->v;
       a.src_head_stride = app->kv.head_stride ? app->kv.head_stride : (long long)r->rows * r->cols * d;
       a.src_token_stride = app->kv.token_stride;
       a.dst = r->k_layer(layer);
-      a.dst2 = r->v_layer(layer);
       a.dst_head_stride = r->kv_head_stride();
-      a.s0 = r->s0_layer(layer);
-      a.s1 = r->s1_layer(layer);
-      a.part_head_stride = r->part_head_stride();
-      a.ext_s0 = r->s0_layer(layer);
-      a.norm2 = r->kn2_layer(layer);
-      a.norm2_head_stride = r->kn2_head_stride();
+      r->append_outputs(layer, a);
       a.rows = r->rows;
       a.cols = r->cols;
       a.tiles_w = r->tiles_w;
@@ -1268,7 +1281,17 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
       fa.kv_pg.count[0] = 1;
       fa.kv_pg.ext_slot[0] = partner;
       fa.kv_sl.s[0] = app_slot;
-      if ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.src2)) % 16 != 0)
+      // V: the same tiles, packed only (no partials, no bounds, never rotated)
+      PackPoolArgs& av = fa.v;
+      av = a;
+      av.src = app->v;
+      av.dst = r->v_layer(layer);
+      av.s0 = av.s1 = nullptr;
+      av.ext_s0 = nullptr;
+      av.norm2 = nullptr;
+      av.p0 = av.p1 = nullptr;
+      av.pflag = nullptr;
+      if ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(av.src)) % 16 != 0)
         return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
     }
     // one pass over Q: swizzled query tiles for the tensor cores + pooled partials for the plan
@@ -1309,6 +1332,10 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
     p.k_s0 = r->s0_layer(layer);
     p.k_s1 = r->s1_layer(layer);
     p.k_head_stride = r->part_head_stride();
+    p.k_p0 = r->p0_layer(layer);
+    p.k_p1 = r->p1_layer(layer);
+    p.k_flag = r->kfl_layer(layer);
+    p.k_flag_head_stride = r->kn2_head_stride();
     p.scale = 1.0f / std::sqrt(static_cast<float>(d));  // sparse.cpp:97
     p.topk = topk;
     p.cap = cap;
@@ -1323,10 +1350,14 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
                 : 0;
     // launch 1: ring append + Q pack/pool (independent inputs, one pass)
     const size_t smem_p = ring_pack_smem(d, max_cnt, rope_bytes);
-    const unsigned grid_p = (unsigned)((app ? r->heads * g.n_tiles : 0) + r->heads * g.nq_trows * g.n_tiles);
+    const unsigned grid_p = (unsigned)((app ? 2 * r->heads * g.n_tiles : 0) + r->heads * g.nq_trows * g.n_tiles);
     auto kp = r->rope ? ring_pack_kernel<true> : ring_pack_kernel<false>;
     FVSR_TRY(ensure_smem(kp, smem_p));
     FVSR_CUDA(launch_k(kp, dim3(grid_p), dim3(kPPThreads), smem_p, s, fa));
+    if (ctx->flags & FVSR_FLAG_SYNC_CHECK) {
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return fail(FVSR_E_CUDA, "ring_pack kernel: %s", cudaGetErrorString(e));
+    }
     // launch 2: coarse scores + top-k (programmatic launch: its prologue overlaps launch 1's tail)
     const size_t smem_s = mask_select_smem(d, g.bnk);
     const unsigned grid_s = (unsigned)(r->heads * ((g.bnq + kFrontQB - 1) / kFrontQB));
@@ -1347,7 +1378,7 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
     }
     if (ctx->flags & FVSR_FLAG_SYNC_CHECK) {  // debugging: attribute a fault to the front launches
       const cudaError_t e = cudaStreamSynchronize(s);
-      if (e != cudaSuccess) return fail(FVSR_E_CUDA, "ring front kernels: %s", cudaGetErrorString(e));
+      if (e != cudaSuccess) return fail(FVSR_E_CUDA, "mask_select kernel: %s", cudaGetErrorString(e));
     }
   }
   if (app) {  // the new frame is in the ring from here on

@@ -160,6 +160,13 @@ struct PackPoolArgs {
   const float* ext_s0;         // partner S0 for single-frame groups (ring appends), may be null
   float* norm2;                // optional: max squared row norm of src per frame-tile [slot][tile]
   long long norm2_head_stride; // elements
+  // optional: the pooled block means themselves (avg_pool_blocks' final 1/count scale applied):
+  // p0 = S0 / (rows x cols of the tile), p1 = S1 / (2 x that), same layout as s0 / s1; pflag
+  // [slot][tile] (stride norm2_head_stride) gets bit 0 / bit 1 when p0 / p1 has a non-finite
+  // value (matmul's check_finite, P/src/tensor.cpp:126-127, without re-reading the rows)
+  float* p0;
+  float* p1;
+  unsigned* pflag;
   int rows, cols, tiles_w, n_tiles, d;
   // optional fused RoPE of src (apply_rope, P/src/rope.cpp:30-62) before pooling / packing:
   // (cos, sin) tables per axis position, float-rounded from the reference's double math
@@ -257,6 +264,7 @@ __device__ __forceinline__ void pack_pool_body(const PackPoolArgs& a, const Pool
       if (8 * tw + k < a.cols) rw_t[i] = a.rope_w[(8 * tw + k) * hw + p];
     }
   }
+  if (a.pflag && tid < cnt) a.pflag[head * a.norm2_head_stride + (long long)slots.s[f0 + tid] * a.n_tiles + tile] = 0u;
   __syncthreads();
   mbar_wait(bar, (uint32_t)use & 1u);
   // RoPE (ROPE): applied on the fly where the pooling and packing phases read the staged
@@ -268,8 +276,9 @@ __device__ __forceinline__ void pack_pool_body(const PackPoolArgs& a, const Pool
     if (pi < r_ht + r_hh) return rtab[cnt * r_ht + rh * r_hh + (pi - r_ht)];
     return rtab[cnt * r_ht + 8 * r_hh + rw * r_hw + (pi - r_ht - r_hh)];
   };
-  // pooling (exact token order; rows past the frame are skipped, not added as zeros)
-  if (2 * tid < d) {
+  // pooling (exact token order; rows past the frame are skipped, not added as zeros); a pass
+  // with no partials (s0 null: the ring append's V) only packs
+  if (a.s0 && 2 * tid < d) {
     const int c = 2 * tid;
     const long long po = (long long)tile * d + c;
     const bool ext = cnt == 1 && es >= 0 && a.ext_s0 != nullptr;
@@ -318,6 +327,22 @@ __device__ __forceinline__ void pack_pool_body(const PackPoolArgs& a, const Pool
         float* S1 = a.s1 + head * a.part_head_stride + (long long)slot * a.n_tiles * d + po;
         S1[0] = s1x;
         S1[1] = s1y;
+      }
+      if (a.p0) {  // block means: single-frame block of this frame; pair block ending here
+        const long long pofs = head * a.part_head_stride + (long long)slot * a.n_tiles * d + po;
+        const float inv0 = __fdiv_rn(1.0f, (float)(hc * wc));
+        const float m0x = __fmul_rn(s0x, inv0), m0y = __fmul_rn(s0y, inv0);
+        a.p0[pofs] = m0x;
+        a.p0[pofs + 1] = m0y;
+        unsigned bad = (isfinite(m0x) && isfinite(m0y)) ? 0u : 1u;
+        if (cont) {
+          const float inv1 = __fdiv_rn(1.0f, (float)(2 * hc * wc));
+          const float m1x = __fmul_rn(s1x, inv1), m1y = __fmul_rn(s1y, inv1);
+          a.p1[pofs] = m1x;
+          a.p1[pofs + 1] = m1y;
+          if (!(isfinite(m1x) && isfinite(m1y))) bad |= 2u;
+        }
+        if (bad && a.pflag) atomicOr(a.pflag + head * a.norm2_head_stride + (long long)slot * a.n_tiles + tile, bad);
       }
       if (fi == 0 && cnt == 2) {  // frame B continues frame A's sequence
         s1x = s0x;
@@ -507,6 +532,10 @@ struct SelectParams {
   const float* k_s0;
   const float* k_s1;
   long long k_head_stride;  // elements, indexed [slot][n_tiles][d]
+  const float* k_p0;        // ring block means (PackPoolArgs::p0 / p1, same layout as k_s0 / k_s1)
+  const float* k_p1;
+  const unsigned* k_flag;   // [slot][n_tiles] non-finite bits of k_p0 / k_p1
+  long long k_flag_head_stride;
   float scale;
   long long topk;
   int cap;
@@ -659,9 +688,66 @@ constexpr int kTopkWarps = 8;
 // whose counts are ballot popcounts (no shuffles); all candidates above T are taken, and
 // the lowest ids among those equal to T fill the rest — exactly the stable-sort prefix.  A
 // ballot compaction emits ascending ids.  `sc` (global or shared) holds the row's scores.
+// Threshold of a warp's candidates by radix select: the kprime-th largest order score (with
+// multiplicity) in four 8-bit digit rounds, each a shared-memory histogram of the candidates
+// that match the digits fixed so far (`hist`: 256 words per warp) and a suffix scan over the
+// lanes' 8-bin slices.  Same T and take_eq as the 32-round bit search; requires
+// 0 < kprime < number of candidates.
 template <int NPER>
-__device__ __forceinline__ void topk_row(const DevGeom& g, const DevMask& m, const SelectParams& p, int qb, int head,
-                                         const float* sc) {
+__device__ __forceinline__ uint32_t kth_largest_radix(const uint32_t (&os)[NPER], int kprime, unsigned* hist,
+                                                      int& take_eq) {
+  const int lane = threadIdx.x & 31;
+  uint32_t prefix = 0u, pmask = 0u;
+  int need = kprime;
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    reinterpret_cast<uint4*>(hist)[2 * lane] = make_uint4(0u, 0u, 0u, 0u);
+    reinterpret_cast<uint4*>(hist)[2 * lane + 1] = make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if (os[i] != 0u && (os[i] & pmask) == prefix) atomicAdd(&hist[(os[i] >> shift) & 255u], 1u);
+    __syncwarp();
+    const uint4 h0 = reinterpret_cast<const uint4*>(hist)[2 * lane];
+    const uint4 h1 = reinterpret_cast<const uint4*>(hist)[2 * lane + 1];
+    const int c[8] = {(int)h0.x, (int)h0.y, (int)h0.z, (int)h0.w, (int)h1.x, (int)h1.y, (int)h1.z, (int)h1.w};
+    int local = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) local += c[j];
+    int suf = local;  // candidates with digit >= 8 * lane
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_down_sync(0xffffffffu, suf, o);
+      if (lane + o < 32) suf += v;
+    }
+    const int above = suf - local;  // candidates with digit >= 8 * (lane + 1)
+    const bool mine = above < need && suf >= need;
+    const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+    int dg = 0, a = above;
+    if (mine) {
+      dg = -1;
+#pragma unroll
+      for (int j = 7; j >= 0; --j)
+        if (dg < 0) {
+          if (a + c[j] >= need) dg = j;
+          else a += c[j];
+        }
+      dg += 8 * lane;
+    }
+    dg = __shfl_sync(0xffffffffu, dg, src);
+    a = __shfl_sync(0xffffffffu, a, src);
+    need -= a;
+    prefix |= (uint32_t)dg << shift;
+    pmask |= 255u << shift;
+    __syncwarp();
+  }
+  take_eq = need;
+  return prefix;
+}
+
+template <int NPER>
+__device__ __forceinline__ void topk_core(const DevGeom& g, const DevMask& m, const SelectParams& p, int qb, int head,
+                                          const float (&sv)[NPER], unsigned* hist) {
   const int lane = threadIdx.x & 31;
   const int bnk = g.bnk;
   const int qtr = qb / g.n_tiles, qtile = qb - qtr * g.n_tiles;
@@ -669,12 +755,6 @@ __device__ __forceinline__ void topk_row(const DevGeom& g, const DevMask& m, con
   int dg = -1;
   if (g.q_tr_diag[qtr] >= 0) dg = g.q_tr_diag[qtr] * g.n_tiles + qtile;
   uint32_t os[NPER];
-  float sv[NPER];
-#pragma unroll
-  for (int i = 0; i < NPER; ++i) {  // all loads in flight before any use
-    const int kb = 32 * i + lane;
-    sv[i] = kb < bnk ? sc[kb] : 0.0f;
-  }
   bool dg_ok = false;
   int n_cand = 0;
 #pragma unroll
@@ -701,6 +781,8 @@ __device__ __forceinline__ void topk_row(const DevGeom& g, const DevMask& m, con
   if (kprime <= 0) {
     T = 0xFFFFFFFFu;
     take_eq = 0;
+  } else if (kprime < n_cand && hist) {
+    T = kth_largest_radix<NPER>(os, kprime, hist, take_eq);
   } else if (kprime < n_cand) {
     uint32_t prefix = 0u;
 #pragma unroll 1
@@ -742,6 +824,20 @@ __device__ __forceinline__ void topk_row(const DevGeom& g, const DevMask& m, con
   }
 }
 
+// topk_core of a row whose scores are in memory (global or shared)
+template <int NPER>
+__device__ __forceinline__ void topk_row(const DevGeom& g, const DevMask& m, const SelectParams& p, int qb, int head,
+                                         const float* sc, unsigned* hist = nullptr) {
+  const int lane = threadIdx.x & 31;
+  float sv[NPER];
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {  // all loads in flight before any use
+    const int kb = 32 * i + lane;
+    sv[i] = kb < g.bnk ? sc[kb] : 0.0f;
+  }
+  topk_core<NPER>(g, m, p, qb, head, sv, hist);
+}
+
 
 
 template <int NPER>
@@ -755,26 +851,45 @@ __global__ void __launch_bounds__(kTopkWarps * 32) topk_select_kernel(const __gr
   const int qb = blockIdx.x * kTopkWarps + warp;
   if (qb >= g.bnq) return;
   const int head = blockIdx.y;
-  topk_row<NPER>(g, m, p, qb, head, scores + ((long long)head * g.bnq + qb) * g.bnk);
+  __shared__ __align__(16) unsigned hist[kTopkWarps][256];
+  topk_row<NPER>(g, m, p, qb, head, scores + ((long long)head * g.bnq + qb) * g.bnk, hist[warp]);
 }
 
 // ---------------------------------------------------------------------------------------
 // Streaming front end of one layer-step (ring append + mask builder) in two launches:
-//   ring_pack_kernel   blocks [0, heads*n_tiles): KVCache::append of the new frame's tile
-//                      (swizzled K/V ring slot, pooled partials, |k| bounds); the blocks after
-//                      that: the query frames' tiles (packed for the tensor cores, pooled
-//                      partials, |q| bounds).  Independent inputs, one pass over HBM.
+//   ring_pack_kernel   blocks [0, heads*n_tiles): KVCache::append of the new frame's K tile
+//                      (swizzled ring slot, pooled partials, |k| bounds); the next heads*n_tiles
+//                      blocks: its V tile (swizzled ring slot only); the blocks after that: the
+//                      query frames' tiles (packed for the tensor cores, pooled partials, |q|
+//                      bounds).  Independent inputs, one pass over HBM; one 16 KB tile per block
+//                      keeps ~13 blocks (208 KB of loads in flight) on every SM.
 //   mask_select_kernel kFrontQB q-blocks of one head per block: pooled queries, coarse scores
 //                      against the ring's pooled keys streamed through shared memory in
 //                      kFrontKC-block chunks (exact sequential chains, P/src/tensor.cpp:121-151,
 //                      sparse.cpp:97-99), top-k with the forced diagonal (topk_row).
 // ---------------------------------------------------------------------------------------
-constexpr int kFrontQB = 8;     // q-blocks per mask-select block (one warp each for top-k)
-constexpr int kFrontThreads = kFrontQB * 32;
-constexpr int kFrontKC = kFrontThreads;  // pooled key blocks staged per chunk: one per thread
+#ifndef FVSR_FRONT_QB
+#define FVSR_FRONT_QB 6
+#endif
+constexpr int kFrontQB = FVSR_FRONT_QB;  // q-blocks (pooled query rows) per mask-select block
+constexpr int kFrontQP = kFrontQB <= 2 ? 2 : (kFrontQB <= 4 ? 4 : 8);  // query slots per channel (transposed tile)
+constexpr int kFrontThreads = 256; // one key block per thread (strided past 256)
+
+// Packed fp32 pair add (FADD2): {a0, a1} += {b0, b1}, each lane rounded exactly as add.rn.f32.
+// (A packed multiply feeding it gets contracted into FFMA2 by ptxas, so the products stay
+// scalar __fmul_rn.)
+__device__ __forceinline__ void padd_rn(float& a0, float& a1, float b0, float b1) {
+  unsigned long long x;
+  asm("{\n\t.reg .b64 b2;\n\tmov.b64 b2, {%3, %4};\n\tmov.b64 %0, {%1, %2};\n\t"
+      "add.rn.f32x2 %0, %0, b2;\n\t}"
+      : "=l"(x)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(x));
+}
 
 struct FrontArgs {
-  PackPoolArgs kv;   // append: src = k, src2 = v, dst/dst2 = ring slots (src null: no append)
+  PackPoolArgs kv;   // append K: src = k, dst = ring slot, partials + |k| bounds (src null: no append)
+  PackPoolArgs v;    // append V: src = v, dst = ring slot, pack only (s0 null)
   PoolGroups kv_pg;
   SlotList kv_sl;
   PackPoolArgs q;    // query frames: packed tiles + pooled partials into the workspace
@@ -784,7 +899,7 @@ struct FrontArgs {
 };
 
 inline size_t ring_pack_smem(int d, int max_q_cnt, size_t rope_bytes) {
-  return std::max(pack_pool_smem(d, 1, true), pack_pool_smem(d, max_q_cnt, false)) + rope_bytes;
+  return pack_pool_smem(d, max_q_cnt, false) + rope_bytes;
 }
 
 template <bool ROPE>
@@ -800,19 +915,34 @@ __global__ void __launch_bounds__(kPPThreads) ring_pack_kernel(const __grid_cons
     return;
   }
   b -= n_append;
+  if (b < n_append) {  // V: never rotated
+    const int head = b / fa.n_tiles;
+    pack_pool_body<false>(fa.v, fa.kv_pg, fa.kv_sl, b - head * fa.n_tiles, 0, head, sm_rp);
+    return;
+  }
+  b -= n_append;
   const int per_head = fa.q_trows * fa.n_tiles;
   const int head = b / per_head, rem = b - head * per_head, qtr = rem / fa.n_tiles;
   pack_pool_body<ROPE>(fa.q, fa.q_pg, fa.q_sl, rem - qtr * fa.n_tiles, qtr, head, sm_rp);
 }
 
 inline size_t mask_select_smem(int d, int bnk) {
-  return ((size_t)(kFrontQB + kFrontKC) * (d + 4) + (size_t)kFrontQB * bnk) * 4;
+  return (size_t)d * kFrontQP * 4 + (size_t)kFrontQB * bnk * 4 + (size_t)kFrontQB * 256 * 4;
 }
 
+// Coarse scores + top-k of kFrontQB (head, q-block) rows per block.  Thread t owns key blocks
+// t, t + 256, ...: it streams the key block's mean (the ring's p0 / p1 row, written by the
+// append pass with its non-finite bits) from L2 and runs the kFrontQB query chains on it,
+// scalar products and the adds in packed pairs (FADD2; per chain the reference's exact order --
+// channels ascending, separate multiply and add from 0.0f, then the 1/sqrt(d) multiply; P/src/tensor.cpp:121-151,
+// sparse.cpp:97-99); the pooled queries (S / count, scaled here) sit transposed in shared
+// memory, [channel][query slot], so one channel's queries are one broadcast load.  Scores go
+// to shared memory; warp r then selects row r (topk_row, radix threshold).
 template <int NPER>
 __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid_constant__ DevGeom g,
                                                                     const __grid_constant__ DevMask m,
                                                                     const __grid_constant__ SelectParams p) {
+  static_assert(kFrontQB >= 1 && kFrontQB <= 8 && kFrontQB * 32 <= kFrontThreads, "one warp per row for top-k");
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) float sm_ms[];
@@ -821,20 +951,14 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
   const int head = blockIdx.x / per_head;
   const int qb0 = (blockIdx.x - head * per_head) * kFrontQB;
   const int nqb = min(kFrontQB, g.bnq - qb0);
-  const int d = g.d, ld = d + 4, d4 = d >> 2, bnk = g.bnk;
-  float* pq = sm_ms;                 // [kFrontQB][d+4]
-  float* pk = pq + kFrontQB * ld;    // [kFrontKC][d+4]
-  float* sc = pk + kFrontKC * ld;    // [kFrontQB][bnk]
+  const int d = g.d, d4 = d >> 2, bnk = g.bnk;
+  float* qT = sm_ms;                                          // [d][kFrontQP]
+  unsigned* hist = reinterpret_cast<unsigned*>(qT + d * kFrontQP);   // [kFrontQB][256] (16 B aligned)
+  float* sc = reinterpret_cast<float*>(hist + kFrontQB * 256);         // [kFrontQB][bnk]
   bool fin = true;
-  // pooled keys, kFrontKC blocks per chunk; each chunk's row sources and 1/count come from
-  // one thread per row (shared), then every thread has its loads of the chunk in flight at once
-  constexpr int kPer = kFrontKC * 32 / kFrontThreads;  // float4 per thread per chunk (d <= 128)
-  __shared__ const float* rsrc[kFrontKC];
-  __shared__ float rinv[kFrontKC];
-  const int lg4 = d4 == 32 ? 5 : 4;  // d in {64, 128}
   // pooled queries: S1 (two-frame rows) or S0, times 1/count (avg_pool_blocks' final scale)
-  for (int idx = tid; idx < kFrontQB * d4; idx += kFrontThreads) {
-    const int r = idx >> lg4, c4 = idx & (d4 - 1);
+  for (int idx = tid; idx < kFrontQP * d4; idx += kFrontThreads) {
+    const int r = idx / d4, c4 = idx - r * d4;
     float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r < nqb) {
       const int qb = qb0 + r, qtr = qb / g.n_tiles, qtile = qb - qtr * g.n_tiles;
@@ -848,72 +972,76 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
       w.w = __fmul_rn(w.w, inv);
       fin = fin && isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w);
     }
-    *reinterpret_cast<float4*>(pq + r * ld + c4 * 4) = w;
+    qT[(4 * c4 + 0) * kFrontQP + r] = w.x;
+    qT[(4 * c4 + 1) * kFrontQP + r] = w.y;
+    qT[(4 * c4 + 2) * kFrontQP + r] = w.z;
+    qT[(4 * c4 + 3) * kFrontQP + r] = w.w;
   }
-  for (int kc0 = 0; kc0 < bnk; kc0 += kFrontKC) {
-    const int nk = min(kFrontKC, bnk - kc0);
-    if (tid < kFrontKC) {
-      const int kb = kc0 + tid;
-      const float* src = nullptr;
-      float inv = 0.0f;
-      if (tid < nk) {
-        const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
-        const int kcnt = g.k_tr_count[ktr], kf = g.k_tr_first[ktr] + kcnt - 1;
-        src = (kcnt == 2 ? p.k_s1 : p.k_s0) + head * p.k_head_stride + ((long long)g.k_slot[kf] * g.n_tiles + ktile) * d;
-        inv = __fdiv_rn(1.0f, (float)(kcnt * tile_h_count(g, ktile) * tile_w_count(g, ktile)));
-      }
-      rsrc[tid] = src;
-      rinv[tid] = inv;
-    }
-    __syncthreads();  // row sources ready; the previous chunk's scores have read pk
-    {
-      float4 kv4[kPer];
+  __syncthreads();
+  for (int kb = tid; kb < bnk; kb += kFrontThreads) {
+    const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+    const int kcnt = g.k_tr_count[ktr], kf = g.k_tr_first[ktr] + kcnt - 1;
+    const long long slot_tile = (long long)g.k_slot[kf] * g.n_tiles + ktile;
+    if (p.k_flag[head * p.k_flag_head_stride + slot_tile] & (kcnt == 2 ? 2u : 1u)) fin = false;
+    const float4* kr = reinterpret_cast<const float4*>((kcnt == 2 ? p.k_p1 : p.k_p0) + head * p.k_head_stride +
+                                                       slot_tile * d);
+    float acc[kFrontQP];
 #pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        const int idx = tid + j * kFrontThreads, r = idx >> lg4, c4 = idx & (d4 - 1);
-        const float* src = r < kFrontKC ? rsrc[r] : nullptr;
-        kv4[j] = src ? __ldg(reinterpret_cast<const float4*>(src) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+    for (int r = 0; r < kFrontQP; ++r) acc[r] = 0.0f;
+    auto channel = [&](float k, int c) {
+#if FVSR_MS_EXP == 2
+      acc[0] = __fadd_rn(acc[0], k);  // experiment: no chains
+      return;
+#endif
+      float qv[kFrontQP];
+      if constexpr (kFrontQP == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(qT + c * kFrontQP);
+        qv[0] = t.x;
+        qv[1] = t.y;
+      } else {
 #pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        const int idx = tid + j * kFrontThreads, r = idx >> lg4, c4 = idx & (d4 - 1);
-        if (r < nk) {
-          const float inv = rinv[r];
-          float4 w = kv4[j];
-          w.x = __fmul_rn(w.x, inv);
-          w.y = __fmul_rn(w.y, inv);
-          w.z = __fmul_rn(w.z, inv);
-          w.w = __fmul_rn(w.w, inv);
-          fin = fin && isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w);
-          *reinterpret_cast<float4*>(pk + r * ld + c4 * 4) = w;
-        }
-      }
-    }
-    __syncthreads();
-    // thread t scores key block kc0 + t against the kFrontQB pooled queries: kFrontQB
-    // independent exact chains (channels ascending, separate multiply and add from 0.0f, then
-    // the 1/sqrt(d) multiply); query rows are warp-broadcast loads, the key row stays put
-    if (tid < nk) {
-      float acc[kFrontQB];
-#pragma unroll
-      for (int k = 0; k < kFrontQB; ++k) acc[k] = 0.0f;
-      const float* kr = pk + tid * ld;
-#pragma unroll 2
-      for (int c = 0; c < d; c += 4) {
-        const float4 b = *reinterpret_cast<const float4*>(kr + c);
-#pragma unroll
-        for (int k = 0; k < kFrontQB; ++k) {
-          const float4 a = *reinterpret_cast<const float4*>(pq + k * ld + c);
-          chain4(acc[k], a, b);
+        for (int r4 = 0; r4 < kFrontQP; r4 += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(qT + c * kFrontQP + r4);
+          qv[r4] = t.x;
+          qv[r4 + 1] = t.y;
+          qv[r4 + 2] = t.z;
+          qv[r4 + 3] = t.w;
         }
       }
 #pragma unroll
-      for (int k = 0; k < kFrontQB; ++k) sc[k * bnk + kc0 + tid] = __fmul_rn(acc[k], p.scale);
+      for (int r = 0; r + 1 < kFrontQB; r += 2) padd_rn(acc[r], acc[r + 1], __fmul_rn(qv[r], k), __fmul_rn(qv[r + 1], k));
+      if constexpr (kFrontQB & 1) acc[kFrontQB - 1] = __fadd_rn(acc[kFrontQB - 1], __fmul_rn(qv[kFrontQB - 1], k));
+    };
+    // the row in batches of 8 channel quads, the next batch's loads in flight meanwhile
+    float4 cur[8], nxt[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cur[j] = j < d4 ? __ldg(kr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+    for (int b = 0; b < d4; b += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) nxt[j] = b + 8 + j < d4 ? __ldg(kr + b + 8 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (b + j < d4) {
+          const int c = 4 * (b + j);
+          channel(cur[j].x, c);
+          channel(cur[j].y, c + 1);
+          channel(cur[j].z, c + 2);
+          channel(cur[j].w, c + 3);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
     }
-    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kFrontQB; ++r) sc[r * bnk + kb] = __fmul_rn(acc[r], p.scale);
   }
   if (!fin) atomicOr(p.err, kErrShape);
-  if (warp < nqb) topk_row<NPER>(g, m, p, qb0 + warp, head, sc + warp * bnk);
+  __syncthreads();
+#if FVSR_MS_EXP == 1
+  return;  // experiment: scores only
+#endif
+  if (warp < nqb) topk_row<NPER>(g, m, p, qb0 + warp, head, sc + warp * bnk, hist + warp * 256);
 }
 
 // ---------------------------------------------------------------------------------------
