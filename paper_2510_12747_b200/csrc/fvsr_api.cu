@@ -433,6 +433,63 @@ int ensure_smem(K* kern, size_t bytes) {
   return FVSR_OK;
 }
 
+// Prefer the largest shared-memory carveout for a kernel whose occupancy is bounded by it
+// (once per device and kernel).
+template <typename K>
+int ensure_carveout(K* kern) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, bool> done;
+  int dev = 0;
+  FVSR_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  bool& d = done[{dev, reinterpret_cast<const void*>(kern)}];
+  if (!d) {
+    FVSR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    d = true;
+  }
+  return FVSR_OK;
+}
+
+// Tensor map of a token-major bf16 source for the TMA pack/pool path: 5-D (channel, col, row,
+// frame, head), box (64, 8, 8, 1, 1), 128-byte swizzle, zero fill past the edges.  false when
+// the driver entry point is missing or the layout does not meet TMA's alignment rules (the
+// caller then keeps the bulk-copy path).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+bool encode_src_map(CUtensorMap* m, const void* src, int d, int rows, int cols, int frames, int heads,
+                    long long token_stride, long long head_stride) {
+  EncodeTiledFn fn = encode_tiled_fn();
+#ifdef FVSR_NO_TMA_PACK
+  fn = nullptr;  // experiment builds only: keep the bulk-copy pack/pool path
+#endif
+  if (!fn || !src || (d != 64 && d != 128)) return false;
+  const long long ts = token_stride ? token_stride : d;
+  const long long fs = (long long)rows * cols * ts;
+  const long long hs = head_stride ? head_stride : fs * frames;
+  if (reinterpret_cast<uintptr_t>(src) % 16 != 0 || (ts * 2) % 16 != 0 || (hs * 2) % 16 != 0) return false;
+  const cuuint64_t dims[5] = {(cuuint64_t)d, (cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)frames, (cuuint64_t)heads};
+  const cuuint64_t strides[4] = {(cuuint64_t)(ts * 2), (cuuint64_t)(cols * ts * 2), (cuuint64_t)(fs * 2),
+                                 (cuuint64_t)(hs * 2)};
+  const cuuint32_t box[5] = {64, 8, 8, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(src), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int launch_pack_pool(const PackPoolArgs& a, const PoolGroups& pg, const SlotList& sl, dim3 grid, int max_cnt,
                      cudaStream_t s) {
   if (a.d % 8 != 0) return fail(FVSR_E_CONFIG, "pack_pool: head_dim must be a multiple of 8 (got %d)", a.d);
@@ -1107,6 +1164,8 @@ int ring_append_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, int frame_id, const
   a.n_tiles = r->n_tiles;
   a.d = r->d;
   FVSR_TRY(rope_args(r, &frame_id, 1, a));
+  a.use_tma = encode_src_map(&a.tm, a.src, r->d, r->rows, r->cols, 1, r->heads, 0, a.src_head_stride) &&
+              encode_src_map(&a.tm2, a.src2, r->d, r->rows, r->cols, 1, r->heads, 0, a.src_head_stride);
   PoolGroups pg{};
   pg.first[0] = 0;
   pg.count[0] = 1;
@@ -1277,6 +1336,7 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
       a.n_tiles = r->n_tiles;
       a.d = d;
       FVSR_TRY(rope_args(r, &app->frame_id, 1, a));
+      a.use_tma = encode_src_map(&a.tm, a.src, d, r->rows, r->cols, 1, r->heads, a.src_token_stride, a.src_head_stride);
       fa.kv_pg.first[0] = 0;
       fa.kv_pg.count[0] = 1;
       fa.kv_pg.ext_slot[0] = partner;
@@ -1291,6 +1351,8 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
       av.norm2 = nullptr;
       av.p0 = av.p1 = nullptr;
       av.pflag = nullptr;
+      av.use_tma = encode_src_map(&av.tm, av.src, d, r->rows, r->cols, 1, r->heads, av.src_token_stride,
+                                  av.src_head_stride);
       if ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(av.src)) % 16 != 0)
         return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
     }
@@ -1314,6 +1376,7 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
     if (reinterpret_cast<uintptr_t>(q) % 16 != 0)
       return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
     FVSR_TRY(rope_args(r, q_frame_ids, nq, a));
+    a.use_tma = encode_src_map(&a.tm, q, d, g.rows, g.cols, g.nqf, r->heads, a.src_token_stride, a.src_head_stride);
     int max_cnt = 1;
     for (int t = 0; t < g.nq_trows; ++t) {
       fa.q_pg.first[t] = g.q_tr_first[t];
@@ -1353,6 +1416,7 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
     const unsigned grid_p = (unsigned)((app ? 2 * r->heads * g.n_tiles : 0) + r->heads * g.nq_trows * g.n_tiles);
     auto kp = r->rope ? ring_pack_kernel<true> : ring_pack_kernel<false>;
     FVSR_TRY(ensure_smem(kp, smem_p));
+    FVSR_TRY(ensure_carveout(kp));  // 12 blocks of ~18 KB resident per SM
     FVSR_CUDA(launch_k(kp, dim3(grid_p), dim3(kPPThreads), smem_p, s, fa));
     if (ctx->flags & FVSR_FLAG_SYNC_CHECK) {
       const cudaError_t e = cudaStreamSynchronize(s);

@@ -15,6 +15,7 @@
 #include <type_traits>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda.h>  // CUtensorMap (the driver entry point is resolved at run time)
 #include <cuda_runtime.h>
 
 namespace fvsr {
@@ -182,6 +183,17 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
                "r"(bytes)
                : "memory");
+}
+// Tiled tensor copy global -> shared through a tensor map (TMA), 5-D box at the given
+// coordinates (innermost first); completion counted on `bar` in bytes (out-of-bounds box
+// elements are written as zeros and counted).
+__device__ __forceinline__ void tma_load_5d(void* dst, const void* map, int c0, int c1, int c2, int c3, int c4,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
 }
 // global -> L2 bulk prefetch (no completion tracking)
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {

@@ -145,7 +145,13 @@ __global__ void __launch_bounds__(256) pool_partials_kernel(const T* __restrict_
 // the swizzled tiles with coalesced 16-byte stores (thread i writes destination chunk i;
 // the source chunk is the inverse swizzle).  Requires d % 8 == 0 (16-byte rows).
 // ---------------------------------------------------------------------------------------
-struct PackPoolArgs {
+struct alignas(64) PackPoolArgs {
+  // TMA path (use_tma): tensor maps of src / src2 as 5-D (channel, col, row, frame, head) with a
+  // (64, 8, 8, 1, 1) box and 128-byte swizzle, i.e. one box = one 64-channel panel of a frame-tile
+  // in exactly the ring's swizzled layout (fvsr_common.cuh); built on the host per call
+  CUtensorMap tm;
+  CUtensorMap tm2;
+  int use_tma;
   const uint16_t* src;   // pooled + packed, [heads][frames * rows * cols][d]
   const uint16_t* src2;  // packed only (may be null)
   long long src_head_stride;  // elements (both sources)
@@ -181,7 +187,23 @@ constexpr int kPPThreads = 128;
 
 // shared bytes: [cnt frames][1 or 2 tensors][64 rows][d] bf16 + barrier
 inline size_t pack_pool_smem(int d, int max_cnt, bool two) {
-  return (size_t)max_cnt * (two ? 2 : 1) * 64 * d * 2 + 16;
+  return (size_t)max_cnt * (two ? 2 : 1) * 64 * d * 2 + 16 + 1024;  // + 1 KB: 128-byte-swizzle alignment
+}
+
+#ifndef FVSR_PP_EXP
+#define FVSR_PP_EXP 0  // experiment builds only (build_variant): 1 = ring pack data movement only
+#endif
+
+// Packed fp32 pair add (FADD2): {a0, a1} += {b0, b1}, each lane rounded exactly as add.rn.f32.
+// (A packed multiply feeding it gets contracted into FFMA2 by ptxas, so the products stay
+// scalar __fmul_rn.)
+__device__ __forceinline__ void padd_rn(float& a0, float& a1, float b0, float b1) {
+  unsigned long long x;
+  asm("{\n\t.reg .b64 b2;\n\tmov.b64 b2, {%3, %4};\n\tmov.b64 %0, {%1, %2};\n\t"
+      "add.rn.f32x2 %0, %0, b2;\n\t}"
+      : "=l"(x)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(x));
 }
 
 // one bf16 channel pair (x0 | x1 << 16) rotated by (cos, sin): x0*c - x1*s, x0*s + x1*c in
@@ -413,6 +435,189 @@ __device__ __forceinline__ void pack_pool_body(const PackPoolArgs& a, const Pool
   }
 }
 
+// The same pass with the tiles brought in by the tensor cores' copy engine already in the
+// ring's layout: one TMA box per 64-channel panel per (frame, tensor) lands swizzled (and
+// zero-filled past the frame edge) in shared memory, the threads pool (and with ROPE first
+// rotate in place) and take the |row| bounds from it, and one bulk copy per frame-tile
+// writes it to the ring slot / query workspace.  No per-chunk register traffic: an append of
+// V is three instructions of one thread.
+template <bool ROPE>
+__device__ __forceinline__ void pack_pool_tma(const PackPoolArgs& a, const PoolGroups& groups, const SlotList& slots,
+                                              int tile, int grp, int head, uint8_t* sm_raw) {
+  const int tid = threadIdx.x;
+  const int d = a.d;
+  const int th = tile / a.tiles_w, tw = tile - th * a.tiles_w;
+  const int hc = min(8, a.rows - 8 * th), wc = min(8, a.cols - 8 * tw);
+  const uint32_t tile_bytes = (uint32_t)d * 128u;
+  const int f0 = groups.first[grp], cnt = groups.count[grp], es = groups.ext_slot[grp];
+  const int nt = a.src2 ? 2 : 1;
+  uint8_t* base = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
+  auto stage = [&](int fi, int t) -> uint8_t* { return base + (size_t)(fi * nt + t) * tile_bytes; };
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + (size_t)cnt * nt * tile_bytes);
+  float2* rtab = reinterpret_cast<float2*>(base + (size_t)cnt * nt * tile_bytes + 16);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    mbar_arrive_expect_tx(bar, tile_bytes * cnt * nt);
+    for (int fi = 0; fi < cnt; ++fi)
+      for (int t = 0; t < nt; ++t)
+        for (int pnl = 0; pnl < d / 64; ++pnl)
+          tma_load_5d(stage(fi, t) + pnl * 8192, t == 0 ? &a.tm : &a.tm2, 64 * pnl, 8 * tw, 8 * th, f0 + fi, head, bar);
+  }
+  if (a.pflag && tid < cnt) a.pflag[head * a.norm2_head_stride + (long long)slots.s[f0 + tid] * a.n_tiles + tile] = 0u;
+  const int r_ht = a.rope_dt >> 1, r_hh = a.rope_dh >> 1, r_hw = a.rope_dw >> 1;
+  if constexpr (ROPE) {  // this tile's (cos, sin): t: [cnt][dt/2], h: [8][dh/2], w: [8][dw/2]
+    for (int i = tid; i < cnt * r_ht; i += kPPThreads) {
+      const int fi = i / r_ht, q = i - fi * r_ht;
+      rtab[i] = a.rope_t[(long long)a.rope_fid[f0 + fi] * r_ht + q];
+    }
+    float2* rh_t = rtab + cnt * r_ht;
+    for (int i = tid; i < 8 * r_hh; i += kPPThreads) {
+      const int k = i / r_hh, q = i - k * r_hh;
+      if (8 * th + k < a.rows) rh_t[i] = a.rope_h[(8 * th + k) * r_hh + q];
+    }
+    float2* rw_t = rh_t + 8 * r_hh;
+    for (int i = tid; i < 8 * r_hw; i += kPPThreads) {
+      const int k = i / r_hw, q = i - k * r_hw;
+      if (8 * tw + k < a.cols) rw_t[i] = a.rope_w[(8 * tw + k) * r_hw + q];
+    }
+  }
+  __syncthreads();  // barrier initialised, flags reset, RoPE tables staged
+  mbar_wait(bar, 0);
+  // byte offset of (row r, channel c) in a swizzled frame-tile
+  auto at = [](int r, int c) -> uint32_t {
+    return (uint32_t)((c >> 6) * 8192 + r * 128 + ((((c & 63) >> 3) ^ (r & 7)) << 4) + (c & 7) * 2);
+  };
+  if constexpr (ROPE) {  // rotate src in place (rows past the frame stay zero)
+    const int chunks = (int)tile_bytes / 16;
+    for (int fi = 0; fi < cnt; ++fi) {
+      uint8_t* st = stage(fi, 0);
+      for (int i = tid; i < chunks; i += kPPThreads) {
+        const int pnl = i >> 9, r = (i >> 3) & 63, j = i & 7;
+        const int rh = r >> 3, rw = r & 7;
+        if (rh >= hc || rw >= wc) continue;
+        const int p0 = (pnl * 64 + ((j ^ (r & 7)) << 3)) >> 1;  // first channel pair of the chunk
+        uint4 v = *reinterpret_cast<uint4*>(st + (size_t)i * 16);
+        auto cs = [&](int pi) -> float2 {
+          if (pi < r_ht) return rtab[fi * r_ht + pi];
+          if (pi < r_ht + r_hh) return rtab[cnt * r_ht + rh * r_hh + (pi - r_ht)];
+          return rtab[cnt * r_ht + 8 * r_hh + rw * r_hw + (pi - r_ht - r_hh)];
+        };
+        v.x = rope_word(v.x, cs(p0));
+        v.y = rope_word(v.y, cs(p0 + 1));
+        v.z = rope_word(v.z, cs(p0 + 2));
+        v.w = rope_word(v.w, cs(p0 + 3));
+        *reinterpret_cast<uint4*>(st + (size_t)i * 16) = v;
+      }
+    }
+    __syncthreads();
+  }
+#if FVSR_PP_EXP == 1
+  if (0) {  // experiment: data movement only
+#else
+  // pooling: channels 2t, 2t+1 in exact token order (rows past the frame skipped)
+  if (a.s0 && 2 * tid < d) {
+#endif
+    const int c = 2 * tid;
+    const long long po = (long long)tile * d + c;
+    const bool ext = cnt == 1 && es >= 0 && a.ext_s0 != nullptr;
+    float s1x = 0.0f, s1y = 0.0f;
+    if (ext) {
+      const float* e = a.ext_s0 + head * a.part_head_stride + (long long)es * a.n_tiles * d + po;
+      s1x = e[0];
+      s1y = e[1];
+    }
+    for (int fi = 0; fi < cnt; ++fi) {
+      const int slot = slots.s[f0 + fi];
+      const bool cont = fi == 1 || ext;
+      const uint8_t* st = stage(fi, 0);
+      float s0x = 0.0f, s0y = 0.0f;
+      // x and y advance together as one packed add
+      for (int rh = 0; rh < hc; ++rh) {
+        uint32_t w[8];
+#pragma unroll
+        for (int rw = 0; rw < 8; ++rw) w[rw] = *reinterpret_cast<const uint32_t*>(st + at(rh * 8 + rw, c));
+#pragma unroll
+        for (int rw = 0; rw < 8; ++rw) {
+          if (rw < wc) {
+            const float x = __uint_as_float(w[rw] << 16), y = __uint_as_float(w[rw] & 0xffff0000u);
+            padd_rn(s0x, s0y, x, y);
+            if (cont) padd_rn(s1x, s1y, x, y);
+          }
+        }
+      }
+      const long long pofs = head * a.part_head_stride + (long long)slot * a.n_tiles * d + po;
+      a.s0[pofs] = s0x;
+      a.s0[pofs + 1] = s0y;
+      if (cont) {
+        a.s1[pofs] = s1x;
+        a.s1[pofs + 1] = s1y;
+      }
+      if (a.p0) {  // block means: single-frame block of this frame; pair block ending here
+        const float inv0 = __fdiv_rn(1.0f, (float)(hc * wc));
+        const float m0x = __fmul_rn(s0x, inv0), m0y = __fmul_rn(s0y, inv0);
+        a.p0[pofs] = m0x;
+        a.p0[pofs + 1] = m0y;
+        unsigned bad = (isfinite(m0x) && isfinite(m0y)) ? 0u : 1u;
+        if (cont) {
+          const float inv1 = __fdiv_rn(1.0f, (float)(2 * hc * wc));
+          const float m1x = __fmul_rn(s1x, inv1), m1y = __fmul_rn(s1y, inv1);
+          a.p1[pofs] = m1x;
+          a.p1[pofs + 1] = m1y;
+          if (!(isfinite(m1x) && isfinite(m1y))) bad |= 2u;
+        }
+        if (bad && a.pflag) atomicOr(a.pflag + head * a.norm2_head_stride + (long long)slot * a.n_tiles + tile, bad);
+      }
+      if (fi == 0 && cnt == 2) {  // frame B continues frame A's sequence
+        s1x = s0x;
+        s1y = s0y;
+      }
+    }
+  }
+  // |row| bounds of src (max squared row norm per frame-tile): two threads per row
+  if (a.norm2 && FVSR_PP_EXP != 1) {
+    __shared__ float wmax_t[kPPThreads / 32];
+    const int r = tid >> 1, half = tid & 1, cpt = d >> 1;  // channels per thread
+    for (int fi = 0; fi < cnt; ++fi) {
+      const uint8_t* st = stage(fi, 0);
+      float acc4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // four independent chains
+#pragma unroll 8
+      for (int c = half * cpt; c < (half + 1) * cpt; c += 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(st + at(r, c));
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float x = __uint_as_float(w4[e] << 16), y = __uint_as_float(w4[e] & 0xffff0000u);
+          acc4[e] = fmaf(x, x, fmaf(y, y, acc4[e]));
+        }
+      }
+      float acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+#pragma unroll
+      for (int o = 2; o < 32; o <<= 1) acc = fmaxf(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+      if ((tid & 31) == 0) wmax_t[tid >> 5] = acc;
+      __syncthreads();
+      if (tid == 0) {
+        float mx = wmax_t[0];
+#pragma unroll
+        for (int w = 1; w < kPPThreads / 32; ++w) mx = fmaxf(mx, wmax_t[w]);
+        a.norm2[head * a.norm2_head_stride + (long long)slots.s[f0 + fi] * a.n_tiles + tile] = mx;
+      }
+      __syncthreads();
+    }
+  }
+  if constexpr (ROPE) fence_proxy_async_smem();  // rotated tiles: generic writes -> async-proxy reads
+  __syncthreads();
+  if (tid == 0) {
+    for (int fi = 0; fi < cnt; ++fi) {
+      const long long to = head * a.dst_head_stride + ((long long)slots.s[f0 + fi] * a.n_tiles + tile) * tile_bytes;
+      for (int t = 0; t < nt; ++t) bulk_s2g((t == 0 ? a.dst : a.dst2) + to, stage(fi, t), tile_bytes);
+    }
+    bulk_commit();
+    bulk_wait_read();  // shared memory stays valid until the copies have read it
+  }
+}
+
 template <bool ROPE>
 __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_constant__ PackPoolArgs a,
                                                                const __grid_constant__ PoolGroups groups,
@@ -420,7 +625,10 @@ __global__ void __launch_bounds__(kPPThreads) pack_pool_kernel(const __grid_cons
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) uint8_t sm_pp[];
-  pack_pool_body<ROPE>(a, groups, slots, blockIdx.x, blockIdx.y, blockIdx.z, sm_pp);
+  if (a.use_tma)
+    pack_pool_tma<ROPE>(a, groups, slots, blockIdx.x, blockIdx.y, blockIdx.z, sm_pp);
+  else
+    pack_pool_body<ROPE>(a, groups, slots, blockIdx.x, blockIdx.y, blockIdx.z, sm_pp);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -875,18 +1083,6 @@ constexpr int kFrontQB = FVSR_FRONT_QB;  // q-blocks (pooled query rows) per mas
 constexpr int kFrontQP = kFrontQB <= 2 ? 2 : (kFrontQB <= 4 ? 4 : 8);  // query slots per channel (transposed tile)
 constexpr int kFrontThreads = 256; // one key block per thread (strided past 256)
 
-// Packed fp32 pair add (FADD2): {a0, a1} += {b0, b1}, each lane rounded exactly as add.rn.f32.
-// (A packed multiply feeding it gets contracted into FFMA2 by ptxas, so the products stay
-// scalar __fmul_rn.)
-__device__ __forceinline__ void padd_rn(float& a0, float& a1, float b0, float b1) {
-  unsigned long long x;
-  asm("{\n\t.reg .b64 b2;\n\tmov.b64 b2, {%3, %4};\n\tmov.b64 %0, {%1, %2};\n\t"
-      "add.rn.f32x2 %0, %0, b2;\n\t}"
-      : "=l"(x)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(x));
-}
-
 struct FrontArgs {
   PackPoolArgs kv;   // append K: src = k, dst = ring slot, partials + |k| bounds (src null: no append)
   PackPoolArgs v;    // append V: src = v, dst = ring slot, pack only (s0 null)
@@ -903,27 +1099,37 @@ inline size_t ring_pack_smem(int d, int max_q_cnt, size_t rope_bytes) {
 }
 
 template <bool ROPE>
-__global__ void __launch_bounds__(kPPThreads) ring_pack_kernel(const __grid_constant__ FrontArgs fa) {
+__global__ void __launch_bounds__(kPPThreads, 12) ring_pack_kernel(const __grid_constant__ FrontArgs fa) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) uint8_t sm_rp[];
   const int n_append = fa.kv.src != nullptr ? fa.heads * fa.n_tiles : 0;
   int b = blockIdx.x;
+  auto run = [&](const PackPoolArgs& a, const PoolGroups& pg, const SlotList& sl, int tile, int grp, int head,
+                 bool rope) {
+    if (a.use_tma) {
+      if (rope) pack_pool_tma<ROPE>(a, pg, sl, tile, grp, head, sm_rp);
+      else pack_pool_tma<false>(a, pg, sl, tile, grp, head, sm_rp);
+    } else {
+      if (rope) pack_pool_body<ROPE>(a, pg, sl, tile, grp, head, sm_rp);
+      else pack_pool_body<false>(a, pg, sl, tile, grp, head, sm_rp);
+    }
+  };
   if (b < n_append) {
     const int head = b / fa.n_tiles;
-    pack_pool_body<ROPE>(fa.kv, fa.kv_pg, fa.kv_sl, b - head * fa.n_tiles, 0, head, sm_rp);
+    run(fa.kv, fa.kv_pg, fa.kv_sl, b - head * fa.n_tiles, 0, head, true);
     return;
   }
   b -= n_append;
   if (b < n_append) {  // V: never rotated
     const int head = b / fa.n_tiles;
-    pack_pool_body<false>(fa.v, fa.kv_pg, fa.kv_sl, b - head * fa.n_tiles, 0, head, sm_rp);
+    run(fa.v, fa.kv_pg, fa.kv_sl, b - head * fa.n_tiles, 0, head, false);
     return;
   }
   b -= n_append;
   const int per_head = fa.q_trows * fa.n_tiles;
   const int head = b / per_head, rem = b - head * per_head, qtr = rem / fa.n_tiles;
-  pack_pool_body<ROPE>(fa.q, fa.q_pg, fa.q_sl, rem - qtr * fa.n_tiles, qtr, head, sm_rp);
+  run(fa.q, fa.q_pg, fa.q_sl, rem - qtr * fa.n_tiles, qtr, head, true);
 }
 
 inline size_t mask_select_smem(int d, int bnk) {
