@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -51,14 +52,42 @@ fvsr_ctx* context() {
   return ctx.get();
 }
 
+// Per-thread cache of device buffers by byte size: a call's buffers go back to the cache when
+// it returns, so repeated calls with the same shapes do not allocate.  Calls on one thread
+// are stream-ordered on the default stream and synchronise before returning, so a cached
+// buffer is idle when it is handed out again.
+struct BufCache {
+  std::multimap<std::size_t, void*> free_;
+  ~BufCache() {
+    for (auto& kv : free_) cudaFree(kv.second);
+  }
+  void* get(std::size_t bytes) {
+    auto it = free_.find(bytes);
+    if (it != free_.end()) {
+      void* p = it->second;
+      free_.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    return p;
+  }
+  void put(std::size_t bytes, void* p) { free_.emplace(bytes, p); }
+};
+BufCache& buf_cache() {
+  thread_local BufCache c;
+  return c;
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
-  explicit DevBuf(std::size_t n) {
-    if (n) cuda_check(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+  std::size_t bytes = 0;
+  explicit DevBuf(std::size_t n) : bytes(n * sizeof(T)) {
+    if (n) p = static_cast<T*>(buf_cache().get(bytes));
   }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) buf_cache().put(bytes, p);
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
