@@ -167,7 +167,8 @@ struct alignas(64) PackPoolArgs {
   float* norm2;                // optional: max squared row norm of src per frame-tile [slot][tile]
   long long norm2_head_stride; // elements
   // optional: the pooled block means themselves (avg_pool_blocks' final 1/count scale applied):
-  // p0 = S0 / (rows x cols of the tile), p1 = S1 / (2 x that), same layout as s0 / s1; pflag
+  // p0 = S0 / (rows x cols of the tile), p1 = S1 / (2 x that), channel-quad interleaved
+  // [slot][d/4][tile][4] (head stride as s0 / s1); pflag
   // [slot][tile] (stride norm2_head_stride) gets bit 0 / bit 1 when p0 / p1 has a non-finite
   // value (matmul's check_finite, P/src/tensor.cpp:126-127, without re-reading the rows)
   float* p0;
@@ -190,6 +191,12 @@ inline size_t pack_pool_smem(int d, int max_cnt, bool two) {
   return (size_t)max_cnt * (two ? 2 : 1) * 64 * d * 2 + 16 + 1024;  // + 1 KB: 128-byte-swizzle alignment
 }
 
+#ifndef FVSR_MS_WHOLE
+#define FVSR_MS_WHOLE 0
+#endif
+#ifndef FVSR_TOPK_MATCH
+#define FVSR_TOPK_MATCH 0
+#endif
 #ifndef FVSR_PP_EXP
 #define FVSR_PP_EXP 0  // experiment builds only (build_variant): 1 = ring pack data movement only
 #endif
@@ -354,14 +361,18 @@ __device__ __forceinline__ void pack_pool_body(const PackPoolArgs& a, const Pool
         const long long pofs = head * a.part_head_stride + (long long)slot * a.n_tiles * d + po;
         const float inv0 = __fdiv_rn(1.0f, (float)(hc * wc));
         const float m0x = __fmul_rn(s0x, inv0), m0y = __fmul_rn(s0y, inv0);
-        a.p0[pofs] = m0x;
-        a.p0[pofs + 1] = m0y;
+        // quad-interleaved [slot][c/4][tile][4]: a warp of the selector reading 32 consecutive
+        // tiles' channel quad is one contiguous 512-byte run
+        const long long qofs = head * a.part_head_stride + (((long long)slot * (d >> 2) + (c >> 2)) * a.n_tiles + tile) * 4 +
+                               (c & 3);
+        a.p0[qofs] = m0x;
+        a.p0[qofs + 1] = m0y;
         unsigned bad = (isfinite(m0x) && isfinite(m0y)) ? 0u : 1u;
         if (cont) {
           const float inv1 = __fdiv_rn(1.0f, (float)(2 * hc * wc));
           const float m1x = __fmul_rn(s1x, inv1), m1y = __fmul_rn(s1y, inv1);
-          a.p1[pofs] = m1x;
-          a.p1[pofs + 1] = m1y;
+          a.p1[qofs] = m1x;
+          a.p1[qofs + 1] = m1y;
           if (!(isfinite(m1x) && isfinite(m1y))) bad |= 2u;
         }
         if (bad && a.pflag) atomicOr(a.pflag + head * a.norm2_head_stride + (long long)slot * a.n_tiles + tile, bad);
@@ -556,14 +567,18 @@ __device__ __forceinline__ void pack_pool_tma(const PackPoolArgs& a, const PoolG
       if (a.p0) {  // block means: single-frame block of this frame; pair block ending here
         const float inv0 = __fdiv_rn(1.0f, (float)(hc * wc));
         const float m0x = __fmul_rn(s0x, inv0), m0y = __fmul_rn(s0y, inv0);
-        a.p0[pofs] = m0x;
-        a.p0[pofs + 1] = m0y;
+        // quad-interleaved [slot][c/4][tile][4]: a warp of the selector reading 32 consecutive
+        // tiles' channel quad is one contiguous 512-byte run
+        const long long qofs = head * a.part_head_stride + (((long long)slot * (d >> 2) + (c >> 2)) * a.n_tiles + tile) * 4 +
+                               (c & 3);
+        a.p0[qofs] = m0x;
+        a.p0[qofs + 1] = m0y;
         unsigned bad = (isfinite(m0x) && isfinite(m0y)) ? 0u : 1u;
         if (cont) {
           const float inv1 = __fdiv_rn(1.0f, (float)(2 * hc * wc));
           const float m1x = __fmul_rn(s1x, inv1), m1y = __fmul_rn(s1y, inv1);
-          a.p1[pofs] = m1x;
-          a.p1[pofs + 1] = m1y;
+          a.p1[qofs] = m1x;
+          a.p1[qofs + 1] = m1y;
           if (!(isfinite(m1x) && isfinite(m1y))) bad |= 2u;
         }
         if (bad && a.pflag) atomicOr(a.pflag + head * a.norm2_head_stride + (long long)slot * a.n_tiles + tile, bad);
@@ -744,6 +759,7 @@ struct SelectParams {
   const float* k_p1;
   const unsigned* k_flag;   // [slot][n_tiles] non-finite bits of k_p0 / k_p1
   long long k_flag_head_stride;
+
   float scale;
   long long topk;
   int cap;
@@ -912,9 +928,19 @@ __device__ __forceinline__ uint32_t kth_largest_radix(const uint32_t (&os)[NPER]
     reinterpret_cast<uint4*>(hist)[2 * lane] = make_uint4(0u, 0u, 0u, 0u);
     reinterpret_cast<uint4*>(hist)[2 * lane + 1] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
+#if FVSR_TOPK_MATCH
+#pragma unroll
+    for (int i = 0; i < NPER; ++i) {  // warp-aggregated: one atomic per distinct digit
+      const bool in = os[i] != 0u && (os[i] & pmask) == prefix;
+      const unsigned dgt = in ? (os[i] >> shift) & 255u : 256u;
+      const unsigned peers = __match_any_sync(0xffffffffu, dgt);
+      if (in && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&hist[dgt], (unsigned)__popc(peers));
+    }
+#else
 #pragma unroll
     for (int i = 0; i < NPER; ++i)
       if (os[i] != 0u && (os[i] & pmask) == prefix) atomicAdd(&hist[(os[i] >> shift) & 255u], 1u);
+#endif
     __syncwarp();
     const uint4 h0 = reinterpret_cast<const uint4*>(hist)[2 * lane];
     const uint4 h1 = reinterpret_cast<const uint4*>(hist)[2 * lane + 1];
@@ -984,6 +1010,9 @@ __device__ __forceinline__ void topk_core(const DevGeom& g, const DevMask& m, co
   if (!__any_sync(0xffffffffu, dg_ok)) dg = -1;
   const long long kp64 = p.topk - (dg >= 0 ? 1 : 0);
   const int kprime = kp64 > (long long)INT32_MAX ? INT32_MAX : (int)kp64;
+#ifdef FVSR_MS_TRACE
+  const long long tk1 = clock64();
+#endif
   uint32_t T = 1u;  // every candidate
   int take_eq = 1 << 30;
   if (kprime <= 0) {
@@ -1007,6 +1036,9 @@ __device__ __forceinline__ void topk_core(const DevGeom& g, const DevMask& m, co
     for (int i = 0; i < NPER; ++i) gt += __popc(__ballot_sync(0xffffffffu, os[i] > T));
     take_eq = kprime - gt;
   }
+#ifdef FVSR_MS_TRACE
+  const long long tk2 = clock64();
+#endif
   int* out = p.sel + row * p.cap;
   const unsigned lt = (1u << lane) - 1u;
   int total = 0, eq_seen = 0;
@@ -1030,6 +1062,11 @@ __device__ __forceinline__ void topk_core(const DevGeom& g, const DevMask& m, co
     if (p.diag) p.diag[row] = dg;
     if (total > p.cap) atomicOr(p.err, kErrInvariant);
   }
+#ifdef FVSR_MS_TRACE
+  const long long tk3 = clock64();
+  if (lane == 0 && blockIdx.x % 37 == 0 && (threadIdx.x >> 5) < 2)
+    printf("TK b%d w%d thr %lld emit %lld\n", blockIdx.x, threadIdx.x >> 5, tk2 - tk1, tk3 - tk2);
+#endif
 }
 
 // topk_core of a row whose scores are in memory (global or shared)
@@ -1149,8 +1186,14 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
                                                                     const __grid_constant__ DevMask m,
                                                                     const __grid_constant__ SelectParams p) {
   static_assert(kFrontQB >= 1 && kFrontQB <= 8 && kFrontQB * 32 <= kFrontThreads, "one warp per row for top-k");
+#ifdef FVSR_MS_TRACE
+  const long long tr0 = clock64();
+#endif
   pdl_wait();
   pdl_trigger();
+#ifdef FVSR_MS_TRACE
+  const long long tr1 = clock64();
+#endif
   extern __shared__ __align__(16) float sm_ms[];
   const int tid = threadIdx.x, warp = tid >> 5;
   const int per_head = (g.bnq + kFrontQB - 1) / kFrontQB;
@@ -1184,13 +1227,19 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
     qT[(4 * c4 + 3) * kFrontQP + r] = w.w;
   }
   __syncthreads();
+#ifdef FVSR_MS_TRACE
+  const long long tr2 = clock64();
+#endif
   for (int kb = tid; kb < bnk; kb += kFrontThreads) {
     const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
     const int kcnt = g.k_tr_count[ktr], kf = g.k_tr_first[ktr] + kcnt - 1;
     const long long slot_tile = (long long)g.k_slot[kf] * g.n_tiles + ktile;
     if (p.k_flag[head * p.k_flag_head_stride + slot_tile] & (kcnt == 2 ? 2u : 1u)) fin = false;
+    // block mean rows are channel-quad interleaved ([slot][d/4][tile][4]): quad j of this key
+    // block is kr[j * n_tiles], and the warp's 32 consecutive key blocks read one 512-byte run
     const float4* kr = reinterpret_cast<const float4*>((kcnt == 2 ? p.k_p1 : p.k_p0) + head * p.k_head_stride +
-                                                       slot_tile * d);
+                                                       ((long long)g.k_slot[kf] * d4 * g.n_tiles + ktile) * 4);
+    const int qs = g.n_tiles;  // float4 stride between channel quads
     float acc[kFrontQP];
 #pragma unroll
     for (int r = 0; r < kFrontQP; ++r) acc[r] = 0.0f;
@@ -1218,36 +1267,57 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
       for (int r = 0; r + 1 < kFrontQB; r += 2) padd_rn(acc[r], acc[r + 1], __fmul_rn(qv[r], k), __fmul_rn(qv[r + 1], k));
       if constexpr (kFrontQB & 1) acc[kFrontQB - 1] = __fadd_rn(acc[kFrontQB - 1], __fmul_rn(qv[kFrontQB - 1], k));
     };
+#if FVSR_MS_WHOLE
+    // the whole row in flight at once (one memory latency per key block), then the chains
+    float4 kv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) kv[j] = j < d4 ? __ldg(kr + (long long)j * qs) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j == 16 && d4 == 16) break;
+      channel(kv[j].x, 4 * j);
+      channel(kv[j].y, 4 * j + 1);
+      channel(kv[j].z, 4 * j + 2);
+      channel(kv[j].w, 4 * j + 3);
+    }
+#else
     // the row in batches of 8 channel quads, the next batch's loads in flight meanwhile
     float4 cur[8], nxt[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) cur[j] = j < d4 ? __ldg(kr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < 8; ++j) cur[j] = j < d4 ? __ldg(kr + (long long)j * qs) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
     for (int b = 0; b < d4; b += 8) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) nxt[j] = b + 8 + j < d4 ? __ldg(kr + b + 8 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < 8; ++j) nxt[j] = b + 8 + j < d4 ? __ldg(kr + (long long)(b + 8 + j) * qs) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (b + j < d4) {
-          const int c = 4 * (b + j);
-          channel(cur[j].x, c);
-          channel(cur[j].y, c + 1);
-          channel(cur[j].z, c + 2);
-          channel(cur[j].w, c + 3);
-        }
+      for (int j = 0; j < 8; ++j) {  // d4 is 16 or 32: every batch is whole (no branch between quads)
+        const int c = 4 * (b + j);
+        channel(cur[j].x, c);
+        channel(cur[j].y, c + 1);
+        channel(cur[j].z, c + 2);
+        channel(cur[j].w, c + 3);
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
     }
+#endif
 #pragma unroll
     for (int r = 0; r < kFrontQB; ++r) sc[r * bnk + kb] = __fmul_rn(acc[r], p.scale);
   }
   if (!fin) atomicOr(p.err, kErrShape);
   __syncthreads();
+#ifdef FVSR_MS_TRACE
+  const long long tr3 = clock64();
+#endif
 #if FVSR_MS_EXP == 1
   return;  // experiment: scores only
 #endif
   if (warp < nqb) topk_row<NPER>(g, m, p, qb0 + warp, head, sc + warp * bnk, hist + warp * 256);
+#ifdef FVSR_MS_TRACE
+  const long long tr4 = clock64();
+  if ((tid & 31) == 0 && blockIdx.x % 37 == 0 && warp < 2)
+    printf("MS b%d w%d wait %lld q %lld score %lld topk %lld\n", blockIdx.x, warp, tr1 - tr0, tr2 - tr1, tr3 - tr2, tr4 - tr3);
+#endif
 }
 
 // ---------------------------------------------------------------------------------------
