@@ -893,10 +893,12 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
               // allowed query cols / rows of the 8x8 query tile, closed form (window_bits)
               const uint32_t hb = window_bits(m.mode, kh, qh0, m.extent_h, g.rows);
               const uint32_t wb = window_bits(m.mode, kw, qw0, m.extent_w, g.cols);
-              // 64-bit tile mask: byte r (query tile row r) = wb where hb has bit r
-              unsigned long long rows64 = 0;
-#pragma unroll
-              for (int r = 0; r < 8; ++r) rows64 |= ((hb >> r) & 1u) ? (0xffull << (8 * r)) : 0ull;
+              // 64-bit tile mask: byte r (query tile row r) = wb where hb has bit r (bit r of
+              // hb spread to byte r, then any nonzero byte widened to 0xff without carries)
+              unsigned long long rows64 = ((unsigned long long)(hb & 0xffu) * 0x0101010101010101ull) &
+                                          0x8040201008040201ull;
+              rows64 = (((rows64 + 0x7f7f7f7f7f7f7f7full) | rows64) & 0x8080808080808080ull) >> 7;
+              rows64 *= 0xffull;
               const unsigned long long m64 = rows64 & ((unsigned long long)wb * 0x0101010101010101ull);
 #pragma unroll
               for (int w = 0; w < kW; ++w) mk[w] = (uint32_t)(m64 >> ((col0 + 32 * w) & 63)) & qvalid[w];

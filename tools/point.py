@@ -25,5 +25,10 @@ a = ap.parse_args()
 m = fv.Mask.all_allowed()
 if a.mask and a.mask[0] == "loc":
     m = fv.Mask.locality(int(a.mask[1]), int(a.mask[2]), truncated=a.mask[3] == "trunc")
+ctx = fv.Context.default()
+ctx.read_tiles()
 r = run_point(a.rows, a.cols, a.heads, 128, 4, a.topk, m, layers=2, steps=a.steps, warmup=2)
+tiles, full = ctx.read_tiles()
+r["tiles_per_step"] = tiles / (2 * a.steps + 2)  # timed loop + span pass + warm-up steps
+r["full_tiles_per_step"] = full / (2 * a.steps + 2)
 print(r)
