@@ -472,9 +472,6 @@ EncodeTiledFn encode_tiled_fn() {
 bool encode_src_map(CUtensorMap* m, const void* src, int d, int rows, int cols, int frames, int heads,
                     long long token_stride, long long head_stride) {
   EncodeTiledFn fn = encode_tiled_fn();
-#ifdef FVSR_NO_TMA_PACK
-  fn = nullptr;  // experiment builds only: keep the bulk-copy pack/pool path
-#endif
   if (!fn || !src || (d != 64 && d != 128)) return false;
   const long long ts = token_stride ? token_stride : d;
   const long long fs = (long long)rows * cols * ts;

@@ -120,9 +120,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // hardware park the waiting thread until the phase flips instead of spinning (a spinning
 // waiter steals issue slots from the warps doing the work).  A watchdog turns a protocol
 // deadlock into a trap instead of a hung device.
-#ifndef FVSR_MBAR_TEST_FIRST
-#define FVSR_MBAR_TEST_FIRST 0
-#endif
 // Wait for a phase that is far away (e.g. a whole unit): poll with test_wait and sleep in
 // between instead of the try_wait suspend, which wakes on every barrier event of the CTA and
 // would steal issue slots from the warps on the critical path.
@@ -154,9 +151,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return done != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#if FVSR_MBAR_TEST_FIRST
-  if (mbar_test(bar, parity)) return;
-#endif
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
   for (int it = 0;; ++it) {

@@ -191,15 +191,6 @@ inline size_t pack_pool_smem(int d, int max_cnt, bool two) {
   return (size_t)max_cnt * (two ? 2 : 1) * 64 * d * 2 + 16 + 1024;  // + 1 KB: 128-byte-swizzle alignment
 }
 
-#ifndef FVSR_MS_WHOLE
-#define FVSR_MS_WHOLE 0
-#endif
-#ifndef FVSR_TOPK_MATCH
-#define FVSR_TOPK_MATCH 0
-#endif
-#ifndef FVSR_PP_EXP
-#define FVSR_PP_EXP 0  // experiment builds only (build_variant): 1 = ring pack data movement only
-#endif
 
 // Packed fp32 pair add (FADD2): {a0, a1} += {b0, b1}, each lane rounded exactly as add.rn.f32.
 // (A packed multiply feeding it gets contracted into FFMA2 by ptxas, so the products stay
@@ -523,12 +514,8 @@ __device__ __forceinline__ void pack_pool_tma(const PackPoolArgs& a, const PoolG
     }
     __syncthreads();
   }
-#if FVSR_PP_EXP == 1
-  if (0) {  // experiment: data movement only
-#else
   // pooling: channels 2t, 2t+1 in exact token order (rows past the frame skipped)
   if (a.s0 && 2 * tid < d) {
-#endif
     const int c = 2 * tid;
     const long long po = (long long)tile * d + c;
     const bool ext = cnt == 1 && es >= 0 && a.ext_s0 != nullptr;
@@ -590,7 +577,7 @@ __device__ __forceinline__ void pack_pool_tma(const PackPoolArgs& a, const PoolG
     }
   }
   // |row| bounds of src (max squared row norm per frame-tile): two threads per row
-  if (a.norm2 && FVSR_PP_EXP != 1) {
+  if (a.norm2) {
     __shared__ float wmax_t[kPPThreads / 32];
     const int r = tid >> 1, half = tid & 1, cpt = d >> 1;  // channels per thread
     for (int fi = 0; fi < cnt; ++fi) {
@@ -928,19 +915,9 @@ __device__ __forceinline__ uint32_t kth_largest_radix(const uint32_t (&os)[NPER]
     reinterpret_cast<uint4*>(hist)[2 * lane] = make_uint4(0u, 0u, 0u, 0u);
     reinterpret_cast<uint4*>(hist)[2 * lane + 1] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
-#if FVSR_TOPK_MATCH
-#pragma unroll
-    for (int i = 0; i < NPER; ++i) {  // warp-aggregated: one atomic per distinct digit
-      const bool in = os[i] != 0u && (os[i] & pmask) == prefix;
-      const unsigned dgt = in ? (os[i] >> shift) & 255u : 256u;
-      const unsigned peers = __match_any_sync(0xffffffffu, dgt);
-      if (in && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&hist[dgt], (unsigned)__popc(peers));
-    }
-#else
 #pragma unroll
     for (int i = 0; i < NPER; ++i)
       if (os[i] != 0u && (os[i] & pmask) == prefix) atomicAdd(&hist[(os[i] >> shift) & 255u], 1u);
-#endif
     __syncwarp();
     const uint4 h0 = reinterpret_cast<const uint4*>(hist)[2 * lane];
     const uint4 h1 = reinterpret_cast<const uint4*>(hist)[2 * lane + 1];
@@ -1010,9 +987,6 @@ __device__ __forceinline__ void topk_core(const DevGeom& g, const DevMask& m, co
   if (!__any_sync(0xffffffffu, dg_ok)) dg = -1;
   const long long kp64 = p.topk - (dg >= 0 ? 1 : 0);
   const int kprime = kp64 > (long long)INT32_MAX ? INT32_MAX : (int)kp64;
-#ifdef FVSR_MS_TRACE
-  const long long tk1 = clock64();
-#endif
   uint32_t T = 1u;  // every candidate
   int take_eq = 1 << 30;
   if (kprime <= 0) {
@@ -1036,9 +1010,6 @@ __device__ __forceinline__ void topk_core(const DevGeom& g, const DevMask& m, co
     for (int i = 0; i < NPER; ++i) gt += __popc(__ballot_sync(0xffffffffu, os[i] > T));
     take_eq = kprime - gt;
   }
-#ifdef FVSR_MS_TRACE
-  const long long tk2 = clock64();
-#endif
   int* out = p.sel + row * p.cap;
   const unsigned lt = (1u << lane) - 1u;
   int total = 0, eq_seen = 0;
@@ -1062,11 +1033,6 @@ __device__ __forceinline__ void topk_core(const DevGeom& g, const DevMask& m, co
     if (p.diag) p.diag[row] = dg;
     if (total > p.cap) atomicOr(p.err, kErrInvariant);
   }
-#ifdef FVSR_MS_TRACE
-  const long long tk3 = clock64();
-  if (lane == 0 && blockIdx.x % 37 == 0 && (threadIdx.x >> 5) < 2)
-    printf("TK b%d w%d thr %lld emit %lld\n", blockIdx.x, threadIdx.x >> 5, tk2 - tk1, tk3 - tk2);
-#endif
 }
 
 // topk_core of a row whose scores are in memory (global or shared)
@@ -1113,10 +1079,7 @@ __global__ void __launch_bounds__(kTopkWarps * 32) topk_select_kernel(const __gr
 //                      kFrontKC-block chunks (exact sequential chains, P/src/tensor.cpp:121-151,
 //                      sparse.cpp:97-99), top-k with the forced diagonal (topk_row).
 // ---------------------------------------------------------------------------------------
-#ifndef FVSR_FRONT_QB
-#define FVSR_FRONT_QB 6
-#endif
-constexpr int kFrontQB = FVSR_FRONT_QB;  // q-blocks (pooled query rows) per mask-select block
+constexpr int kFrontQB = 6;  // q-blocks (pooled query rows) per mask-select block (2-8 measured; 6 fills 132 SMs)
 constexpr int kFrontQP = kFrontQB <= 2 ? 2 : (kFrontQB <= 4 ? 4 : 8);  // query slots per channel (transposed tile)
 constexpr int kFrontThreads = 256; // one key block per thread (strided past 256)
 
@@ -1186,14 +1149,8 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
                                                                     const __grid_constant__ DevMask m,
                                                                     const __grid_constant__ SelectParams p) {
   static_assert(kFrontQB >= 1 && kFrontQB <= 8 && kFrontQB * 32 <= kFrontThreads, "one warp per row for top-k");
-#ifdef FVSR_MS_TRACE
-  const long long tr0 = clock64();
-#endif
   pdl_wait();
   pdl_trigger();
-#ifdef FVSR_MS_TRACE
-  const long long tr1 = clock64();
-#endif
   extern __shared__ __align__(16) float sm_ms[];
   const int tid = threadIdx.x, warp = tid >> 5;
   const int per_head = (g.bnq + kFrontQB - 1) / kFrontQB;
@@ -1227,9 +1184,6 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
     qT[(4 * c4 + 3) * kFrontQP + r] = w.w;
   }
   __syncthreads();
-#ifdef FVSR_MS_TRACE
-  const long long tr2 = clock64();
-#endif
   for (int kb = tid; kb < bnk; kb += kFrontThreads) {
     const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
     const int kcnt = g.k_tr_count[ktr], kf = g.k_tr_first[ktr] + kcnt - 1;
@@ -1244,10 +1198,6 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
 #pragma unroll
     for (int r = 0; r < kFrontQP; ++r) acc[r] = 0.0f;
     auto channel = [&](float k, int c) {
-#if FVSR_MS_EXP == 2
-      acc[0] = __fadd_rn(acc[0], k);  // experiment: no chains
-      return;
-#endif
       float qv[kFrontQP];
       if constexpr (kFrontQP == 2) {
         const float2 t = *reinterpret_cast<const float2*>(qT + c * kFrontQP);
@@ -1267,20 +1217,6 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
       for (int r = 0; r + 1 < kFrontQB; r += 2) padd_rn(acc[r], acc[r + 1], __fmul_rn(qv[r], k), __fmul_rn(qv[r + 1], k));
       if constexpr (kFrontQB & 1) acc[kFrontQB - 1] = __fadd_rn(acc[kFrontQB - 1], __fmul_rn(qv[kFrontQB - 1], k));
     };
-#if FVSR_MS_WHOLE
-    // the whole row in flight at once (one memory latency per key block), then the chains
-    float4 kv[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) kv[j] = j < d4 ? __ldg(kr + (long long)j * qs) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j == 16 && d4 == 16) break;
-      channel(kv[j].x, 4 * j);
-      channel(kv[j].y, 4 * j + 1);
-      channel(kv[j].z, 4 * j + 2);
-      channel(kv[j].w, 4 * j + 3);
-    }
-#else
     // the row in batches of 8 channel quads, the next batch's loads in flight meanwhile
     float4 cur[8], nxt[8];
 #pragma unroll
@@ -1300,24 +1236,12 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
 #pragma unroll
       for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
     }
-#endif
 #pragma unroll
     for (int r = 0; r < kFrontQB; ++r) sc[r * bnk + kb] = __fmul_rn(acc[r], p.scale);
   }
   if (!fin) atomicOr(p.err, kErrShape);
   __syncthreads();
-#ifdef FVSR_MS_TRACE
-  const long long tr3 = clock64();
-#endif
-#if FVSR_MS_EXP == 1
-  return;  // experiment: scores only
-#endif
   if (warp < nqb) topk_row<NPER>(g, m, p, qb0 + warp, head, sc + warp * bnk, hist + warp * 256);
-#ifdef FVSR_MS_TRACE
-  const long long tr4 = clock64();
-  if ((tid & 31) == 0 && blockIdx.x % 37 == 0 && warp < 2)
-    printf("MS b%d w%d wait %lld q %lld score %lld topk %lld\n", blockIdx.x, warp, tr1 - tr0, tr2 - tr1, tr3 - tr2, tr4 - tr3);
-#endif
 }
 
 // ---------------------------------------------------------------------------------------
