@@ -98,8 +98,10 @@ typedef struct {
   int64_t words_per_row; /* FVSR_MASK_BITMASK only: (Lk + 63) / 64 */
 } fvsr_mask;
 
-/* FVSR_FLAG_SYNC_CHECK: synchronize and check the device error word after every call. */
-enum { FVSR_FLAG_SYNC_CHECK = 1 };
+/* FVSR_FLAG_SYNC_CHECK: synchronize and check the device error word after every call.
+ * FVSR_FLAG_NO_TMA: stage the ring append / query pack with 1-D bulk copies instead of
+ * tensor-map TMA (the fallback when the driver's tensor-map entry point is unavailable). */
+enum { FVSR_FLAG_SYNC_CHECK = 1, FVSR_FLAG_NO_TMA = 2 };
 
 /* Output layouts of fvsr_ring_attention. */
 enum {
@@ -125,7 +127,7 @@ FVSR_API const char* fvsr_last_error(void);
 /* Binds to the current CUDA device; fails with FVSR_E_CUDA unless it is sm_100. */
 FVSR_API int32_t fvsr_ctx_create(fvsr_ctx** out);
 FVSR_API void fvsr_ctx_destroy(fvsr_ctx* ctx);
-/* Call flags (FVSR_FLAG_SYNC_CHECK) applied to every later call on this context. */
+/* Call flags (FVSR_FLAG_*) applied to every later call on this context. */
 FVSR_API int32_t fvsr_ctx_set_flags(fvsr_ctx* ctx, int32_t flags);
 /* Synchronizes `stream`, reads and clears the device error word. */
 FVSR_API int32_t fvsr_check_errors(fvsr_ctx* ctx, fvsr_stream_t stream);

@@ -469,8 +469,9 @@ EncodeTiledFn encode_tiled_fn() {
   }();
   return fn;
 }
-bool encode_src_map(CUtensorMap* m, const void* src, int d, int rows, int cols, int frames, int heads,
-                    long long token_stride, long long head_stride) {
+bool encode_src_map(const fvsr_ctx* ctx, CUtensorMap* m, const void* src, int d, int rows, int cols, int frames,
+                    int heads, long long token_stride, long long head_stride) {
+  if (ctx->flags & FVSR_FLAG_NO_TMA) return false;
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn || !src || (d != 64 && d != 128)) return false;
   const long long ts = token_stride ? token_stride : d;
@@ -1161,8 +1162,8 @@ int ring_append_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, int frame_id, const
   a.n_tiles = r->n_tiles;
   a.d = r->d;
   FVSR_TRY(rope_args(r, &frame_id, 1, a));
-  a.use_tma = encode_src_map(&a.tm, a.src, r->d, r->rows, r->cols, 1, r->heads, 0, a.src_head_stride) &&
-              encode_src_map(&a.tm2, a.src2, r->d, r->rows, r->cols, 1, r->heads, 0, a.src_head_stride);
+  a.use_tma = encode_src_map(ctx, &a.tm, a.src, r->d, r->rows, r->cols, 1, r->heads, 0, a.src_head_stride) &&
+              encode_src_map(ctx, &a.tm2, a.src2, r->d, r->rows, r->cols, 1, r->heads, 0, a.src_head_stride);
   PoolGroups pg{};
   pg.first[0] = 0;
   pg.count[0] = 1;
@@ -1333,7 +1334,7 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
       a.n_tiles = r->n_tiles;
       a.d = d;
       FVSR_TRY(rope_args(r, &app->frame_id, 1, a));
-      a.use_tma = encode_src_map(&a.tm, a.src, d, r->rows, r->cols, 1, r->heads, a.src_token_stride, a.src_head_stride);
+      a.use_tma = encode_src_map(ctx, &a.tm, a.src, d, r->rows, r->cols, 1, r->heads, a.src_token_stride, a.src_head_stride);
       fa.kv_pg.first[0] = 0;
       fa.kv_pg.count[0] = 1;
       fa.kv_pg.ext_slot[0] = partner;
@@ -1348,7 +1349,7 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
       av.norm2 = nullptr;
       av.p0 = av.p1 = nullptr;
       av.pflag = nullptr;
-      av.use_tma = encode_src_map(&av.tm, av.src, d, r->rows, r->cols, 1, r->heads, av.src_token_stride,
+      av.use_tma = encode_src_map(ctx, &av.tm, av.src, d, r->rows, r->cols, 1, r->heads, av.src_token_stride,
                                   av.src_head_stride);
       if ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(av.src)) % 16 != 0)
         return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
@@ -1373,7 +1374,7 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
     if (reinterpret_cast<uintptr_t>(q) % 16 != 0)
       return fail(FVSR_E_CONFIG, "pack_pool: token-major inputs must be 16-byte aligned");
     FVSR_TRY(rope_args(r, q_frame_ids, nq, a));
-    a.use_tma = encode_src_map(&a.tm, q, d, g.rows, g.cols, g.nqf, r->heads, a.src_token_stride, a.src_head_stride);
+    a.use_tma = encode_src_map(ctx, &a.tm, q, d, g.rows, g.cols, g.nqf, r->heads, a.src_token_stride, a.src_head_stride);
     int max_cnt = 1;
     for (int t = 0; t < g.nq_trows; ++t) {
       fa.q_pg.first[t] = g.q_tr_first[t];

@@ -159,7 +159,7 @@ class Context:
         return int(self.lib.fvsr_ctx_launch_count(self.h))
 
     def set_flags(self, flags: int) -> None:
-        """fvsr_ctx_set_flags: FLAG_SYNC_CHECK (see include/fvsr_b200.h)."""
+        """fvsr_ctx_set_flags: FLAG_SYNC_CHECK | FLAG_NO_TMA (see include/fvsr_b200.h)."""
         self.flags = int(flags)
         check(self.lib.fvsr_ctx_set_flags(self.h, int(flags)))
 

@@ -59,6 +59,57 @@ def test_fused_step_equals_separate_calls(rows, cols, heads, d, topk, window, ma
     assert a.frame_ids(0) == b.frame_ids(0)
 
 
+@pytest.mark.parametrize("rows,cols,heads,d,topk,mask,rope,tq", [
+    (48, 88, 4, 128, 27, None, False, 1),
+    (20, 28, 2, 64, 3, ("loc", 7, 9, False), True, 1),
+    (18, 30, 2, 128, 4, None, True, 2),
+])
+def test_bulk_copy_pack_matches_tma_pack(rows, cols, heads, d, topk, mask, rope, tq):
+    """The ring append / query pack staged with 1-D bulk copies (FVSR_FLAG_NO_TMA, the
+    fallback without the driver's tensor-map entry point) against the tensor-map TMA path:
+    the same ring contents, so identical selections and outputs within the bf16 tolerance
+    (the |k| bounds are summed in a different order; they only pick the softmax mode)."""
+    N = rows * cols
+    window = 4
+    m = fv.Mask.all_allowed() if mask is None else fv.Mask.locality(mask[1], mask[2], truncated=mask[3])
+    bulk_ctx = fv.Context()
+    bulk_ctx.set_flags(fv._abi.FLAG_NO_TMA)
+    a = fv.KVRing(1, heads, d, rows, cols, window + tq)
+    b = fv.KVRing(1, heads, d, rows, cols, window + tq, ctx=bulk_ctx)
+    if rope:
+        a.set_rope()
+        b.set_rope()
+    port = oracle.Port()
+    qprev = None
+    for t in range(7):
+        x = oracle.bf16_round(np.stack([port.gaussian(900 + 10 * t + h, 3 * N * d).reshape(3, N, d)
+                                        for h in range(heads)]))
+        q, k, v = to_dev(x[:, 0]), to_dev(x[:, 1]), to_dev(x[:, 2])
+        qids = [t] if tq == 1 or t % 2 == 0 else [t - 1, t]
+        if len(qids) == 2:
+            q = torch.cat([qprev, q], dim=1)
+        if tq == 1 or len(qids) == 2:
+            bnq, bnk = fv.block_counts(fv.TokenGrid(qids, rows, cols),
+                                       fv.TokenGrid(a.frame_ids(0) + [t], rows, cols))
+            cap = min(topk, bnk)
+            sa = torch.empty((heads, bnq, cap), dtype=torch.int32, device="cuda")
+            sb = torch.empty_like(sa)
+            oa = a.step(0, t, k, v, q, qids, m, topk, sel=sa, sel_count=torch.empty((heads, bnq), dtype=torch.int32,
+                                                                                   device="cuda"))
+            ob = b.step(0, t, k, v, q, qids, m, topk, sel=sb, sel_count=torch.empty((heads, bnq), dtype=torch.int32,
+                                                                                   device="cuda"))
+            assert torch.equal(sa, sb), f"t={t}: selections differ"
+            oa, ob = oa.float().cpu().numpy(), ob.float().cpu().numpy()
+            assert rel_l2(ob, oa) <= REL_L2_TOL and max_abs(ob, oa) <= MAX_ABS_TOL, t
+        else:
+            a.append(0, t, k, v)
+            b.append(0, t, k, v)
+        qprev = to_dev(x[:, 0])
+        a.evict(0, window)
+        b.evict(0, window)
+    bulk_ctx.check_errors()
+
+
 def test_fused_step_matches_oracle_768x1408():
     """BASELINE config #2 through fvsr_ring_step: indices bit-exact and output within tolerance."""
     rows, cols, d, heads, topk, window = 48, 88, 128, 12, 27, 4
