@@ -334,6 +334,8 @@ def run_b200(args):
     pairs_span = ctx.read_pairs()
     tiles_span, full_span = ctx.read_tiles()
     attn_ms, attn_n = ctx.timing_read(_abi.TIME_ATTENTION)
+    pk_ms, pk_n = ctx.timing_read(_abi.TIME_PACK)
+    se_ms, se_n = ctx.timing_read(_abi.TIME_SELECT)
     fr_ms, fr_n = ctx.timing_read(_abi.TIME_FRONT, clear=True)
     # the same step with the paper's locality window at 768x1408 (48x72 latent tokens, truncated;
     # SURVEY 8(d)), measured the same way (spans + kernel-counted pairs)
@@ -511,6 +513,15 @@ def run_b200(args):
              "algorithmic_bytes": ap_bytes + mb_bytes,
              "gbs": (ap_bytes + mb_bytes) / (fr_avg / 1e3) / 1e9 if fr_avg > 0 else None, "peak_gbs": pk["hbm_gbs"],
              "frac": (ap_bytes + mb_bytes) / (fr_avg / 1e3) / 1e9 / pk["hbm_gbs"] if fr_avg > 0 else None}
+    # per launch: the append + query pack is an HBM copy (bound: HBM); the selector reads only
+    # the pooled rows and is latency-bound (its bytes are reported, not a bound)
+    pack_bytes = 2 * 2 * nh * N * D * 2 + 2 * nh * N * D * 2 + nh * tiles * D * 4 * 5
+    sel_bytes = nh * bnk * D * 4 + nh * tiles * D * 4 + nh * tiles * TOPK * 4
+    for name, ms, n, nbytes in (("ring_pack", pk_ms, pk_n, pack_bytes), ("mask_select", se_ms, se_n, sel_bytes)):
+        avg = ms / max(1, n)
+        front[name] = {"avg_us": avg * 1e3, "algorithmic_bytes": nbytes,
+                       "gbs": nbytes / (avg / 1e3) / 1e9 if avg > 0 else None,
+                       "frac_of_hbm": nbytes / (avg / 1e3) / 1e9 / pk["hbm_gbs"] if avg > 0 else None}
 
     # ---- CPU baseline (reference on host cores, rank 0, N=1 only) ----------------------------
     cpu = None

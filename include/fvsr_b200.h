@@ -113,8 +113,17 @@ enum {
 /* Eviction strategies == vsr::EvictStrategy (P/include/vsr/kv_cache.hpp:12). */
 enum { FVSR_EVICT_SLIDING = 0, FVSR_EVICT_UNIFORM = 1, FVSR_EVICT_HEAD_WISE = 2 };
 
-/* Kernel classes timed by fvsr_ctx_timing_enable. */
-enum { FVSR_TIME_APPEND = 0, FVSR_TIME_MASK_BUILDER = 1, FVSR_TIME_ATTENTION = 2, FVSR_TIME_FRONT = 3 };
+/* Kernel classes timed by fvsr_ctx_timing_enable.  A ring step's front (FVSR_TIME_FRONT) is
+ * also split into its two launches: FVSR_TIME_PACK (ring append + query pack) and
+ * FVSR_TIME_SELECT (coarse scores + top-k). */
+enum {
+  FVSR_TIME_APPEND = 0,
+  FVSR_TIME_MASK_BUILDER = 1,
+  FVSR_TIME_ATTENTION = 2,
+  FVSR_TIME_FRONT = 3,
+  FVSR_TIME_PACK = 4,
+  FVSR_TIME_SELECT = 5
+};
 
 typedef struct fvsr_ctx fvsr_ctx;
 typedef struct fvsr_ring fvsr_ring;

@@ -28,7 +28,7 @@ LOCALITY_PRESERVED, LOCALITY_TRUNCATED = 0, 1
 FLAG_SYNC_CHECK = 1
 FLAG_NO_TMA = 2
 OUT_TOKEN_MAJOR, OUT_TILE_MAJOR = 0, 1
-TIME_APPEND, TIME_MASK_BUILDER, TIME_ATTENTION, TIME_FRONT = 0, 1, 2, 3
+TIME_APPEND, TIME_MASK_BUILDER, TIME_ATTENTION, TIME_FRONT, TIME_PACK, TIME_SELECT = 0, 1, 2, 3, 4, 5
 
 
 class Error(RuntimeError):

@@ -1415,7 +1415,10 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
     auto kp = r->rope ? ring_pack_kernel<true> : ring_pack_kernel<false>;
     FVSR_TRY(ensure_smem(kp, smem_p));
     FVSR_TRY(ensure_carveout(kp));  // 12 blocks of ~18 KB resident per SM
-    FVSR_CUDA(launch_k(kp, dim3(grid_p), dim3(kPPThreads), smem_p, s, fa));
+    {
+      SpanGuard sp(ctx, s, FVSR_TIME_PACK);
+      FVSR_CUDA(launch_k(kp, dim3(grid_p), dim3(kPPThreads), smem_p, s, fa));
+    }
     if (ctx->flags & FVSR_FLAG_SYNC_CHECK) {
       const cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) return fail(FVSR_E_CUDA, "ring_pack kernel: %s", cudaGetErrorString(e));
@@ -1428,6 +1431,7 @@ int ring_step_view(fvsr_ctx* ctx, fvsr_ring* r, int layer, const uint16_t* q, co
       FVSR_CUDA(launch_kp(true, kern, dim3(grid_s), dim3(kFrontThreads), smem_s, s, g, dm, p));
       return FVSR_OK;
     };
+    SpanGuard ss(ctx, s, FVSR_TIME_SELECT);
     if (smem_s <= 200 * 1024) {
       st = g.bnk <= 256 ? launch_s(mask_select_kernel<8>)
                         : (g.bnk <= 1024 ? launch_s(mask_select_kernel<32>) : launch_s(mask_select_kernel<128>));
