@@ -1184,20 +1184,31 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
     qT[(4 * c4 + 3) * kFrontQP + r] = w.w;
   }
   __syncthreads();
-  for (int kb = tid; kb < bnk; kb += kFrontThreads) {
-    const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
-    const int kcnt = g.k_tr_count[ktr], kf = g.k_tr_first[ktr] + kcnt - 1;
-    const long long slot_tile = (long long)g.k_slot[kf] * g.n_tiles + ktile;
-    if (p.k_flag[head * p.k_flag_head_stride + slot_tile] & (kcnt == 2 ? 2u : 1u)) fin = false;
-    // block mean rows are channel-quad interleaved ([slot][d/4][tile][4]): quad j of this key
-    // block is kr[j * n_tiles], and the warp's 32 consecutive key blocks read one 512-byte run
-    const float4* kr = reinterpret_cast<const float4*>((kcnt == 2 ? p.k_p1 : p.k_p0) + head * p.k_head_stride +
-                                                       ((long long)g.k_slot[kf] * d4 * g.n_tiles + ktile) * 4);
-    const int qs = g.n_tiles;  // float4 stride between channel quads
-    float acc[kFrontQP];
+  // NK key blocks of this thread scored together: one load of each channel's queries serves
+  // NK * kFrontQB chains (bnk > 256: 2 keys per pass; the headline's bnk <= 256 has one)
+  auto score = [&](auto nk_tag, int kb0) {
+    constexpr int NK = decltype(nk_tag)::value;
+    constexpr int kBatch = NK == 1 ? 8 : 4;  // channel quads per key in flight per batch
+    const float4* kr[NK];
 #pragma unroll
-    for (int r = 0; r < kFrontQP; ++r) acc[r] = 0.0f;
-    auto channel = [&](float k, int c) {
+    for (int e = 0; e < NK; ++e) {
+      const int kb = kb0 + e * kFrontThreads;
+      const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
+      const int kcnt = g.k_tr_count[ktr], kf = g.k_tr_first[ktr] + kcnt - 1;
+      const long long slot_tile = (long long)g.k_slot[kf] * g.n_tiles + ktile;
+      if (p.k_flag[head * p.k_flag_head_stride + slot_tile] & (kcnt == 2 ? 2u : 1u)) fin = false;
+      // block mean rows are channel-quad interleaved ([slot][d/4][tile][4]): quad j of this key
+      // block is kr[j * n_tiles], and the warp's 32 consecutive key blocks read one 512-byte run
+      kr[e] = reinterpret_cast<const float4*>((kcnt == 2 ? p.k_p1 : p.k_p0) + head * p.k_head_stride +
+                                              ((long long)g.k_slot[kf] * d4 * g.n_tiles + ktile) * 4);
+    }
+    const int qs = g.n_tiles;  // float4 stride between channel quads
+    float acc[NK][kFrontQP];
+#pragma unroll
+    for (int e = 0; e < NK; ++e)
+#pragma unroll
+      for (int r = 0; r < kFrontQP; ++r) acc[e][r] = 0.0f;
+    auto channel = [&](const float (&k)[NK], int c) {
       float qv[kFrontQP];
       if constexpr (kFrontQP == 2) {
         const float2 t = *reinterpret_cast<const float2*>(qT + c * kFrontQP);
@@ -1214,31 +1225,56 @@ __global__ void __launch_bounds__(kFrontThreads) mask_select_kernel(const __grid
         }
       }
 #pragma unroll
-      for (int r = 0; r + 1 < kFrontQB; r += 2) padd_rn(acc[r], acc[r + 1], __fmul_rn(qv[r], k), __fmul_rn(qv[r + 1], k));
-      if constexpr (kFrontQB & 1) acc[kFrontQB - 1] = __fadd_rn(acc[kFrontQB - 1], __fmul_rn(qv[kFrontQB - 1], k));
+      for (int e = 0; e < NK; ++e) {
+#pragma unroll
+        for (int r = 0; r + 1 < kFrontQB; r += 2)
+          padd_rn(acc[e][r], acc[e][r + 1], __fmul_rn(qv[r], k[e]), __fmul_rn(qv[r + 1], k[e]));
+        if constexpr (kFrontQB & 1)
+          acc[e][kFrontQB - 1] = __fadd_rn(acc[e][kFrontQB - 1], __fmul_rn(qv[kFrontQB - 1], k[e]));
+      }
     };
-    // the row in batches of 8 channel quads, the next batch's loads in flight meanwhile
-    float4 cur[8], nxt[8];
+    // the rows in batches of channel quads, the next batch's loads in flight meanwhile
+    float4 cur[NK][kBatch], nxt[NK][kBatch];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) cur[j] = j < d4 ? __ldg(kr + (long long)j * qs) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = 0; e < NK; ++e)
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) cur[e][j] = __ldg(kr[e] + (long long)j * qs);
 #pragma unroll 1
-    for (int b = 0; b < d4; b += 8) {
+    for (int b = 0; b < d4; b += kBatch) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) nxt[j] = b + 8 + j < d4 ? __ldg(kr + (long long)(b + 8 + j) * qs) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int e = 0; e < NK; ++e)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {  // d4 is 16 or 32: every batch is whole (no branch between quads)
+        for (int j = 0; j < kBatch; ++j)
+          nxt[e][j] = b + kBatch + j < d4 ? __ldg(kr[e] + (long long)(b + kBatch + j) * qs) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {  // d4 is 16 or 32: every batch is whole (no branch between quads)
         const int c = 4 * (b + j);
-        channel(cur[j].x, c);
-        channel(cur[j].y, c + 1);
-        channel(cur[j].z, c + 2);
-        channel(cur[j].w, c + 3);
+        float kx[NK], ky[NK], kz[NK], kw[NK];
+#pragma unroll
+        for (int e = 0; e < NK; ++e) {
+          kx[e] = cur[e][j].x;
+          ky[e] = cur[e][j].y;
+          kz[e] = cur[e][j].z;
+          kw[e] = cur[e][j].w;
+        }
+        channel(kx, c);
+        channel(ky, c + 1);
+        channel(kz, c + 2);
+        channel(kw, c + 3);
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
+      for (int e = 0; e < NK; ++e)
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) cur[e][j] = nxt[e][j];
     }
 #pragma unroll
-    for (int r = 0; r < kFrontQB; ++r) sc[r * bnk + kb] = __fmul_rn(acc[r], p.scale);
-  }
+    for (int e = 0; e < NK; ++e)
+#pragma unroll
+      for (int r = 0; r < kFrontQB; ++r) sc[r * bnk + kb0 + e * kFrontThreads] = __fmul_rn(acc[e][r], p.scale);
+  };
+  int kb = tid;
+  for (; kb + kFrontThreads < bnk; kb += 2 * kFrontThreads) score(std::integral_constant<int, 2>{}, kb);
+  if (kb < bnk) score(std::integral_constant<int, 1>{}, kb);
   if (!fin) atomicOr(p.err, kErrShape);
   __syncthreads();
   if (warp < nqb) topk_row<NPER>(g, m, p, qb0 + warp, head, sc + warp * bnk, hist + warp * 256);
