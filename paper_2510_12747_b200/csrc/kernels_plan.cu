@@ -968,11 +968,38 @@ __device__ __forceinline__ void topk_core(const DevGeom& g, const DevMask& m, co
   uint32_t os[NPER];
   bool dg_ok = false;
   int n_cand = 0;
+  // Locality window: coarse-allowed depends on the (query tile, key tile) pair only, so the
+  // row's allowed key tiles are one bit table (in the radix histogram's space, which is not in
+  // use yet), built 32 tiles per step; the candidates then walk their key tile incrementally
+  const bool loc_table = m.kind == 1 && hist != nullptr && g.n_tiles <= 32 * 256;
+  int kt = lane % g.n_tiles;  // key tile of candidate kb = 32 * i + lane
+  if (loc_table) {
+    const int qh0 = 8 * (qtile / g.tiles_w), qw0 = 8 * (qtile % g.tiles_w);
+    const int qhc = tile_h_count(g, qtile), qwc = tile_w_count(g, qtile);
+    for (int t0 = 0; t0 < g.n_tiles; t0 += 32) {
+      const int t = t0 + lane;
+      bool a = false;
+      if (t < g.n_tiles) {
+        const int kth = t / g.tiles_w, ktw = t - kth * g.tiles_w;
+        a = range_overlap(m.mode, qh0, qhc, 8 * kth, tile_h_count(g, t), m.extent_h, g.rows) &&
+            range_overlap(m.mode, qw0, qwc, 8 * ktw, tile_w_count(g, t), m.extent_w, g.cols);
+      }
+      const unsigned w = __ballot_sync(0xffffffffu, a);
+      if (lane == 0) hist[t0 >> 5] = w;
+    }
+    __syncwarp();
+  }
 #pragma unroll
   for (int i = 0; i < NPER; ++i) {
     const int kb = 32 * i + lane;
     bool al = kb < bnk;
-    if (m.kind != 0 && al) {
+    if (loc_table) {
+      if (i > 0) {
+        kt += 32;
+        while (kt >= g.n_tiles) kt -= g.n_tiles;
+      }
+      al = al && ((hist[kt >> 5] >> (kt & 31)) & 1u);
+    } else if (m.kind != 0 && al) {
       const int ktr = kb / g.n_tiles, ktile = kb - ktr * g.n_tiles;
       al = coarse_allowed_masked(g, m, qtr, qtile, ktr, ktile);
     }
@@ -985,6 +1012,7 @@ __device__ __forceinline__ void topk_core(const DevGeom& g, const DevMask& m, co
     n_cand += __popc(__ballot_sync(0xffffffffu, os[i] != 0u));
   }
   if (!__any_sync(0xffffffffu, dg_ok)) dg = -1;
+  if (loc_table) __syncwarp();  // the table's reads before the radix histogram reuses its space
   const long long kp64 = p.topk - (dg >= 0 ? 1 : 0);
   const int kprime = kp64 > (long long)INT32_MAX ? INT32_MAX : (int)kp64;
   uint32_t T = 1u;  // every candidate
