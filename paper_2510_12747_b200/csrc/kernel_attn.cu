@@ -965,10 +965,17 @@ __global__ void __launch_bounds__(AttnCfg<D, NQ>::kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 16; ++i) pk[16 * w + i] = 0u;
               } else {
-                if (kFixed && mw == 0xffffffffu) {
-                  // references fixed at 0, every key allowed: d = s * scale * log2(e)
+                if (kFixed && (MK != 0 || mw == 0xffffffffu)) {
+                  // references fixed at 0: d = s * scale * log2(e) in packed pairs; with a token
+                  // mask a partially allowed word then sends its masked columns to -inf (exp 0).
+                  // (All-allowed units keep the select-in-FFMA form below for edge-tile words:
+                  // the hot loop of the headline compiles best that way.)
 #pragma unroll
                   for (int i = 0; i < 16; ++i) fmul2(d[2 * i], d[2 * i + 1], sl2);
+                  if (MK != 0 && mw != 0xffffffffu) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) d[i] = ((mw >> i) & 1u) ? d[i] : -INFINITY;
+                  }
                 } else {
 #pragma unroll
                   for (int i = 0; i < 32; i += 4) {
