@@ -7,7 +7,7 @@ import pytest
 import torch
 
 import oracle
-from tests.helpers import MAX_ABS_TOL, REL_L2_TOL, max_abs, qkv, rel_l2, to_dev, to_oracle_mask
+from tests.helpers import MAX_ABS_TOL, REL_L2_TOL, max_abs, oracle_outs, oracle_plans, qkv, rel_l2, to_dev, to_oracle_mask
 
 pytestmark = pytest.mark.gpu
 
@@ -140,3 +140,36 @@ def test_fused_step_matches_oracle_768x1408():
                                                         plans[h], oracle.head_scale(d)), range(heads)))
     got = out.float().cpu().numpy()
     assert rel_l2(got, ref) <= REL_L2_TOL and max_abs(got, ref) <= MAX_ABS_TOL
+
+
+def test_ring_step_over_1024_key_blocks():
+    """A ring context with more than 1024 key blocks (13 frames of 8x20 tiles: 7 temporal rows x
+    160 tiles = 1120) runs the selector's widest instantiation (NPER = 128 candidates per lane,
+    four key blocks per thread): selections exact and outputs within tolerance of the oracle."""
+    heads, rows, cols, d, topk, window = 1, 64, 160, 64, 20, 12
+    N = rows * cols
+    ring = fv.KVRing(1, heads, d, rows, cols, window)
+    port = oracle.Port()
+    store = {}
+    for t in range(window + 1):
+        x = oracle.bf16_round(port.gaussian(3100 + t, 3 * N * d).reshape(3, 1, N, d))
+        store[t] = x
+        q, k, v = to_dev(x[0]), to_dev(x[1]), to_dev(x[2])
+        ids = ring.frame_ids(0) + [t]
+        if t < window:
+            ring.append(0, t, k, v)
+            continue
+        bnq, bnk = fv.block_counts(fv.TokenGrid([t], rows, cols), fv.TokenGrid(ids, rows, cols))
+        assert bnk > 1024
+        sel = torch.empty((heads, bnq, topk), dtype=torch.int32, device="cuda")
+        cnt = torch.empty((heads, bnq), dtype=torch.int32, device="cuda")
+        out = ring.step(0, t, k, v, q, [t], fv.Mask.all_allowed(), topk, sel=sel, sel_count=cnt)
+        out = out.float().cpu().numpy()
+        K = np.concatenate([store[i][1] for i in ids], axis=1)
+        V = np.concatenate([store[i][2] for i in ids], axis=1)
+        Q = store[t][0]
+        plans = oracle_plans(Q, K, [t], ids, rows, cols, oracle.Mask.all(), topk)
+        assert np.array_equal(sel[0].cpu().numpy()[:, : plans[0].sel.shape[1]], plans[0].sel)
+        assert np.array_equal(cnt[0].cpu().numpy(), plans[0].count)
+        ref = oracle_outs(Q, K, V, [t], ids, rows, cols, oracle.Mask.all(), plans, oracle.head_scale(d))
+        assert rel_l2(out, ref) <= REL_L2_TOL and max_abs(out, ref) <= MAX_ABS_TOL
