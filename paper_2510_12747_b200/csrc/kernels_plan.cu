@@ -1097,10 +1097,10 @@ __global__ void __launch_bounds__(kTopkWarps * 32) topk_select_kernel(const __gr
 // ---------------------------------------------------------------------------------------
 // Streaming front end of one layer-step (ring append + mask builder) in two launches:
 //   ring_pack_kernel   blocks [0, heads*n_tiles): KVCache::append of the new frame's K tile
-//                      (swizzled ring slot, pooled partials, |k| bounds); the next heads*n_tiles
-//                      blocks: its V tile (swizzled ring slot only); the blocks after that: the
-//                      query frames' tiles (packed for the tensor cores, pooled partials, |q|
-//                      bounds).  Independent inputs, one pass over HBM; one 16 KB tile per block
+//                      (swizzled ring slot, pooled partials, |k| bounds); then the query
+//                      frames' tiles (packed for the tensor cores, pooled partials, |q|
+//                      bounds); the last heads*n_tiles blocks: the new frame's V tile
+//                      (swizzled ring slot only).  Independent inputs, one pass over HBM; one 16 KB tile per block
 //                      keeps ~13 blocks (208 KB of loads in flight) on every SM.
 //   mask_select_kernel kFrontQB q-blocks of one head per block: pooled queries, coarse scores
 //                      against the ring's pooled keys streamed through shared memory in
@@ -1143,21 +1143,23 @@ __global__ void __launch_bounds__(kPPThreads, 12) ring_pack_kernel(const __grid_
       else pack_pool_body<false>(a, pg, sl, tile, grp, head, sm_rp);
     }
   };
+  // K tiles, then query tiles (both pool and bound), then V tiles (copy only) last: the
+  // launch's last partial wave is then made of the cheapest blocks
   if (b < n_append) {
     const int head = b / fa.n_tiles;
     run(fa.kv, fa.kv_pg, fa.kv_sl, b - head * fa.n_tiles, 0, head, true);
     return;
   }
   b -= n_append;
-  if (b < n_append) {  // V: never rotated
-    const int head = b / fa.n_tiles;
-    run(fa.v, fa.kv_pg, fa.kv_sl, b - head * fa.n_tiles, 0, head, false);
+  const int per_head = fa.q_trows * fa.n_tiles;
+  if (b < fa.heads * per_head) {
+    const int head = b / per_head, rem = b - head * per_head, qtr = rem / fa.n_tiles;
+    run(fa.q, fa.q_pg, fa.q_sl, rem - qtr * fa.n_tiles, qtr, head, true);
     return;
   }
-  b -= n_append;
-  const int per_head = fa.q_trows * fa.n_tiles;
-  const int head = b / per_head, rem = b - head * per_head, qtr = rem / fa.n_tiles;
-  run(fa.q, fa.q_pg, fa.q_sl, rem - qtr * fa.n_tiles, qtr, head, true);
+  b -= fa.heads * per_head;
+  const int head = b / fa.n_tiles;  // V: never rotated
+  run(fa.v, fa.kv_pg, fa.kv_sl, b - head * fa.n_tiles, 0, head, false);
 }
 
 inline size_t mask_select_smem(int d, int bnk) {
