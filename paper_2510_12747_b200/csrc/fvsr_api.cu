@@ -388,13 +388,6 @@ int after_launch(fvsr_ctx* ctx, cudaStream_t s, int nlaunch) {
 // FVSR_PDL=0 disables it (plain stream order).
 // Only the attention kernel (one persistent CTA per SM, long prologue) is launched this way:
 // small many-CTA kernels launched early pile onto the first SMs that free up.
-inline int pdl_mode() {
-  static const int mode = [] {
-    const char* e = std::getenv("FVSR_PDL");
-    return e ? std::atoi(e) : 1;  // 0 off, 1 attention only, 2 every kernel
-  }();
-  return mode;
-}
 template <typename... KArgs, typename... Args>
 cudaError_t launch_kp(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                       Args&&... args) {
@@ -407,7 +400,10 @@ cudaError_t launch_kp(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (pdl_mode() == 2 || (pdl && pdl_mode() == 1)) ? 1 : 0;
+  // programmatic dependent launch for the kernels that ask for it (the mask selector and the
+  // attention: their prologues overlap the predecessor's tail).  On every kernel it measured
+  // worse (139.3 vs 135.0 us per step): early-resident append blocks crowd the attention's tail.
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 template <typename... KArgs, typename... Args>
